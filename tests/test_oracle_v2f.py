@@ -1,0 +1,150 @@
+"""Pins for oracle O5-O9: digests, block scores, budgeted
+top-k via block-to-token mapping, attention over the
+selection and the LSE merge."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dynsplit_oracle as O
+from synth import generators as G
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+EX = json.load(open(os.path.join(GOLD, "v2f_examples.json")))
+
+
+def test_digest_examples():
+    ex = EX["digest_two_tokens"]
+    K = np.array(ex["keys"], float)[:, None, :]
+    kmax, kmin = O.digests(K, [0, 2])
+    assert kmax[0, 0].tolist() == ex["key_max"] and kmin[0, 0].tolist() == ex["key_min"]
+    kmax, kmin = O.digests(K, [0, 1, 2])          # singleton blocks
+    assert np.array_equal(kmax[0], K[:, 0]) and np.array_equal(kmin[0], K[:, 0])
+
+
+def test_digest_containment():
+    _, K, _ = G.decode_qkv(1, 700, 4, 2, 32)
+    starts = O.segment(G.tokens(1, 700), G.T7_IDS, G.T7_W10, 32, 14)
+    kmax, kmin = O.digests(K, starts)
+    for b in range(len(starts) - 1):
+        blk = K[starts[b]:starts[b + 1]].transpose(1, 0, 2)   # [H, n, d]
+        assert np.all(blk <= kmax[:, b, None, :]) and np.all(blk >= kmin[:, b, None, :])
+        assert np.all(np.any(blk == kmax[:, b, None, :], axis=1))
+        assert np.all(np.any(blk == kmin[:, b, None, :], axis=1))
+
+
+def test_block_score_special_cases_and_upper_bound():
+    q, K, _ = G.decode_qkv(2, 500, 4, 2, 32)
+    starts = O.segment(G.tokens(2, 500), G.T7_IDS, G.T7_W10, 32, 14)
+    kmax, kmin = O.digests(K, starts)
+    for h in range(4):
+        sc = O.block_scores(q[h], kmax[h // 2], kmin[h // 2])
+        for b in range(len(starts) - 1):
+            dots = K[starts[b]:starts[b + 1], h // 2, :].astype(np.float64) @ q[h].astype(np.float64)
+            assert sc[b] >= dots.max() - 1e-9           # S:281 upper bound
+    # singleton block -> exact q.k; zero query -> 0
+    k1 = K[:1, 0, :]
+    assert O.block_scores(q[0], k1, k1)[0] == pytest.approx(float(k1[0].astype(float) @ q[0].astype(float)), abs=1e-12)
+    assert np.all(O.block_scores(np.zeros(32), kmax[0], kmin[0]) == 0)
+
+
+@pytest.mark.parametrize("name", ["select_tie", "map_block_to_tokens"])
+def test_selection_examples(name):
+    ex = EX[name]
+    toks = O.select_tokens(ex["scores"], ex["block_starts"], ex["budget"])
+    sb, m, keep = O.selection_from_tokens(toks, ex["scores"], ex["block_starts"], ex["budget"])
+    assert (sb, m, keep) == (ex["sel_blocks"], ex["marginal"], ex["keep"])
+    if "tokens" in ex:
+        assert toks.tolist() == ex["tokens"]
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_token_sort_equals_block_fill(seed):
+    # S:301 / S:522: the materialised per-token stable sort equals an
+    # independent block-order fill, including integer scores with many ties.
+    r = G.rng(seed, 12)
+    S = int(r.integers(1, 600))
+    starts = O.segment(G.tokens(seed, S), G.T7_IDS, G.T7_W10, int(r.integers(4, 40)), 3)
+    nb = len(starts) - 1
+    scores = r.integers(-3, 4, size=nb).astype(float) if seed % 2 else r.standard_normal(nb)
+    budget = int(r.integers(1, S + 20))
+    toks = O.select_tokens(scores, starts, budget)
+    sb, m, keep = O.selection_from_tokens(toks, scores, starts, budget)
+    sb2, m2, keep2, toks2 = O.select_blocks_direct(scores, starts, budget)
+    assert (sb, m, keep) == (sb2, m2, keep2)
+    assert np.array_equal(toks, toks2)
+    assert len(toks) == min(budget, S)             # budget exactness
+    if budget >= S:
+        assert m == -1 and len(toks) == S
+
+
+def test_attention_matches_torch_sdpa():
+    q, K, V = G.decode_qkv(3, 400, 8, 2, 64)
+    scale = 1 / math.sqrt(64)
+    for h in range(8):
+        o, lse = O.dense_attention(q[h], K[:, h // 4], V[:, h // 4], scale)
+        qt = torch.tensor(q[h], dtype=torch.float64)[None, None, None, :]
+        kt = torch.tensor(K[:, h // 4], dtype=torch.float64)[None, None]
+        vt = torch.tensor(V[:, h // 4], dtype=torch.float64)[None, None]
+        ref = torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, scale=scale)[0, 0, 0].numpy()
+        assert np.allclose(o, ref, atol=1e-12)
+        lse_ref = torch.logsumexp(torch.tensor(K[:, h // 4], dtype=torch.float64) @ torch.tensor(q[h], dtype=torch.float64) * scale, 0).item()
+        assert lse == pytest.approx(lse_ref, abs=1e-12)
+
+
+def test_sparse_attention_special_cases():
+    q, K, V = G.decode_qkv(4, 300, 2, 1, 32)
+    sc = 1 / math.sqrt(32)
+    o, _ = O.sparse_attention(q[0], K[:, 0], V[:, 0], [17], sc)
+    assert np.array_equal(o, V[17, 0].astype(np.float64))
+    Keq = np.repeat(K[:1, 0], 300, axis=0)
+    o, lse = O.dense_attention(q[0], Keq, V[:, 0], sc)
+    assert np.allclose(o, V[:, 0].astype(np.float64).mean(0), atol=1e-12)
+    with pytest.raises(ValueError):
+        O.sparse_attention(q[0], K[:, 0], V[:, 0], [], sc)
+
+
+def test_masked_dense_equivalence():
+    # S:367 / S:402: attention over the selection equals dense attention with
+    # non-selected logits set to -inf (library SDPA with a boolean mask).
+    q, K, V = G.decode_qkv(5, 500, 4, 2, 64)
+    starts = O.segment(G.tokens(5, 500), G.T7_IDS, G.T7_W10, 32, 14)
+    res = O.decode_step(q, K, V, starts, 77)
+    for h in range(4):
+        mask = torch.zeros(1, 1, 1, 500, dtype=torch.bool)
+        mask[..., torch.tensor(res["tokens"][h])] = True
+        qt = torch.tensor(q[h], dtype=torch.float64)[None, None, None]
+        kt = torch.tensor(K[:, h // 2], dtype=torch.float64)[None, None]
+        vt = torch.tensor(V[:, h // 2], dtype=torch.float64)[None, None]
+        ref = torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, attn_mask=mask, scale=1 / 8)
+        assert np.allclose(res["o"][h], ref[0, 0, 0].numpy(), atol=1e-12)
+        assert len(res["tokens"][h]) == 77
+
+
+def test_full_budget_equals_dense():
+    q, K, V = G.decode_qkv(6, 256, 4, 4, 32)
+    starts = O.segment(G.tokens(6, 256), G.T7_IDS, G.T7_W10, 32, 14)
+    res = O.decode_step(q, K, V, starts, 10_000)
+    for h in range(4):
+        o, lse = O.dense_attention(q[h], K[:, h], V[:, h], 1 / math.sqrt(32))
+        assert np.allclose(res["o"][h], o, atol=1e-12) and res["lse"][h] == pytest.approx(lse, abs=1e-12)
+        assert res["marginal"][h] == -1
+
+
+def test_merge_of_splits_equals_one_pass():
+    q, K, V = G.decode_qkv(7, 333, 1, 1, 32)
+    sc = 1 / math.sqrt(32)
+    full_o, full_lse = O.dense_attention(q[0], K[:, 0], V[:, 0], sc)
+    r = G.rng(7, 13)
+    for _ in range(10):
+        cuts = sorted(set(r.integers(1, 333, size=int(r.integers(1, 6))).tolist()))
+        parts = np.split(np.arange(333), cuts)
+        os_, ls_ = zip(*[O.sparse_attention(q[0], K[:, 0], V[:, 0], p, sc) for p in parts])
+        # an empty part contributes lse = -inf
+        o, L = O.merge_partials(np.vstack(os_ + (np.zeros(32),)), np.array(ls_ + (-np.inf,)))
+        assert np.allclose(o, full_o, atol=1e-12) and L == pytest.approx(full_lse, abs=1e-12)
+    o, L = O.merge_partials(np.zeros((2, 32)), np.array([-np.inf, -np.inf]))
+    assert L == -np.inf and np.all(o == 0)
