@@ -1,0 +1,268 @@
+/*
+ * dynsplit.h -- C ABI of the B200-native DynSplit-KV hot path (libdynsplit.so).
+ *
+ * DynSplit-KV: arXiv 2602.03184 ("PAPER", cited P:<line> of
+ * /root/reference/PAPER.md).  Prefill block construction (Alg. 1 delimiter
+ * scoring, DD-Select segmentation, uniform page mapping + min/max key
+ * digests) and per-decode-step selection-driven sparse attention (block
+ * scoring, budgeted top-k through block-to-token mapping, split-K
+ * flash-decoding over the selected pages with a log-sum-exp merge).
+ *
+ * Conventions for every entry point
+ *  - Tensor pointers are DEVICE pointers owned by the caller unless the name
+ *    ends in _host.  The library allocates nothing and never synchronises the
+ *    host; all work is enqueued on `stream` (cudaStream_t passed as void*).
+ *  - Shapes come in a dynsplit_shape; layouts are C-contiguous, listed per
+ *    argument below.  "kv dtype" = shape->kv_dtype (bf16 or fp32) applies to
+ *    q, Qs, Ks, K, V, Kp, Vp and digests; scores, o and lse are always fp32.
+ *  - Host-detectable errors (null pointer, bad shape/config, dtype, too-small
+ *    workspace) return a status BEFORE anything is launched.  A launch failure
+ *    returns DYNSPLIT_ERR_CUDA (cudaGetLastError is consumed).
+ *  - Workspaces (`ws`) are sized by dynsplit_workspace_bytes(op, ...), must
+ *    be 256-byte aligned and zero-filled once before first use (the library
+ *    keeps its internal counters zeroed between calls).  A workspace may be
+ *    reused by consecutive calls on the same stream, never concurrently.
+ *  - Functions are stateless and thread-safe; every one is graph-capturable.
+ *  - Query head h reads KV head h / (Hq/Hkv) (GQA).  head_dim d must be 128.
+ *  - Symbol notation follows the paper: W, R, alpha (Alg. 1); C,
+ *    Delta, lambda (DD-Select); P = page size of the
+ *    uniform mapping (north star; V2F P:247-270).
+ */
+#ifndef DYNSPLIT_H_
+#define DYNSPLIT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DYNSPLIT_OK = 0,
+  DYNSPLIT_ERR_INVALID_ARGUMENT = 1,   /* null pointer, budget < 1, Delta >= C, ... */
+  DYNSPLIT_ERR_DIMENSION_MISMATCH = 2, /* Hq % Hkv != 0, d != 128, Hq/Hkv > 8 */
+  DYNSPLIT_ERR_EMPTY_SEQUENCE = 3,     /* S < 1 or B < 1 */
+  DYNSPLIT_ERR_WORKSPACE_TOO_SMALL = 4,
+  DYNSPLIT_ERR_UNSUPPORTED = 5,        /* dtype / size outside what the kernels implement */
+  DYNSPLIT_ERR_CUDA = 6
+} dynsplit_status;
+
+typedef enum { DYNSPLIT_BF16 = 0, DYNSPLIT_FP32 = 1 } dynsplit_dtype;
+
+typedef enum {
+  DYNSPLIT_OP_SCORE_DELIMITERS = 0,
+  DYNSPLIT_OP_SEGMENT = 1,
+  DYNSPLIT_OP_BUILD_BLOCKS = 2,
+  DYNSPLIT_OP_SELECT = 3,
+  DYNSPLIT_OP_DECODE_ATTN = 4
+} dynsplit_op;
+
+typedef struct {
+  int32_t B;               /* sequences in the batch */
+  int32_t S;               /* context length (tokens per sequence) */
+  int32_t Hq, Hkv;         /* query / KV heads; g = Hq/Hkv in {1,2,4,8} */
+  int32_t d;               /* head dim, must be 128 */
+  int32_t n_score_layers;  /* Ls: layers averaged by Alg.1's E_{l,h,q} */
+  int32_t kv_dtype;        /* dynsplit_dtype */
+} dynsplit_shape;
+
+typedef struct {
+  int32_t W;               /* future window, Alg.1 line 3; paper 8 */
+  int32_t R;               /* overlap size, Alg.1 lines 4-5; paper 128 */
+  float alpha_pen;         /* long-range penalty alpha, Alg.1 line 8; paper 1 */
+  int32_t C;               /* base chunk size; default 32 (DESIGN.md R-C) */
+  int32_t delta;           /* maximum deviation Delta; 14 */
+  int32_t lambda_num;      /* DD-Select mix lambda = num/den ("alpha"); 1/2 */
+  int32_t lambda_den;
+  int32_t page_size;       /* P: fixed page length of the uniform mapping; 16 */
+} dynsplit_config;
+
+/* Fills the defaults above. */
+void dynsplit_default_config(dynsplit_config* cfg);
+
+/* Upper bound on blocks of one sequence: floor(S/(C-Delta)) + 1 (every
+ * non-final DD-Select chunk has >= C-Delta tokens). */
+int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* cfg);
+/* Upper bound on pages of one sequence: max_blocks + ceil(S/P). */
+int32_t dynsplit_max_pages(int32_t S, const dynsplit_config* cfg);
+/* Upper bound on blocks one head selects under `budget` tokens. */
+int32_t dynsplit_max_selected(int32_t budget, int32_t S, const dynsplit_config* cfg);
+/* Bytes of the opaque worklist produced by dynsplit_select. */
+size_t dynsplit_worklist_bytes(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                               int32_t budget);
+/* Bytes of workspace needed by `op` (a dynsplit_op).  0 on invalid input. */
+size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* shape,
+                                const dynsplit_config* cfg, int32_t budget);
+const char* dynsplit_status_string(int32_t status);
+const char* dynsplit_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Prefill, row a1: delimiter importance scoring, Algorithm 1 with
+ * the score of P:176-184.  For every position i whose token id is one of
+ * delim_ids (the semantic-boundary set B) and with a non-empty future
+ * window F_i = {i+1..min(i+W,S-1)}:
+ *   s_i = mean_{l<Ls, h<Hq, q in F_i} ( sum_{k in O_i} A_qk - alpha sum_{k in D_i} A_qk )
+ * O_i = {max(0,i-R+1)..i}, D_i = {0..i-R} (empty if i<R), A = causal
+ * softmax(Qs Ks^T / sqrt(d)).  Tensor cores compute the row log-sum-exps; the
+ * band of W+R keys is recomputed to obtain O_i and the future mass; D_i's
+ * mass is 1 - O - F.
+ *   tokens      int32 [B, S]
+ *   delim_ids   int32 [n_ids] (device), 1 <= n_ids <= 64
+ *   Qs          kv dtype [Ls, B, S, Hq, d];  Ks kv dtype [Ls, B, S, Hkv, d]
+ *   delim_scores (out) fp32 [B, S]; NaN where i is not a valid candidate.
+ * Workspace: DYNSPLIT_OP_SCORE_DELIMITERS.  bf16 only.
+ * ------------------------------------------------------------------------- */
+dynsplit_status dynsplit_score_delimiters(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                          const int32_t* tokens, const int32_t* delim_ids,
+                                          int32_t n_ids, const void* Qs, const void* Ks,
+                                          float* delim_scores, void* ws, size_t ws_bytes,
+                                          void* stream);
+
+/* Prefill, row a2: per-token-id weights (Table 7).  For each
+ * id: mean of the valid s_i at its positions, min-max normalised over the ids
+ * present (a single id or equal means -> 1.0), rounded half-up to tenths.
+ * Ids without a valid score get 0.
+ *   delim_scores fp32 [B, S] (NaN = not a candidate) -> w10 (out) uint8 [B, n_ids] */
+dynsplit_status dynsplit_weight_table(const dynsplit_shape* shape, const int32_t* tokens,
+                                      const int32_t* delim_ids, int32_t n_ids,
+                                      const float* delim_scores, uint8_t* w10, void* stream);
+
+/* Prefill, row a3: DD-Select.  s_c = 0; s_e = s_c + C; if s_e >= S
+ * the last chunk is [s_c, S); otherwise e* = argmax over boundary tokens e in
+ * [s_e-Delta, s_e+Delta] intersect [s_c+1, S-1] of lambda*w_e + (1-lambda)*p_e,
+ * p_e = 1 - |e-s_e|/(Delta+1), evaluated as an exact integer key, ties to the
+ * smallest e, e* = s_e if there is none; emit [s_c, e*), s_c = e*.
+ *   w10           uint8 [B, n_ids] (weights in tenths, per sequence)
+ *   block_starts  (out) int32 [B, max_blocks+1]: starts, then S, then S-padding
+ *   n_blocks      (out) int32 [B]
+ * Workspace: DYNSPLIT_OP_SEGMENT. */
+dynsplit_status dynsplit_segment(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                 const int32_t* tokens, const int32_t* delim_ids, int32_t n_ids,
+                                 const uint8_t* w10, int32_t* block_starts, int32_t* n_blocks,
+                                 void* ws, size_t ws_bytes, void* stream);
+
+/* Prefill, row a4 (part 1): uniform mapping of blocks onto P-token pages.
+ * pages_b = ceil(len_b/P); page_first = exclusive scan (padded with n_pages);
+ * page_block[j] = owning block (-1 past n_pages); page_valid[j] =
+ * min(P, len_b - P*(j - page_first[b])) (0 past n_pages).
+ *   page_first int32 [B, max_blocks+1]; page_block int32 [B, max_pages];
+ *   page_valid int16 [B, max_pages]; n_pages int32 [B] */
+dynsplit_status dynsplit_map_pages(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                   const int32_t* block_starts, const int32_t* n_blocks,
+                                   int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                                   int32_t* n_pages, void* stream);
+
+/* Prefill, row a4 (part 2): repack one layer's K and V into pages and build the
+ * V2F digests (element-wise max and min of each block's keys).
+ * Token t of block b at offset o goes to page page_first[b] + o/P, slot o%P;
+ * padding slots are zeroed.
+ *   K, V     kv dtype [B, S, Hkv, d] (token-major, as produced by a model)
+ *   Kp, Vp   (out) kv dtype [B, Hkv, max_pages, P, d]
+ *   digests  (out) kv dtype [B, Hkv, max_blocks, 2, d]  ([..,0,:] = kmax, [..,1,:] = kmin) */
+dynsplit_status dynsplit_repack_digest(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                       const void* K, const void* V, const int32_t* block_starts,
+                                       const int32_t* n_blocks, const int32_t* page_first,
+                                       void* Kp, void* Vp, void* digests, void* stream);
+
+/* Prefill, rows a1-a4 for one layer's K/V.  static_w10 == NULL: dynamic mode
+ * (a1 scoring on Qs/Ks, a2 table, written to w10); else static mode (a host
+ * uint8 [n_ids] table broadcast to every sequence, e.g. Table 7).  Qs/Ks may
+ * be NULL in static mode; delim_scores may be NULL.  Then a3 (segment) and
+ * a4 (map + repack + digest).  Workspace: DYNSPLIT_OP_BUILD_BLOCKS. */
+dynsplit_status dynsplit_build_blocks(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                      const int32_t* tokens, const int32_t* delim_ids,
+                                      int32_t n_ids, const uint8_t* static_w10_host,
+                                      const void* Qs, const void* Ks, const void* K, const void* V,
+                                      uint8_t* w10, float* delim_scores, int32_t* block_starts,
+                                      int32_t* n_blocks, int32_t* page_first, int32_t* page_block,
+                                      int16_t* page_valid, int32_t* n_pages, void* Kp, void* Vp,
+                                      void* digests, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Decode, row a5: block scoring (V2F top-k block selection score):
+ *   scores[b,h,blk] = sum_j max(q_j kmax_j, q_j kmin_j)   for blk < n_blocks[b]
+ * (an upper bound of max_t q.k_t over the block).  One digest read serves the
+ * g query heads of a KV head.  fp32, fixed per-block reduction order.
+ *   q kv dtype [B, Hq, d]; digests as above; scores (out) fp32 [B, Hq, max_blocks] */
+dynsplit_status dynsplit_score_blocks(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                      const void* q, const void* digests, const int32_t* n_blocks,
+                                      float* scores, void* stream);
+
+/* Decode, row a6: budgeted top-k through block-to-token mapping (P:257-264,
+ * Step 1 P:749).  Per (b, query head): every token inherits its block's score;
+ * the top `budget` tokens by (score desc, token index asc) are taken.
+ * Equivalently blocks are visited by (score desc, index asc) and taken whole
+ * while the budget lasts; the block that reaches the budget ("marginal") keeps
+ * its first marginal_keep tokens.  If all tokens fit: marginal = -1, keep = 0.
+ * Only blocks in [blk_lo, blk_hi) compete (seq-split shards; pass 0 and
+ * INT32_MAX for the whole sequence); worklist page ids are then relative to
+ * page_first[b, blk_lo].
+ *   scores          fp32 [B, Hq, max_blocks]
+ *   sel_blocks      (out) int32 [B, Hq, max_sel] ascending block ids (may be NULL)
+ *   n_sel, marginal_block, marginal_keep (out) int32 [B, Hq]
+ *   worklist        (out) opaque, dynsplit_worklist_bytes(); union over the g
+ *                   heads of each KV head of the selected pages with per-head
+ *                   row counts, consumed by dynsplit_decode_attn.
+ * Workspace: DYNSPLIT_OP_SELECT. */
+dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                            int32_t budget, const float* scores,
+                                            const int32_t* block_starts, const int32_t* n_blocks,
+                                            const int32_t* page_first, int32_t blk_lo, int32_t blk_hi,
+                                            int32_t* sel_blocks, int32_t* n_sel,
+                                            int32_t* marginal_block, int32_t* marginal_keep,
+                                            void* worklist, void* ws, size_t ws_bytes, void* stream);
+
+/* Decode, rows a5+a6: dynsplit_score_blocks then dynsplit_select_from_scores
+ * over the whole sequence.  scores_out may be NULL (kept in the workspace). */
+dynsplit_status dynsplit_select(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                int32_t budget, const void* q, const void* digests,
+                                const int32_t* block_starts, const int32_t* n_blocks,
+                                const int32_t* page_first, float* scores_out, int32_t* sel_blocks,
+                                int32_t* n_sel, int32_t* marginal_block, int32_t* marginal_keep,
+                                void* worklist, void* ws, size_t ws_bytes, void* stream);
+
+/* Decode, rows a7+a8 (a9 when worklist == NULL): split-K flash-decoding over
+ * the worklist's pages (Step 3): per query head, z = q.k * scale over
+ * its selected rows, online softmax, o = sum p v; the split partials are
+ * merged by log-sum-exp in fixed split order.  worklist == NULL runs the
+ * dense baseline over every valid row of pages [0, n_pages[b]).
+ *   q kv dtype [B, Hq, d]; Kp, Vp [B, Hkv, max_pages, P, d]; page_valid int16
+ *   [B, max_pages]; n_pages int32 [B] (dense mode only, else may be NULL)
+ *   o (out) fp32 [B, Hq, d];  lse (out) fp32 [B, Hq] (natural log of the
+ *   softmax denominator of the scaled logits; -inf if nothing selected)
+ * Workspace: DYNSPLIT_OP_DECODE_ATTN. */
+dynsplit_status dynsplit_decode_attn(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                     const void* q, const void* Kp, const void* Vp,
+                                     const int16_t* page_valid, const int32_t* n_pages,
+                                     const void* worklist, float scale, float* o, float* lse,
+                                     void* ws, size_t ws_bytes, void* stream);
+
+/* Row a8 standalone (cross-GPU merge of sequence-split shards):
+ *   o_parts fp32 [n_parts, rows, d], lse_parts fp32 [n_parts, rows] ->
+ *   lse = log sum_s exp(lse_s), o = sum_s exp(lse_s - lse) o_s, fixed part order. */
+dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_parts,
+                                        int32_t n_parts, int32_t rows, int32_t d, float* o,
+                                        float* lse, void* stream);
+
+/* One full decode step (a5-a8) with HOST query and outputs: copies q_host
+ * (pinned, kv dtype [B, Hq, d]) to the workspace, runs select + decode_attn,
+ * and copies o/lse back to o_host/lse_host (pinned).  Asynchronous like every
+ * other entry point: synchronise `stream` before reading o_host.
+ * Workspace: dynsplit_workspace_bytes(DYNSPLIT_OP_SELECT) +
+ * dynsplit_workspace_bytes(DYNSPLIT_OP_DECODE_ATTN) + q/o/lse staging
+ * (see dynsplit_step_host_workspace_bytes). */
+size_t dynsplit_step_host_workspace_bytes(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                          int32_t budget);
+dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                          int32_t budget, const void* q_host, const void* digests,
+                                          const int32_t* block_starts, const int32_t* n_blocks,
+                                          const int32_t* page_first, const void* Kp, const void* Vp,
+                                          const int16_t* page_valid, float scale, float* o_host,
+                                          float* lse_host, void* worklist, void* ws,
+                                          size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNSPLIT_H_ */

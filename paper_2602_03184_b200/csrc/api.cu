@@ -1,0 +1,443 @@
+// C ABI of libdynsplit.so (declared and documented in include/dynsplit.h).
+// Validation, workspace carving and launch sequencing only; every step of the
+// path runs in the kernels of decode_kernels.cu / build_kernels.cu /
+// score_kernels.cu.
+#include "../../include/dynsplit.h"
+#include "common.cuh"
+#include "kernels.h"
+
+#include <math.h>
+#include <string.h>
+
+namespace dsk {
+
+int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cached = n;
+  }
+  return cached;
+}
+
+}  // namespace dsk
+
+using namespace dsk;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+inline size_t esize(const dynsplit_shape* s) { return s->kv_dtype == DYNSPLIT_BF16 ? 2 : 4; }
+
+dynsplit_status check_shape(const dynsplit_shape* s) {
+  if (!s) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (s->B < 1 || s->S < 1) return DYNSPLIT_ERR_EMPTY_SEQUENCE;
+  if (s->Hq < 1 || s->Hkv < 1 || s->Hq % s->Hkv) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  const int g = s->Hq / s->Hkv;
+  if (g != 1 && g != 2 && g != 4 && g != 8) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  if (s->d != kD) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  if (s->kv_dtype != DYNSPLIT_BF16 && s->kv_dtype != DYNSPLIT_FP32) return DYNSPLIT_ERR_UNSUPPORTED;
+  return DYNSPLIT_OK;
+}
+
+dynsplit_status check_cfg(const dynsplit_config* c) {
+  if (!c) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->C < 1 || c->delta < 0 || c->delta >= c->C) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->C + c->delta > 65535) return DYNSPLIT_ERR_UNSUPPORTED;
+  if (c->lambda_den < 1 || c->lambda_num < 0 || c->lambda_num > c->lambda_den)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->page_size < 1 || c->page_size > 64) return DYNSPLIT_ERR_UNSUPPORTED;
+  if (c->W < 1 || c->R < 1 || !(c->alpha_pen >= 0.f)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return DYNSPLIT_OK;
+}
+
+inline dynsplit_status cuda_status(cudaError_t e) {
+  return e == cudaSuccess ? DYNSPLIT_OK : DYNSPLIT_ERR_CUDA;
+}
+
+#define DSK_TRY(x)                               \
+  do {                                           \
+    dynsplit_status _s = (x);                    \
+    if (_s != DYNSPLIT_OK) return _s;            \
+  } while (0)
+
+inline int max_wl_of(const dynsplit_shape* s, const dynsplit_config* c, int budget) {
+  const int g = s->Hq / s->Hkv;
+  const int maxp = dynsplit_max_pages(s->S, c);
+  const long long per_head = (long long)budget / c->page_size + dynsplit_max_selected(budget, s->S, c) + 1;
+  const long long v = (long long)g * per_head;
+  return (int)(v < maxp ? v : maxp);
+}
+
+struct WorklistView {
+  int32_t* hdr;
+  int32_t* count;
+  WLEntry* entries;
+};
+inline WorklistView worklist_view(void* wl, const dynsplit_shape* s) {
+  char* p = static_cast<char*>(wl);
+  WorklistView v;
+  v.hdr = reinterpret_cast<int32_t*>(p);
+  v.count = v.hdr + 64;
+  v.entries = reinterpret_cast<WLEntry*>(p + kAlign + align_up((size_t)s->B * s->Hkv * 4));
+  return v;
+}
+
+size_t select_ws(const dynsplit_shape* s, const dynsplit_config* c) {
+  const int maxb = dynsplit_max_blocks(s->S, c);
+  return align_up((size_t)s->B * s->Hq * maxb * 4) + align_up((size_t)s->B * s->Hq * 16);
+}
+size_t decode_ws(const dynsplit_shape* s) {
+  return align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4) +
+         align_up((size_t)s->B * s->Hq * kMaxSplit * 4) + align_up((size_t)s->B * s->Hkv * 4);
+}
+size_t segment_ws(const dynsplit_shape* s) { return align_up((size_t)s->B * s->S * 4); }
+size_t score_ws(const dynsplit_shape* s) {
+  return align_up(score_ws_bytes(s->n_score_layers, s->B, s->S, s->Hq));
+}
+size_t build_ws(const dynsplit_shape* s) {
+  // scoring partials + delim scores (if not returned) + segment next[]
+  return score_ws(s) + align_up((size_t)s->B * s->S * 4) + segment_ws(s);
+}
+size_t step_host_extra(const dynsplit_shape* s) {
+  return align_up((size_t)s->B * s->Hq * kD * esize(s)) + align_up((size_t)s->B * s->Hq * kD * 4) +
+         align_up((size_t)s->B * s->Hq * 4) + 3 * align_up((size_t)s->B * s->Hq * 4);
+}
+
+struct W10Table {
+  uint8_t w[64];
+};
+__global__ void k_fill_w10(W10Table t, int n_ids, uint8_t* w10) {
+  if (threadIdx.x < n_ids) w10[(size_t)blockIdx.x * n_ids + threadIdx.x] = t.w[threadIdx.x];
+}
+
+}  // namespace
+
+extern "C" {
+
+void dynsplit_default_config(dynsplit_config* c) {
+  if (!c) return;
+  c->W = 8;
+  c->R = 128;
+  c->alpha_pen = 1.0f;
+  c->C = 32;
+  c->delta = 14;
+  c->lambda_num = 1;
+  c->lambda_den = 2;
+  c->page_size = 16;
+}
+
+int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* c) {
+  if (!c || c->C - c->delta < 1 || S < 0) return 0;
+  return S / (c->C - c->delta) + 1;
+}
+
+int32_t dynsplit_max_pages(int32_t S, const dynsplit_config* c) {
+  if (!c || c->page_size < 1) return 0;
+  return dynsplit_max_blocks(S, c) + (S + c->page_size - 1) / c->page_size;
+}
+
+int32_t dynsplit_max_selected(int32_t budget, int32_t S, const dynsplit_config* c) {
+  if (!c || c->C - c->delta < 1) return 0;
+  const int32_t maxb = dynsplit_max_blocks(S, c);
+  const long long v = (long long)(budget > 0 ? budget - 1 : 0) / (c->C - c->delta) + 2;
+  return (int32_t)(v < maxb ? v : maxb);
+}
+
+size_t dynsplit_worklist_bytes(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget) {
+  if (check_shape(s) != DYNSPLIT_OK || check_cfg(c) != DYNSPLIT_OK || budget < 1) return 0;
+  return kAlign + align_up((size_t)s->B * s->Hkv * 4) +
+         (size_t)s->B * s->Hkv * max_wl_of(s, c, budget) * sizeof(WLEntry);
+}
+
+size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* s, const dynsplit_config* c,
+                                int32_t budget) {
+  (void)budget;
+  if (check_shape(s) != DYNSPLIT_OK || check_cfg(c) != DYNSPLIT_OK) return 0;
+  switch (op) {
+    case DYNSPLIT_OP_SCORE_DELIMITERS: return score_ws(s);
+    case DYNSPLIT_OP_SEGMENT: return segment_ws(s);
+    case DYNSPLIT_OP_BUILD_BLOCKS: return build_ws(s);
+    case DYNSPLIT_OP_SELECT: return select_ws(s, c);
+    case DYNSPLIT_OP_DECODE_ATTN: return decode_ws(s);
+    default: return 0;
+  }
+}
+
+size_t dynsplit_step_host_workspace_bytes(const dynsplit_shape* s, const dynsplit_config* c,
+                                          int32_t budget) {
+  if (check_shape(s) != DYNSPLIT_OK || check_cfg(c) != DYNSPLIT_OK || budget < 1) return 0;
+  return select_ws(s, c) + decode_ws(s) + step_host_extra(s);
+}
+
+const char* dynsplit_status_string(int32_t st) {
+  switch (st) {
+    case DYNSPLIT_OK: return "ok";
+    case DYNSPLIT_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case DYNSPLIT_ERR_DIMENSION_MISMATCH: return "dimension mismatch";
+    case DYNSPLIT_ERR_EMPTY_SEQUENCE: return "empty sequence";
+    case DYNSPLIT_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case DYNSPLIT_ERR_UNSUPPORTED: return "unsupported";
+    case DYNSPLIT_ERR_CUDA: return "cuda error";
+    default: return "unknown status";
+  }
+}
+
+const char* dynsplit_version(void) { return "dynsplit-b200 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------ prefill
+dynsplit_status dynsplit_score_delimiters(const dynsplit_shape* s, const dynsplit_config* c,
+                                          const int32_t* tokens, const int32_t* delim_ids,
+                                          int32_t n_ids, const void* Qs, const void* Ks,
+                                          float* out, void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!tokens || !delim_ids || !Qs || !Ks || !out || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_ids < 1 || n_ids > 64 || s->n_score_layers < 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (s->kv_dtype != DYNSPLIT_BF16 || c->W > 8) return DYNSPLIT_ERR_UNSUPPORTED;
+  if (ws_bytes < score_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(launch_score_delimiters(tokens, delim_ids, n_ids, Qs, Ks, s->n_score_layers,
+                                             s->B, s->S, s->Hq, s->Hkv, c->W, c->R, c->alpha_pen,
+                                             out, ws, static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_weight_table(const dynsplit_shape* s, const int32_t* tokens,
+                                      const int32_t* delim_ids, int32_t n_ids,
+                                      const float* delim_scores, uint8_t* w10, void* stream) {
+  DSK_TRY(check_shape(s));
+  if (!tokens || !delim_ids || !delim_scores || !w10) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_ids < 1 || n_ids > 64) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(launch_weight_table(tokens, delim_ids, n_ids, delim_scores, w10, s->B, s->S,
+                                         static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_segment(const dynsplit_shape* s, const dynsplit_config* c,
+                                 const int32_t* tokens, const int32_t* delim_ids, int32_t n_ids,
+                                 const uint8_t* w10, int32_t* block_starts, int32_t* n_blocks,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!tokens || !delim_ids || !w10 || !block_starts || !n_blocks || !ws)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_ids < 1 || n_ids > 64) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < segment_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(launch_segment(tokens, delim_ids, n_ids, w10, s->B, s->S, c->C, c->delta,
+                                    c->lambda_num, c->lambda_den, dynsplit_max_blocks(s->S, c),
+                                    static_cast<int32_t*>(ws), block_starts, n_blocks,
+                                    static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_map_pages(const dynsplit_shape* s, const dynsplit_config* c,
+                                   const int32_t* block_starts, const int32_t* n_blocks,
+                                   int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                                   int32_t* n_pages, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!block_starts || !n_blocks || !page_first || !page_block || !page_valid || !n_pages)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(launch_map_pages(block_starts, n_blocks, s->B, dynsplit_max_blocks(s->S, c),
+                                      dynsplit_max_pages(s->S, c), c->page_size, page_first,
+                                      page_block, page_valid, n_pages,
+                                      static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_repack_digest(const dynsplit_shape* s, const dynsplit_config* c,
+                                       const void* K, const void* V, const int32_t* block_starts,
+                                       const int32_t* n_blocks, const int32_t* page_first,
+                                       void* Kp, void* Vp, void* digests, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!K || !V || !block_starts || !n_blocks || !page_first || !Kp || !Vp || !digests)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(launch_repack_digest(s->kv_dtype, K, V, block_starts, n_blocks, page_first,
+                                          s->B, s->S, s->Hkv, dynsplit_max_blocks(s->S, c),
+                                          dynsplit_max_pages(s->S, c), c->page_size, Kp, Vp,
+                                          digests, static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_build_blocks(const dynsplit_shape* s, const dynsplit_config* c,
+                                      const int32_t* tokens, const int32_t* delim_ids,
+                                      int32_t n_ids, const uint8_t* static_w10_host,
+                                      const void* Qs, const void* Ks, const void* K, const void* V,
+                                      uint8_t* w10, float* delim_scores, int32_t* block_starts,
+                                      int32_t* n_blocks, int32_t* page_first, int32_t* page_block,
+                                      int16_t* page_valid, int32_t* n_pages, void* Kp, void* Vp,
+                                      void* digests, void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!tokens || !delim_ids || !w10 || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_ids < 1 || n_ids > 64) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < build_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  void* score_part = w;
+  float* tmp_scores = reinterpret_cast<float*>(w + score_ws(s));
+  int32_t* next_ws = reinterpret_cast<int32_t*>(w + score_ws(s) + align_up((size_t)s->B * s->S * 4));
+  if (static_w10_host) {
+    W10Table t;
+    memset(&t, 0, sizeof(t));
+    memcpy(t.w, static_w10_host, (size_t)n_ids);
+    k_fill_w10<<<s->B, 64, 0, st>>>(t, n_ids, w10);
+    if (cudaGetLastError() != cudaSuccess) return DYNSPLIT_ERR_CUDA;
+  } else {
+    if (!Qs || !Ks) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+    float* sc = delim_scores ? delim_scores : tmp_scores;
+    DSK_TRY(dynsplit_score_delimiters(s, c, tokens, delim_ids, n_ids, Qs, Ks, sc, score_part,
+                                      score_ws(s), stream));
+    DSK_TRY(dynsplit_weight_table(s, tokens, delim_ids, n_ids, sc, w10, stream));
+  }
+  DSK_TRY(dynsplit_segment(s, c, tokens, delim_ids, n_ids, w10, block_starts, n_blocks, next_ws,
+                           segment_ws(s), stream));
+  DSK_TRY(dynsplit_map_pages(s, c, block_starts, n_blocks, page_first, page_block, page_valid,
+                             n_pages, stream));
+  if (K || V || Kp || Vp || digests)
+    DSK_TRY(dynsplit_repack_digest(s, c, K, V, block_starts, n_blocks, page_first, Kp, Vp, digests,
+                                   stream));
+  return DYNSPLIT_OK;
+}
+
+// ------------------------------------------------------------------ decode
+dynsplit_status dynsplit_score_blocks(const dynsplit_shape* s, const dynsplit_config* c,
+                                      const void* q, const void* digests, const int32_t* n_blocks,
+                                      float* scores, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!q || !digests || !n_blocks || !scores) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(launch_score_blocks(s->kv_dtype, s->Hq / s->Hkv, q, digests, n_blocks, scores,
+                                         s->B, s->Hq, s->Hkv, dynsplit_max_blocks(s->S, c),
+                                         static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* s, const dynsplit_config* c,
+                                            int32_t budget, const float* scores,
+                                            const int32_t* block_starts, const int32_t* n_blocks,
+                                            const int32_t* page_first, int32_t blk_lo,
+                                            int32_t blk_hi, int32_t* sel_blocks, int32_t* n_sel,
+                                            int32_t* marginal_block, int32_t* marginal_keep,
+                                            void* worklist, void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (budget < 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (!scores || !block_starts || !n_blocks || !page_first || !n_sel || !marginal_block ||
+      !marginal_keep || !worklist || !ws)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (blk_lo < 0 || blk_hi < blk_lo) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < select_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  const int maxb = dynsplit_max_blocks(s->S, c);
+  if (select_threshold_smem(maxb) > 227 * 1024) return DYNSPLIT_ERR_UNSUPPORTED;
+  char* w = static_cast<char*>(ws);
+  int4* sel_info = reinterpret_cast<int4*>(w + align_up((size_t)s->B * s->Hq * maxb * 4));
+  WorklistView v = worklist_view(worklist, s);
+  return cuda_status(launch_select(s->Hq / s->Hkv, scores, block_starts, n_blocks, page_first, s->B,
+                                   s->Hq, s->Hkv, maxb, dynsplit_max_selected(budget, s->S, c),
+                                   max_wl_of(s, c, budget), c->page_size, budget, blk_lo, blk_hi,
+                                   sel_info, sel_blocks, n_sel, marginal_block, marginal_keep,
+                                   v.count, v.entries, static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_select(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,
+                                const void* q, const void* digests, const int32_t* block_starts,
+                                const int32_t* n_blocks, const int32_t* page_first,
+                                float* scores_out, int32_t* sel_blocks, int32_t* n_sel,
+                                int32_t* marginal_block, int32_t* marginal_keep, void* worklist,
+                                void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < select_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  float* sc = scores_out ? scores_out : static_cast<float*>(ws);
+  DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
+  return dynsplit_select_from_scores(s, c, budget, sc, block_starts, n_blocks, page_first, 0,
+                                     0x7fffffff, sel_blocks, n_sel, marginal_block, marginal_keep,
+                                     worklist, ws, ws_bytes, stream);
+}
+
+dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_config* c,
+                                     const void* q, const void* Kp, const void* Vp,
+                                     const int16_t* page_valid, const int32_t* n_pages,
+                                     const void* worklist, float scale, float* o, float* lse,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!q || !Kp || !Vp || !o || !lse || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  const int dense = worklist == nullptr;
+  if (dense && (!n_pages || !page_valid)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < decode_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)kD);
+  char* w = static_cast<char*>(ws);
+  float* part_o = reinterpret_cast<float*>(w);
+  float* part_lse = reinterpret_cast<float*>(w + align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4));
+  int* counters = reinterpret_cast<int*>(w + align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4) +
+                                         align_up((size_t)s->B * s->Hq * kMaxSplit * 4));
+  const int32_t* hdr = nullptr;
+  const int32_t* cnt = nullptr;
+  const WLEntry* ent = nullptr;
+  if (!dense) {
+    WorklistView v = worklist_view(const_cast<void*>(worklist), s);
+    hdr = v.hdr;
+    cnt = v.count;
+    ent = v.entries;
+  }
+  const int n_split = decode_n_split(s->B, s->Hkv);
+  return cuda_status(launch_decode_attn(s->kv_dtype, s->Hq / s->Hkv, q, Kp, Vp, page_valid, n_pages,
+                                        hdr, cnt, ent, dense, s->B, s->Hq, s->Hkv,
+                                        dynsplit_max_pages(s->S, c), c->page_size, scale, part_o,
+                                        part_lse, counters, n_split, o, lse,
+                                        static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_parts,
+                                        int32_t n_parts, int32_t rows, int32_t d, float* o,
+                                        float* lse, void* stream) {
+  if (!o_parts || !lse_parts || !o || !lse || n_parts < 1 || rows < 1 || d < 1)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(launch_merge(o_parts, lse_parts, n_parts, rows, d, o, lse,
+                                  static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* s, const dynsplit_config* c,
+                                          int32_t budget, const void* q_host, const void* digests,
+                                          const int32_t* block_starts, const int32_t* n_blocks,
+                                          const int32_t* page_first, const void* Kp, const void* Vp,
+                                          const int16_t* page_valid, float scale, float* o_host,
+                                          float* lse_host, void* worklist, void* ws,
+                                          size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!q_host || !o_host || !lse_host || !ws || !worklist) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < dynsplit_step_host_workspace_bytes(s, c, budget))
+    return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  char* ws_sel = w;
+  char* ws_dec = w + select_ws(s, c);
+  char* extra = ws_dec + decode_ws(s);
+  const size_t qbytes = (size_t)s->B * s->Hq * kD * esize(s);
+  void* q_dev = extra;
+  float* o_dev = reinterpret_cast<float*>(extra + align_up(qbytes));
+  float* lse_dev = reinterpret_cast<float*>(extra + align_up(qbytes) + align_up((size_t)s->B * s->Hq * kD * 4));
+  int32_t* nsel = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(lse_dev) + align_up((size_t)s->B * s->Hq * 4));
+  int32_t* marg = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(nsel) + align_up((size_t)s->B * s->Hq * 4));
+  int32_t* keep = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(marg) + align_up((size_t)s->B * s->Hq * 4));
+  if (cudaMemcpyAsync(q_dev, q_host, qbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return DYNSPLIT_ERR_CUDA;
+  DSK_TRY(dynsplit_select(s, c, budget, q_dev, digests, block_starts, n_blocks, page_first, nullptr,
+                          nullptr, nsel, marg, keep, worklist, ws_sel, select_ws(s, c), stream));
+  DSK_TRY(dynsplit_decode_attn(s, c, q_dev, Kp, Vp, page_valid, nullptr, worklist, scale, o_dev,
+                               lse_dev, ws_dec, decode_ws(s), stream));
+  if (cudaMemcpyAsync(o_host, o_dev, (size_t)s->B * s->Hq * kD * 4, cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(lse_host, lse_dev, (size_t)s->B * s->Hq * 4, cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess)
+    return DYNSPLIT_ERR_CUDA;
+  return DYNSPLIT_OK;
+}
+
+}  // extern "C"

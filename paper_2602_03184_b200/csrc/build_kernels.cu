@@ -1,0 +1,382 @@
+// Prefill block-construction kernels of the DynSplit-KV hot path (sm_100a).
+//   a2  k_weight_table     per-id mean -> min-max -> tenths            (T7 P:720-736)
+//   a3  k_dd_next          DD-Select e*(s) for every start s in parallel
+//       k_dd_walk          follow s -> e*(s) from 0 (one thread, smem windows)
+//   a4  k_map_pages        uniform mapping: page_first/page_block/page_valid
+//       k_repack_digest    K,V -> fixed P-token pages + per-block kmax/kmin
+#include "common.cuh"
+#include "kernels.h"
+
+#include <math_constants.h>
+
+namespace dsk {
+
+// ============================================================================
+// a2: weight table.  grid (B), 256 threads.  Per id: sum of the valid s_i in
+// fp64 (each thread a contiguous position range, then a fixed-order tree),
+// count; then mean, min-max over ids present, round half-up to tenths.
+// ============================================================================
+__global__ void __launch_bounds__(256) k_weight_table(const int32_t* __restrict__ tokens,
+                                                      const int32_t* __restrict__ delim_ids, int n_ids,
+                                                      const float* __restrict__ s, uint8_t* __restrict__ w10,
+                                                      int S) {
+  __shared__ double red_s[256];
+  __shared__ int red_c[256];
+  __shared__ double means[64];
+  __shared__ int cnts[64];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int chunk = (S + 255) / 256;
+  const int p0 = tid * chunk, p1 = min(S, p0 + chunk);
+  const int32_t* tk = tokens + (size_t)b * S;
+  const float* sb = s + (size_t)b * S;
+  for (int j = 0; j < n_ids; ++j) {
+    const int id = delim_ids[j];
+    double acc = 0.0;
+    int c = 0;
+    for (int p = p0; p < p1; ++p) {
+      if (tk[p] == id) {
+        const float v = sb[p];
+        if (!isnan(v)) {
+          acc += (double)v;
+          ++c;
+        }
+      }
+    }
+    red_s[tid] = acc;
+    red_c[tid] = c;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+      if (tid < st) {
+        red_s[tid] += red_s[tid + st];
+        red_c[tid] += red_c[tid + st];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      cnts[j] = red_c[0];
+      means[j] = red_c[0] ? red_s[0] / (double)red_c[0] : 0.0;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    bool any = false;
+    double lo = 0.0, hi = 0.0;
+    for (int j = 0; j < n_ids; ++j) {
+      if (!cnts[j]) continue;
+      if (!any || means[j] < lo) lo = means[j];
+      if (!any || means[j] > hi) hi = means[j];
+      any = true;
+    }
+    for (int j = 0; j < n_ids; ++j) {
+      int w = 0;
+      if (cnts[j]) {
+        const double ww = (hi == lo) ? 1.0 : (means[j] - lo) / (hi - lo);
+        w = (int)floor(10.0 * ww + 0.5);
+      }
+      w10[(size_t)b * n_ids + j] = (uint8_t)w;
+    }
+  }
+}
+
+// ============================================================================
+// a3 (part 1): e*(s) for every s (the DD-Select step depends only on s_c).
+// Exact integer key for lambda*w_e + (1-lambda)*p_e scaled by
+// lam_den*10*(Delta+1):  lam_num*w10*(D+1) + (lam_den-lam_num)*10*(D+1-|e-s_e|).
+// Ties -> smallest e (strict >).  grid (ceil(S/256), B), 256 threads.
+// ============================================================================
+__global__ void __launch_bounds__(256) k_dd_next(const int32_t* __restrict__ tokens,
+                                                 const int32_t* __restrict__ delim_ids, int n_ids,
+                                                 const uint8_t* __restrict__ w10, int S, int C,
+                                                 int delta, int lam_num, int lam_den,
+                                                 int32_t* __restrict__ next) {
+  __shared__ int s_ids[64];
+  __shared__ int s_w[64];
+  const int b = blockIdx.y;
+  if (threadIdx.x < n_ids) {
+    s_ids[threadIdx.x] = delim_ids[threadIdx.x];
+    s_w[threadIdx.x] = w10[(size_t)b * n_ids + threadIdx.x];
+  }
+  __syncthreads();
+  const int s = blockIdx.x * 256 + threadIdx.x;
+  if (s >= S) return;
+  const int32_t* tk = tokens + (size_t)b * S;
+  const int s_e = s + C;
+  int nxt;
+  if (s_e >= S) {
+    nxt = S;
+  } else {
+    const int lo = max(s_e - delta, s + 1), hi = min(s_e + delta, S - 1);
+    long long best = -1;
+    nxt = s_e;
+    for (int e = lo; e <= hi; ++e) {
+      const int t = __ldg(tk + e);
+      int w = -1;
+      for (int j = 0; j < n_ids; ++j)
+        if (s_ids[j] == t) {
+          w = s_w[j];
+          break;
+        }
+      if (w >= 0) {
+        const int dist = abs(e - s_e);
+        const long long key = (long long)lam_num * w * (delta + 1) +
+                              (long long)(lam_den - lam_num) * 10 * (delta + 1 - dist);
+        if (key > best) {
+          best = key;
+          nxt = e;
+        }
+      }
+    }
+  }
+  next[(size_t)b * S + s] = nxt;
+}
+
+// ============================================================================
+// a3 (part 2): walk the chain 0 -> e*(0) -> ... (serial by nature, ~S/C
+// steps).  The chain only moves forward, so windows of next[] are staged in
+// smem as 16-bit deltas and thread 0 walks each window.  grid (B), 1024 threads.
+// ============================================================================
+constexpr int kWalkWin = 16384;
+
+__global__ void __launch_bounds__(1024) k_dd_walk(const int32_t* __restrict__ next, int S, int maxb,
+                                                  int32_t* __restrict__ block_starts,
+                                                  int32_t* __restrict__ n_blocks) {
+  __shared__ uint16_t sd[kWalkWin];
+  __shared__ int s_pos, s_n;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int32_t* nx = next + (size_t)b * S;
+  int32_t* bs = block_starts + (size_t)b * (maxb + 1);
+  if (tid == 0) {
+    s_pos = 0;
+    s_n = 0;
+  }
+  __syncthreads();
+  while (s_pos < S) {
+    const int w0 = s_pos;
+    const int wend = min(S, w0 + kWalkWin);
+    for (int i = tid; i < wend - w0; i += 1024) sd[i] = (uint16_t)min(65535, nx[w0 + i] - (w0 + i));
+    __syncthreads();
+    if (tid == 0) {
+      int pos = s_pos, n = s_n;
+      while (pos < wend) {
+        bs[n++] = pos;
+        pos += sd[pos - w0];
+      }
+      s_pos = pos;
+      s_n = n;
+    }
+    __syncthreads();
+  }
+  const int n = s_n;
+  for (int i = n + tid; i <= maxb; i += 1024) bs[i] = S;
+  if (tid == 0) n_blocks[b] = n;
+}
+
+// ============================================================================
+// a4 (part 1): uniform page map.  grid (B), 1024 threads.
+// ============================================================================
+__global__ void __launch_bounds__(1024) k_map_pages(const int32_t* __restrict__ block_starts,
+                                                    const int32_t* __restrict__ n_blocks, int maxb,
+                                                    int maxp, int P, int32_t* __restrict__ page_first,
+                                                    int32_t* __restrict__ page_block,
+                                                    int16_t* __restrict__ page_valid,
+                                                    int32_t* __restrict__ n_pages) {
+  __shared__ int sm[33];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = n_blocks[b];
+  const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
+  int32_t* pf = page_first + (size_t)b * (maxb + 1);
+  int32_t* pb = page_block + (size_t)b * maxp;
+  int16_t* pv = page_valid + (size_t)b * maxp;
+  int carry = 0;
+  for (int c0 = 0; c0 < nb; c0 += 1024) {
+    const int blk = c0 + tid;
+    int len = 0, np = 0;
+    if (blk < nb) {
+      len = bs[blk + 1] - bs[blk];
+      np = (len + P - 1) / P;
+    }
+    const int inc = warp_incl_scan(np);
+    if (lane == 31) sm[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const int x = sm[lane];
+      const int sc = warp_incl_scan(x);
+      sm[lane] = sc - x;
+      if (lane == 31) sm[32] = sc;
+    }
+    __syncthreads();
+    const int off = carry + sm[warp] + inc - np;
+    const int tot = sm[32];
+    if (blk < nb) {
+      pf[blk] = off;
+      for (int jj = 0; jj < np; ++jj) {
+        pb[off + jj] = blk;
+        pv[off + jj] = (int16_t)min(P, len - P * jj);
+      }
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  for (int i = nb + tid; i <= maxb; i += 1024) pf[i] = carry;
+  for (int j = carry + tid; j < maxp; j += 1024) {
+    pb[j] = -1;
+    pv[j] = 0;
+  }
+  if (tid == 0) n_pages[b] = carry;
+}
+
+// ============================================================================
+// a4 (part 2): repack + digests.  grid (min(maxb, 8*SMs), B), 128 threads;
+// CTAs stride over blocks.  Thread hc owns one 16-byte chunk (h, c) of a token
+// row and walks the block's tokens: 16-byte coalesced loads of the
+// token-major K/V rows, stores into the head-major pages, running max/min for
+// the digest (exact: max/min of stored values), zeroed padding slots.
+// ============================================================================
+template <typename T>
+DSK_DEVICE void unpack16(const uint4& u, float* x) {
+  if constexpr (sizeof(T) == 2) {
+    x[0] = bf_lo(u.x); x[1] = bf_hi(u.x); x[2] = bf_lo(u.y); x[3] = bf_hi(u.y);
+    x[4] = bf_lo(u.z); x[5] = bf_hi(u.z); x[6] = bf_lo(u.w); x[7] = bf_hi(u.w);
+  } else {
+    x[0] = __uint_as_float(u.x); x[1] = __uint_as_float(u.y);
+    x[2] = __uint_as_float(u.z); x[3] = __uint_as_float(u.w);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, const T* __restrict__ V,
+                                                       const int32_t* __restrict__ block_starts,
+                                                       const int32_t* __restrict__ n_blocks,
+                                                       const int32_t* __restrict__ page_first, int S,
+                                                       int Hkv, int maxb, int maxp, int P,
+                                                       T* __restrict__ Kp, T* __restrict__ Vp,
+                                                       T* __restrict__ dig) {
+  constexpr int EPC = 16 / sizeof(T);     // elements per 16-byte chunk
+  constexpr int CPR = kD / EPC;           // chunks per head row
+  const int b = blockIdx.y;
+  const int nb = n_blocks[b];
+  const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
+  const int32_t* pf = page_first + (size_t)b * (maxb + 1);
+  const int HC = Hkv * CPR;
+  for (int blk = blockIdx.x; blk < nb; blk += gridDim.x) {
+    const int st = bs[blk], len = bs[blk + 1] - st, p0 = pf[blk];
+    const int npg = (len + P - 1) / P;
+    for (int hc = threadIdx.x; hc < HC; hc += blockDim.x) {
+      const int h = hc / CPR, c = hc % CPR;
+      float mx[EPC], mn[EPC];
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+        mx[e] = -CUDART_INF_F;
+        mn[e] = CUDART_INF_F;
+      }
+      const size_t page_base = ((size_t)b * Hkv + h) * maxp;
+      int t = 0;
+      for (; t + 4 <= len; t += 4) {
+        uint4 kk[4], vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const size_t src = (((size_t)b * S + st + t + u) * Hkv + h) * kD + c * EPC;
+          kk[u] = __ldg(reinterpret_cast<const uint4*>(K + src));
+          vv[u] = __ldg(reinterpret_cast<const uint4*>(V + src));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tt = t + u;
+          const size_t dst = ((page_base + p0 + tt / P) * P + tt % P) * kD + c * EPC;
+          *reinterpret_cast<uint4*>(Kp + dst) = kk[u];
+          *reinterpret_cast<uint4*>(Vp + dst) = vv[u];
+          float x[EPC];
+          unpack16<T>(kk[u], x);
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) {
+            mx[e] = fmaxf(mx[e], x[e]);
+            mn[e] = fminf(mn[e], x[e]);
+          }
+        }
+      }
+      for (; t < len; ++t) {
+        const size_t src = (((size_t)b * S + st + t) * Hkv + h) * kD + c * EPC;
+        const uint4 kk = __ldg(reinterpret_cast<const uint4*>(K + src));
+        const uint4 vv = __ldg(reinterpret_cast<const uint4*>(V + src));
+        const size_t dst = ((page_base + p0 + t / P) * P + t % P) * kD + c * EPC;
+        *reinterpret_cast<uint4*>(Kp + dst) = kk;
+        *reinterpret_cast<uint4*>(Vp + dst) = vv;
+        float x[EPC];
+        unpack16<T>(kk, x);
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          mx[e] = fmaxf(mx[e], x[e]);
+          mn[e] = fminf(mn[e], x[e]);
+        }
+      }
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (int tt = len; tt < npg * P; ++tt) {
+        const size_t dst = ((page_base + p0 + tt / P) * P + tt % P) * kD + c * EPC;
+        *reinterpret_cast<uint4*>(Kp + dst) = z;
+        *reinterpret_cast<uint4*>(Vp + dst) = z;
+      }
+      // digest row: [.., 0, :] = kmax, [.., 1, :] = kmin (values are exact copies)
+      T* dp = dig + (((size_t)b * Hkv + h) * maxb + blk) * 2 * kD + c * EPC;
+      T omx[EPC], omn[EPC];
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+        if constexpr (sizeof(T) == 2) {
+          omx[e] = __float2bfloat16_rn(mx[e]);
+          omn[e] = __float2bfloat16_rn(mn[e]);
+        } else {
+          omx[e] = mx[e];
+          omn[e] = mn[e];
+        }
+      }
+      *reinterpret_cast<uint4*>(dp) = *reinterpret_cast<const uint4*>(omx);
+      *reinterpret_cast<uint4*>(dp + kD) = *reinterpret_cast<const uint4*>(omn);
+    }
+  }
+}
+
+// ============================================================================
+// host launchers
+// ============================================================================
+cudaError_t launch_weight_table(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
+                                const float* s, uint8_t* w10, int B, int S, cudaStream_t st) {
+  k_weight_table<<<B, 256, 0, st>>>(tokens, delim_ids, n_ids, s, w10, S);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segment(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
+                           const uint8_t* w10, int B, int S, int C, int delta, int lam_num,
+                           int lam_den, int maxb, int32_t* next_ws, int32_t* block_starts,
+                           int32_t* n_blocks, cudaStream_t st) {
+  k_dd_next<<<dim3((S + 255) / 256, B), 256, 0, st>>>(tokens, delim_ids, n_ids, w10, S, C, delta,
+                                                       lam_num, lam_den, next_ws);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_dd_walk<<<B, 1024, 0, st>>>(next_ws, S, maxb, block_starts, n_blocks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int maxb, int maxp, int P,
+                             int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                             int32_t* n_pages, cudaStream_t st) {
+  k_map_pages<<<B, 1024, 0, st>>>(bs, nb, maxb, maxp, P, page_first, page_block, page_valid, n_pages);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
+                                 const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
+                                 int maxb, int maxp, int P, void* Kp, void* Vp, void* dig,
+                                 cudaStream_t st) {
+  const int ctas = max(1, min(maxb, num_sms() * 8 / max(1, B)));
+  dim3 grid(ctas, B);
+  if (dtype == 0)
+    k_repack_digest<bf16><<<grid, 128, 0, st>>>(
+        static_cast<const bf16*>(K), static_cast<const bf16*>(V), bs, nb, pf, S, Hkv, maxb, maxp, P,
+        static_cast<bf16*>(Kp), static_cast<bf16*>(Vp), static_cast<bf16*>(dig));
+  else
+    k_repack_digest<float><<<grid, 128, 0, st>>>(
+        static_cast<const float*>(K), static_cast<const float*>(V), bs, nb, pf, S, Hkv, maxb, maxp,
+        P, static_cast<float*>(Kp), static_cast<float*>(Vp), static_cast<float*>(dig));
+  return cudaGetLastError();
+}
+
+}  // namespace dsk

@@ -1,0 +1,52 @@
+// Internal host-side launchers (C++ linkage; not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dsk {
+
+struct WLEntry;
+
+int num_sms();
+int decode_n_split(int B, int Hkv);
+size_t select_threshold_smem(int maxb);
+
+// decode (decode_kernels.cu)
+cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
+                                float* scores, int B, int Hq, int Hkv, int maxb, cudaStream_t st);
+cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const int32_t* nb,
+                          const int32_t* pf, int B, int Hq, int Hkv, int maxb, int max_sel,
+                          int max_wl, int P, int budget, int blk_lo, int blk_hi, int4* sel_info,
+                          int32_t* sel_blocks, int32_t* n_sel, int32_t* marg, int32_t* keep,
+                          int32_t* wl_count, WLEntry* wl, cudaStream_t st);
+cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, const void* Vp,
+                               const int16_t* pv, const int32_t* n_pages, const int32_t* wl_hdr,
+                               const int32_t* wl_count, const WLEntry* wl, int dense, int B, int Hq, int Hkv,
+                               int max_pages, int P, float scale, float* part_o, float* part_lse,
+                               int* counters, int n_split, float* o, float* lse, cudaStream_t st);
+cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,
+                         float* o, float* lse, cudaStream_t st);
+
+// prefill (build_kernels.cu)
+cudaError_t launch_weight_table(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
+                                const float* s, uint8_t* w10, int B, int S, cudaStream_t st);
+cudaError_t launch_segment(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
+                           const uint8_t* w10, int B, int S, int C, int delta, int lam_num,
+                           int lam_den, int maxb, int32_t* next_ws, int32_t* block_starts,
+                           int32_t* n_blocks, cudaStream_t st);
+cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int maxb, int maxp, int P,
+                             int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                             int32_t* n_pages, cudaStream_t st);
+cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
+                                 const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
+                                 int maxb, int maxp, int P, void* Kp, void* Vp, void* dig,
+                                 cudaStream_t st);
+
+// prefill scoring (score_kernels.cu)
+size_t score_ws_bytes(int Ls, int B, int S, int Hq);
+cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
+                                    const void* Qs, const void* Ks, int Ls, int B, int S, int Hq,
+                                    int Hkv, int W, int R, float alpha, float* out, void* ws,
+                                    cudaStream_t st);
+
+}  // namespace dsk

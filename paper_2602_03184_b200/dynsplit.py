@@ -1,0 +1,450 @@
+"""Thin Python binding of libdynsplit.so (include/dynsplit.h).
+
+Argument marshalling only: tensors are checked for dtype/shape/contiguity,
+outputs and workspaces are allocated with torch (device memory plumbing), and
+the raw device pointers plus the current CUDA stream go through ctypes to the
+C ABI.  Every step of the path runs in the library's CUDA kernels; there is no
+fallback -- if the library is missing or no GPU is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit.so")
+
+OK = 0
+BF16, FP32 = 0, 1
+OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN = range(5)
+INT32_MAX = 0x7FFFFFFF
+
+
+class DynsplitError(RuntimeError):
+    pass
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("S", ctypes.c_int32), ("Hq", ctypes.c_int32),
+                ("Hkv", ctypes.c_int32), ("d", ctypes.c_int32),
+                ("n_score_layers", ctypes.c_int32), ("kv_dtype", ctypes.c_int32)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_int32), ("R", ctypes.c_int32), ("alpha_pen", ctypes.c_float),
+                ("C", ctypes.c_int32), ("delta", ctypes.c_int32), ("lambda_num", ctypes.c_int32),
+                ("lambda_den", ctypes.c_int32), ("page_size", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+_SZ = ctypes.c_size_t
+_PS = ctypes.POINTER(Shape)
+_PC = ctypes.POINTER(Config)
+
+# name -> (restype, argtypes); every symbol declared in include/dynsplit.h
+SIGNATURES = {
+    "dynsplit_default_config": (None, [_PC]),
+    "dynsplit_max_blocks": (_I, [_I, _PC]),
+    "dynsplit_max_pages": (_I, [_I, _PC]),
+    "dynsplit_max_selected": (_I, [_I, _I, _PC]),
+    "dynsplit_worklist_bytes": (_SZ, [_PS, _PC, _I]),
+    "dynsplit_workspace_bytes": (_SZ, [_I, _PS, _PC, _I]),
+    "dynsplit_status_string": (ctypes.c_char_p, [_I]),
+    "dynsplit_version": (ctypes.c_char_p, []),
+    "dynsplit_score_delimiters": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_weight_table": (_I, [_PS, _P, _P, _I, _P, _P, _P]),
+    "dynsplit_segment": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_map_pages": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, _P]),
+    "dynsplit_repack_digest": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "dynsplit_build_blocks": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                   _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_score_blocks": (_I, [_PS, _PC, _P, _P, _P, _P, _P]),
+    "dynsplit_select_from_scores": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P,
+                                         _P, _SZ, _P]),
+    "dynsplit_select": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_decode_attn": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, ctypes.c_float, _P, _P, _P,
+                                  _SZ, _P]),
+    "dynsplit_merge_partials": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
+    "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
+    "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
+                                       ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libdynsplit.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DynsplitError(f"{LIB_PATH} missing: run `python -m paper_2602_03184_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        msg = lib().dynsplit_status_string(st).decode()
+        raise DynsplitError(f"{what}: {msg} ({st})")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise DynsplitError("expected a CUDA tensor (the library has no CPU path)")
+    if not t.is_contiguous():
+        raise DynsplitError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return FP32
+    raise DynsplitError(f"unsupported KV dtype {t.dtype}")
+
+
+def default_config(**overrides) -> Config:
+    c = Config()
+    lib().dynsplit_default_config(ctypes.byref(c))
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
+
+
+def make_shape(B, S, Hq, Hkv, d=128, n_score_layers=1, kv_dtype=BF16) -> Shape:
+    return Shape(B, S, Hq, Hkv, d, n_score_layers, kv_dtype)
+
+
+def max_blocks(S: int, cfg: Config) -> int:
+    return lib().dynsplit_max_blocks(S, ctypes.byref(cfg))
+
+
+def max_pages(S: int, cfg: Config) -> int:
+    return lib().dynsplit_max_pages(S, ctypes.byref(cfg))
+
+
+def max_selected(budget: int, S: int, cfg: Config) -> int:
+    return lib().dynsplit_max_selected(budget, S, ctypes.byref(cfg))
+
+
+def workspace_bytes(op: int, shape: Shape, cfg: Config, budget: int = 1) -> int:
+    return lib().dynsplit_workspace_bytes(op, ctypes.byref(shape), ctypes.byref(cfg), budget)
+
+
+def worklist_bytes(shape: Shape, cfg: Config, budget: int) -> int:
+    return lib().dynsplit_worklist_bytes(ctypes.byref(shape), ctypes.byref(cfg), budget)
+
+
+_WS = {}
+
+
+def workspace(nbytes: int, device, key: str) -> torch.Tensor:
+    """Zero-initialised, cached device workspace (the library keeps its
+    counters zeroed between calls, so a workspace is reusable on one stream)."""
+    dev = torch.device(device)
+    k = (dev.index, key)
+    t = _WS.get(k)
+    if t is None or t.numel() < nbytes:
+        t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        _WS[k] = t
+    return t
+
+
+# ---------------------------------------------------------------------------
+# prefill
+# ---------------------------------------------------------------------------
+@dataclass
+class PagedLayer:
+    """Output of block construction for one layer (plan + pages + digests)."""
+    shape: Shape
+    cfg: Config
+    w10: torch.Tensor          # uint8 [B, n_ids]
+    block_starts: torch.Tensor  # int32 [B, max_blocks+1]
+    n_blocks: torch.Tensor     # int32 [B]
+    page_first: torch.Tensor   # int32 [B, max_blocks+1]
+    page_block: torch.Tensor   # int32 [B, max_pages]
+    page_valid: torch.Tensor   # int16 [B, max_pages]
+    n_pages: torch.Tensor      # int32 [B]
+    Kp: Optional[torch.Tensor]  # [B, Hkv, max_pages, P, d]
+    Vp: Optional[torch.Tensor]
+    digests: Optional[torch.Tensor]  # [B, Hkv, max_blocks, 2, d]
+    delim_scores: Optional[torch.Tensor] = None
+
+
+def score_delimiters(tokens, delim_ids, Qs, Ks, cfg: Config):
+    """Row a1 (Alg. 1).  tokens int32 [B,S]; Qs bf16 [Ls,B,S,Hq,d]; Ks [Ls,B,S,Hkv,d]."""
+    Ls, B, S, Hq, d = Qs.shape
+    shape = make_shape(B, S, Hq, Ks.shape[3], d, Ls, _dtype_code(Qs))
+    out = torch.empty(B, S, dtype=torch.float32, device=tokens.device)
+    nb = workspace_bytes(OP_SCORE_DELIMITERS, shape, cfg)
+    ws = workspace(nb, tokens.device, "score")
+    _check(lib().dynsplit_score_delimiters(ctypes.byref(shape), ctypes.byref(cfg), _ptr(tokens),
+                                           _ptr(delim_ids), delim_ids.numel(), _ptr(Qs), _ptr(Ks),
+                                           _ptr(out), _ptr(ws), ws.numel(), _stream()),
+           "score_delimiters")
+    return out
+
+
+def weight_table(tokens, delim_ids, scores):
+    """Row a2.  -> uint8 [B, n_ids] weights in tenths."""
+    B, S = tokens.shape
+    shape = make_shape(B, S, 1, 1)
+    w10 = torch.empty(B, delim_ids.numel(), dtype=torch.uint8, device=tokens.device)
+    _check(lib().dynsplit_weight_table(ctypes.byref(shape), _ptr(tokens), _ptr(delim_ids),
+                                       delim_ids.numel(), _ptr(scores), _ptr(w10), _stream()),
+           "weight_table")
+    return w10
+
+
+def segment(tokens, delim_ids, w10, cfg: Config):
+    """Row a3 (DD-Select).  -> (block_starts [B, maxb+1], n_blocks [B])."""
+    B, S = tokens.shape
+    shape = make_shape(B, S, 1, 1)
+    mb = max_blocks(S, cfg)
+    bs = torch.empty(B, mb + 1, dtype=torch.int32, device=tokens.device)
+    nb = torch.empty(B, dtype=torch.int32, device=tokens.device)
+    ws = workspace(workspace_bytes(OP_SEGMENT, shape, cfg), tokens.device, "segment")
+    _check(lib().dynsplit_segment(ctypes.byref(shape), ctypes.byref(cfg), _ptr(tokens),
+                                  _ptr(delim_ids), delim_ids.numel(), _ptr(w10), _ptr(bs), _ptr(nb),
+                                  _ptr(ws), ws.numel(), _stream()), "segment")
+    return bs, nb
+
+
+def map_pages(block_starts, n_blocks, S: int, cfg: Config):
+    """Row a4 part 1.  -> (page_first, page_block, page_valid, n_pages)."""
+    B = block_starts.shape[0]
+    shape = make_shape(B, S, 1, 1)
+    mb, mp = max_blocks(S, cfg), max_pages(S, cfg)
+    dev = block_starts.device
+    pf = torch.empty(B, mb + 1, dtype=torch.int32, device=dev)
+    pb = torch.empty(B, mp, dtype=torch.int32, device=dev)
+    pv = torch.empty(B, mp, dtype=torch.int16, device=dev)
+    npg = torch.empty(B, dtype=torch.int32, device=dev)
+    _check(lib().dynsplit_map_pages(ctypes.byref(shape), ctypes.byref(cfg), _ptr(block_starts),
+                                    _ptr(n_blocks), _ptr(pf), _ptr(pb), _ptr(pv), _ptr(npg),
+                                    _stream()), "map_pages")
+    return pf, pb, pv, npg
+
+
+def repack_digest(K, V, block_starts, n_blocks, page_first, cfg: Config, out=None):
+    """Row a4 part 2.  K, V [B,S,Hkv,d] -> (Kp, Vp, digests)."""
+    B, S, Hkv, d = K.shape
+    shape = make_shape(B, S, Hkv, Hkv, d, 1, _dtype_code(K))
+    mb, mp, P = max_blocks(S, cfg), max_pages(S, cfg), cfg.page_size
+    if out is None:
+        Kp = torch.empty(B, Hkv, mp, P, d, dtype=K.dtype, device=K.device)
+        Vp = torch.empty_like(Kp)
+        dig = torch.empty(B, Hkv, mb, 2, d, dtype=K.dtype, device=K.device)
+    else:
+        Kp, Vp, dig = out
+    _check(lib().dynsplit_repack_digest(ctypes.byref(shape), ctypes.byref(cfg), _ptr(K), _ptr(V),
+                                        _ptr(block_starts), _ptr(n_blocks), _ptr(page_first),
+                                        _ptr(Kp), _ptr(Vp), _ptr(dig), _stream()), "repack_digest")
+    return Kp, Vp, dig
+
+
+def build_blocks(tokens, delim_ids, K, V, cfg: Config, static_w10=None, Qs=None, Ks=None,
+                 Hq: Optional[int] = None, return_scores: bool = False) -> PagedLayer:
+    """Rows a1-a4 through dynsplit_build_blocks (one C call).
+
+    static_w10: host uint8 sequence (e.g. Table 7) -> static mode; else Qs/Ks
+    (bf16 [Ls,B,S,H*,d]) drive the dynamic scoring.  K/V may be None (plan only).
+    """
+    B, S = tokens.shape
+    dev = tokens.device
+    if K is not None:
+        Hkv, d = K.shape[2], K.shape[3]
+        dt = _dtype_code(K)
+    else:
+        Hkv, d, dt = (Ks.shape[3] if Ks is not None else 1), 128, BF16
+    if Hq is None:
+        Hq = Qs.shape[3] if Qs is not None else Hkv
+    Ls = Qs.shape[0] if Qs is not None else 1
+    shape = make_shape(B, S, Hq, Hkv, d, Ls, dt)
+    mb, mp, P = max_blocks(S, cfg), max_pages(S, cfg), cfg.page_size
+    n_ids = delim_ids.numel()
+    w10 = torch.empty(B, n_ids, dtype=torch.uint8, device=dev)
+    bs = torch.empty(B, mb + 1, dtype=torch.int32, device=dev)
+    nb = torch.empty(B, dtype=torch.int32, device=dev)
+    pf = torch.empty(B, mb + 1, dtype=torch.int32, device=dev)
+    pb = torch.empty(B, mp, dtype=torch.int32, device=dev)
+    pv = torch.empty(B, mp, dtype=torch.int16, device=dev)
+    npg = torch.empty(B, dtype=torch.int32, device=dev)
+    scores = torch.empty(B, S, dtype=torch.float32, device=dev) if (return_scores and static_w10 is None) else None
+    Kp = Vp = dig = None
+    if K is not None:
+        Kp = torch.empty(B, Hkv, mp, P, d, dtype=K.dtype, device=dev)
+        Vp = torch.empty_like(Kp)
+        dig = torch.empty(B, Hkv, mb, 2, d, dtype=K.dtype, device=dev)
+    hostw = None
+    if static_w10 is not None:
+        arr = (ctypes.c_uint8 * n_ids)(*[int(x) for x in static_w10])
+        hostw = ctypes.cast(arr, ctypes.c_void_p)
+    ws = workspace(workspace_bytes(OP_BUILD_BLOCKS, shape, cfg), dev, "build")
+    _check(lib().dynsplit_build_blocks(
+        ctypes.byref(shape), ctypes.byref(cfg), _ptr(tokens), _ptr(delim_ids), n_ids, hostw,
+        _ptr(Qs), _ptr(Ks), _ptr(K), _ptr(V), _ptr(w10), _ptr(scores), _ptr(bs), _ptr(nb),
+        _ptr(pf), _ptr(pb), _ptr(pv), _ptr(npg), _ptr(Kp), _ptr(Vp), _ptr(dig), _ptr(ws),
+        ws.numel(), _stream()), "build_blocks")
+    return PagedLayer(shape, cfg, w10, bs, nb, pf, pb, pv, npg, Kp, Vp, dig, scores)
+
+
+# ---------------------------------------------------------------------------
+# decode
+# ---------------------------------------------------------------------------
+@dataclass
+class Selection:
+    sel_blocks: torch.Tensor    # int32 [B, Hq, max_sel] (ascending; first n_sel valid)
+    n_sel: torch.Tensor         # int32 [B, Hq]
+    marginal_block: torch.Tensor  # int32 [B, Hq]
+    marginal_keep: torch.Tensor   # int32 [B, Hq]
+    worklist: torch.Tensor      # opaque uint8
+    scores: Optional[torch.Tensor] = None  # fp32 [B, Hq, max_blocks]
+
+
+def _decode_shape(q, layer: PagedLayer) -> Shape:
+    B, Hq, d = q.shape
+    s = layer.shape
+    return make_shape(B, s.S, Hq, s.Hkv, d, 1, _dtype_code(q))
+
+
+def score_blocks(q, layer: PagedLayer, out=None):
+    """Row a5.  q [B,Hq,d] -> fp32 [B,Hq,max_blocks]."""
+    shape = _decode_shape(q, layer)
+    mb = max_blocks(shape.S, layer.cfg)
+    sc = out if out is not None else torch.empty(shape.B, shape.Hq, mb, dtype=torch.float32, device=q.device)
+    _check(lib().dynsplit_score_blocks(ctypes.byref(shape), ctypes.byref(layer.cfg), _ptr(q),
+                                       _ptr(layer.digests), _ptr(layer.n_blocks), _ptr(sc),
+                                       _stream()), "score_blocks")
+    return sc
+
+
+def _sel_outputs(shape: Shape, cfg: Config, budget: int, dev, want_blocks=True):
+    ms = max_selected(budget, shape.S, cfg)
+    sb = torch.empty(shape.B, shape.Hq, ms, dtype=torch.int32, device=dev) if want_blocks else None
+    ns = torch.empty(shape.B, shape.Hq, dtype=torch.int32, device=dev)
+    mg = torch.empty_like(ns)
+    kp = torch.empty_like(ns)
+    wl = torch.empty(worklist_bytes(shape, cfg, budget), dtype=torch.uint8, device=dev)
+    return sb, ns, mg, kp, wl
+
+
+def select_from_scores(scores, layer: PagedLayer, budget: int, Hq: int, blk_lo: int = 0,
+                       blk_hi: int = INT32_MAX, out=None, ws=None) -> Selection:
+    """Row a6 on given block scores (seq-split shards pass their block range)."""
+    s = layer.shape
+    shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
+    sb, ns, mg, kp, wl = out if out is not None else _sel_outputs(shape, layer.cfg, budget, scores.device)
+    if ws is None:
+        ws = workspace(workspace_bytes(OP_SELECT, shape, layer.cfg, budget), scores.device, "select")
+    _check(lib().dynsplit_select_from_scores(
+        ctypes.byref(shape), ctypes.byref(layer.cfg), budget, _ptr(scores), _ptr(layer.block_starts),
+        _ptr(layer.n_blocks), _ptr(layer.page_first), blk_lo, blk_hi, _ptr(sb), _ptr(ns), _ptr(mg),
+        _ptr(kp), _ptr(wl), _ptr(ws), ws.numel(), _stream()), "select_from_scores")
+    return Selection(sb, ns, mg, kp, wl, scores)
+
+
+def select(q, layer: PagedLayer, budget: int, keep_scores: bool = True, out=None, ws=None) -> Selection:
+    """Rows a5 + a6 through dynsplit_select."""
+    shape = _decode_shape(q, layer)
+    mb = max_blocks(shape.S, layer.cfg)
+    if out is None:
+        sb, ns, mg, kp, wl = _sel_outputs(shape, layer.cfg, budget, q.device)
+        sc = torch.empty(shape.B, shape.Hq, mb, dtype=torch.float32, device=q.device) if keep_scores else None
+    else:
+        sb, ns, mg, kp, wl, sc = out
+    if ws is None:
+        ws = workspace(workspace_bytes(OP_SELECT, shape, layer.cfg, budget), q.device, "select")
+    _check(lib().dynsplit_select(
+        ctypes.byref(shape), ctypes.byref(layer.cfg), budget, _ptr(q), _ptr(layer.digests),
+        _ptr(layer.block_starts), _ptr(layer.n_blocks), _ptr(layer.page_first), _ptr(sc), _ptr(sb),
+        _ptr(ns), _ptr(mg), _ptr(kp), _ptr(wl), _ptr(ws), ws.numel(), _stream()), "select")
+    return Selection(sb, ns, mg, kp, wl, sc)
+
+
+def decode_attn(q, layer: PagedLayer, worklist: Optional[torch.Tensor], scale: float = 0.0,
+                out=None, ws=None):
+    """Rows a7 + a8 (worklist=None: dense baseline, row a9).  -> (o fp32 [B,Hq,d], lse fp32 [B,Hq])."""
+    shape = _decode_shape(q, layer)
+    if out is None:
+        o = torch.empty(shape.B, shape.Hq, shape.d, dtype=torch.float32, device=q.device)
+        lse = torch.empty(shape.B, shape.Hq, dtype=torch.float32, device=q.device)
+    else:
+        o, lse = out
+    if ws is None:
+        ws = workspace(workspace_bytes(OP_DECODE_ATTN, shape, layer.cfg), q.device, "decode")
+    _check(lib().dynsplit_decode_attn(
+        ctypes.byref(shape), ctypes.byref(layer.cfg), _ptr(q), _ptr(layer.Kp), _ptr(layer.Vp),
+        _ptr(layer.page_valid), _ptr(layer.n_pages), _ptr(worklist), ctypes.c_float(scale),
+        _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream()), "decode_attn")
+    return o, lse
+
+
+def merge_partials(o_parts, lse_parts):
+    """Row a8 standalone.  o_parts [n, rows, d], lse_parts [n, rows]."""
+    n, rows, d = o_parts.shape
+    o = torch.empty(rows, d, dtype=torch.float32, device=o_parts.device)
+    lse = torch.empty(rows, dtype=torch.float32, device=o_parts.device)
+    _check(lib().dynsplit_merge_partials(_ptr(o_parts), _ptr(lse_parts), n, rows, d, _ptr(o),
+                                         _ptr(lse), _stream()), "merge_partials")
+    return o, lse
+
+
+def decode_step_host(q_host, layer: PagedLayer, budget: int, o_host, lse_host, worklist, ws,
+                     scale: float = 0.0):
+    """Rows a5-a8 with pinned HOST q/o/lse through dynsplit_decode_step_host."""
+    B, Hq, d = q_host.shape
+    s = layer.shape
+    shape = make_shape(B, s.S, Hq, s.Hkv, d, 1, _dtype_code(q_host))
+    for t in (q_host, o_host, lse_host):
+        if t.is_cuda or not t.is_pinned():
+            raise DynsplitError("decode_step_host expects pinned host tensors")
+    _check(lib().dynsplit_decode_step_host(
+        ctypes.byref(shape), ctypes.byref(layer.cfg), budget, ctypes.c_void_p(q_host.data_ptr()),
+        _ptr(layer.digests), _ptr(layer.block_starts), _ptr(layer.n_blocks), _ptr(layer.page_first),
+        _ptr(layer.Kp), _ptr(layer.Vp), _ptr(layer.page_valid), ctypes.c_float(scale),
+        ctypes.c_void_p(o_host.data_ptr()), ctypes.c_void_p(lse_host.data_ptr()), _ptr(worklist),
+        _ptr(ws), ws.numel(), _stream()), "decode_step_host")
+
+
+def step_host_workspace_bytes(shape: Shape, cfg: Config, budget: int) -> int:
+    return lib().dynsplit_step_host_workspace_bytes(ctypes.byref(shape), ctypes.byref(cfg), budget)
+
+
+def worklist_rows(worklist: torch.Tensor, shape: Shape, G: int):
+    """Host-side reading of a worklist (metrics only): per (b, KV head) the
+    number of page entries and of rows streamed (max over the G heads of each
+    entry's row count).  Layout: 256-byte header, int32 counts [B*Hkv] padded to
+    256 bytes, then 16-byte entries {int32 page, int32 block, uint8 rows[8]}."""
+    import numpy as np
+    raw = worklist.cpu().numpy()
+    nbh = shape.B * shape.Hkv
+    hdr = raw[:256].view(np.int32)
+    max_wl = int(hdr[1])
+    counts = raw[256:256 + 4 * nbh].view(np.int32).copy()
+    off = 256 + ((4 * nbh + 255) // 256) * 256
+    ent = raw[off: off + 16 * nbh * max_wl].reshape(nbh, max_wl, 16)
+    rows = ent[:, :, 8:8 + G].max(axis=2).astype(np.int64)
+    streamed = np.array([rows[i, : counts[i]].sum() for i in range(nbh)])
+    return counts, streamed

@@ -1,0 +1,83 @@
+"""CPU checks of the C ABI: the library builds for sm_100a, loads, exports
+every symbol include/dynsplit.h declares, and its host-side queries and
+argument validation work without a GPU (no compute calls)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dynsplit.h")
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2602_03184_b200 import build, dynsplit
+    build.build()
+    dynsplit.lib()
+    return dynsplit
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(dynsplit_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported(D):
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", D.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (dynsplit_[a-z0-9_]+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert set(D.SIGNATURES) == set(syms)          # the binding covers the whole ABI
+
+
+def test_library_is_sm100a(D):
+    out = subprocess.run(["cuobjdump", "--list-elf", D.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_default_config_and_bounds(D):
+    c = D.default_config()
+    assert (c.W, c.R, c.alpha_pen, c.C, c.delta, c.lambda_num, c.lambda_den, c.page_size) == \
+        (8, 128, 1.0, 32, 14, 1, 2, 16)
+    # every non-final chunk has >= C - Delta tokens
+    assert D.max_blocks(131072, c) == 131072 // 18 + 1 == 7282
+    assert D.max_pages(131072, c) == 7282 + 8192
+    assert D.max_selected(4096, 131072, c) == 4095 // 18 + 2
+    assert D.lib().dynsplit_version().startswith(b"dynsplit-b200")
+
+
+def test_host_validation_without_gpu(D):
+    L = D.lib()
+    c = D.default_config()
+    bad = D.make_shape(1, 128, 6, 4)                      # Hq % Hkv != 0
+    assert L.dynsplit_score_blocks(ctypes.byref(bad), ctypes.byref(c), None, None, None, None, None) == 2
+    empty = D.make_shape(1, 0, 8, 8)
+    assert L.dynsplit_segment(ctypes.byref(empty), ctypes.byref(c), None, None, 1, None, None, None,
+                              None, 0, None) == 3
+    ok = D.make_shape(1, 128, 8, 8)
+    assert L.dynsplit_select(ctypes.byref(ok), ctypes.byref(c), 16, None, None, None, None, None, None,
+                             None, None, None, None, None, None, 0, None) == 1
+    c2 = D.default_config(delta=32)                       # Delta >= C
+    assert L.dynsplit_workspace_bytes(D.OP_SELECT, ctypes.byref(ok), ctypes.byref(c2), 16) == 0
+    assert D.workspace_bytes(D.OP_DECODE_ATTN, ok, c) > 0
+    assert D.worklist_bytes(ok, c, 64) > 0
+    assert L.dynsplit_status_string(4) == b"workspace too small"
+    d64 = D.make_shape(1, 128, 8, 8, d=64)
+    assert L.dynsplit_score_blocks(ctypes.byref(d64), ctypes.byref(c), None, None, None, None, None) == 2
+
+
+def test_product_path_has_no_oracle_dependency():
+    # The product package never imports the oracle (test infrastructure only).
+    pkg = os.path.join(ROOT, "paper_2602_03184_b200")
+    pat = re.compile(r"^\s*(from\s+oracle|import\s+oracle|#include\s+.*oracle)", re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not pat.search(src), f
