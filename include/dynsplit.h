@@ -19,9 +19,10 @@
  *    workspace) return a status BEFORE anything is launched.  A launch failure
  *    returns DYNSPLIT_ERR_CUDA (cudaGetLastError is consumed).
  *  - Workspaces (`ws`) are sized by dynsplit_workspace_bytes(op, ...), must
- *    be 256-byte aligned and zero-filled once before first use (the library
- *    keeps its internal counters zeroed between calls).  A workspace may be
- *    reused by consecutive calls on the same stream, never concurrently.
+ *    be 256-byte aligned and zero-filled once before first use (the decode
+ *    workspace starts with split-merge counters at a fixed offset, which the
+ *    library leaves zeroed after every call).  A workspace may be reused by
+ *    consecutive calls of any shape on the same stream, never concurrently.
  *  - Functions are stateless and thread-safe; every one is graph-capturable.
  *  - Query head h reads KV head h / (Hq/Hkv) (GQA).  head_dim d must be 128.
  *  - Symbol notation follows the paper: W, R, alpha (Alg. 1); C,
@@ -96,6 +97,10 @@ size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* shape,
                                 const dynsplit_config* cfg, int32_t budget);
 const char* dynsplit_status_string(int32_t status);
 const char* dynsplit_version(void);
+/* Text of the last CUDA error seen by this thread ("launcher: cuda message"),
+ * "" if none.  Set DYNSPLIT_DEBUG=1 to synchronise after every launch so that
+ * asynchronous faults are attributed to the launcher that caused them. */
+const char* dynsplit_last_error(void);
 
 /* ---------------------------------------------------------------------------
  * Prefill, row a1: delimiter importance scoring, Algorithm 1 with

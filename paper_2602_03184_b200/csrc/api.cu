@@ -7,6 +7,8 @@
 #include "kernels.h"
 
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 namespace dsk {
@@ -24,6 +26,41 @@ int num_sms() {
   }
   return cached;
 }
+
+int max_smem_optin() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        n <= 0) {
+      cudaGetLastError();
+      n = 227 * 1024;
+    }
+    cached = n;
+  }
+  return cached;
+}
+
+static thread_local char g_last_error[512] = "";
+const char* last_error();
+
+cudaError_t post_launch(const char* where, cudaStream_t st) {
+  static int debug = -1;
+  if (debug < 0) {
+    const char* e = getenv("DYNSPLIT_DEBUG");
+    debug = (e && *e && *e != '0') ? 1 : 0;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug) {
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+  return e;
+}
+
+const char* last_error() { return g_last_error; }
 
 }  // namespace dsk
 
@@ -94,9 +131,13 @@ size_t select_ws(const dynsplit_shape* s, const dynsplit_config* c) {
   const int maxb = dynsplit_max_blocks(s->S, c);
   return align_up((size_t)s->B * s->Hq * maxb * 4) + align_up((size_t)s->B * s->Hq * 16);
 }
+// Decode workspace: [split-merge counters, fixed kMaxCounters ints at offset 0]
+// [part_o] [part_lse].  Counters sit at a shape-independent offset so that a
+// zero-filled workspace stays valid when reused with any shape.
+constexpr size_t kMaxCounters = 65536;
 size_t decode_ws(const dynsplit_shape* s) {
-  return align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4) +
-         align_up((size_t)s->B * s->Hq * kMaxSplit * 4) + align_up((size_t)s->B * s->Hkv * 4);
+  return kMaxCounters * 4 + align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4) +
+         align_up((size_t)s->B * s->Hq * kMaxSplit * 4);
 }
 size_t segment_ws(const dynsplit_shape* s) { return align_up((size_t)s->B * s->S * 4); }
 size_t score_ws(const dynsplit_shape* s) {
@@ -192,6 +233,8 @@ const char* dynsplit_status_string(int32_t st) {
 
 const char* dynsplit_version(void) { return "dynsplit-b200 0.1 (sm_100a)"; }
 
+const char* dynsplit_last_error(void) { return dsk::last_error(); }
+
 // ------------------------------------------------------------------ prefill
 dynsplit_status dynsplit_score_delimiters(const dynsplit_shape* s, const dynsplit_config* c,
                                           const int32_t* tokens, const int32_t* delim_ids,
@@ -285,7 +328,7 @@ dynsplit_status dynsplit_build_blocks(const dynsplit_shape* s, const dynsplit_co
     memset(&t, 0, sizeof(t));
     memcpy(t.w, static_w10_host, (size_t)n_ids);
     k_fill_w10<<<s->B, 64, 0, st>>>(t, n_ids, w10);
-    if (cudaGetLastError() != cudaSuccess) return DYNSPLIT_ERR_CUDA;
+    if (post_launch("k_fill_w10", st) != cudaSuccess) return DYNSPLIT_ERR_CUDA;
   } else {
     if (!Qs || !Ks) return DYNSPLIT_ERR_INVALID_ARGUMENT;
     float* sc = delim_scores ? delim_scores : tmp_scores;
@@ -371,11 +414,12 @@ dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_con
   if (dense && (!n_pages || !page_valid)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < decode_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)kD);
+  if ((size_t)s->B * s->Hkv > kMaxCounters) return DYNSPLIT_ERR_UNSUPPORTED;
   char* w = static_cast<char*>(ws);
-  float* part_o = reinterpret_cast<float*>(w);
-  float* part_lse = reinterpret_cast<float*>(w + align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4));
-  int* counters = reinterpret_cast<int*>(w + align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4) +
-                                         align_up((size_t)s->B * s->Hq * kMaxSplit * 4));
+  int* counters = reinterpret_cast<int*>(w);
+  float* part_o = reinterpret_cast<float*>(w + kMaxCounters * 4);
+  float* part_lse = reinterpret_cast<float*>(w + kMaxCounters * 4 +
+                                             align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4));
   const int32_t* hdr = nullptr;
   const int32_t* cnt = nullptr;
   const WLEntry* ent = nullptr;
@@ -416,9 +460,9 @@ dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* s, const dynspli
     return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
-  char* ws_sel = w;
-  char* ws_dec = w + select_ws(s, c);
-  char* extra = ws_dec + decode_ws(s);
+  char* ws_dec = w;                      // counters first: shape-independent offset
+  char* ws_sel = w + decode_ws(s);
+  char* extra = ws_sel + select_ws(s, c);
   const size_t qbytes = (size_t)s->B * s->Hq * kD * esize(s);
   void* q_dev = extra;
   float* o_dev = reinterpret_cast<float*>(extra + align_up(qbytes));

@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
 cudaError_t launch_weight_table(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
                                 const float* s, uint8_t* w10, int B, int S, cudaStream_t st) {
   k_weight_table<<<B, 256, 0, st>>>(tokens, delim_ids, n_ids, s, w10, S);
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 cudaError_t launch_segment(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
@@ -349,17 +349,17 @@ cudaError_t launch_segment(const int32_t* tokens, const int32_t* delim_ids, int 
                            int32_t* n_blocks, cudaStream_t st) {
   k_dd_next<<<dim3((S + 255) / 256, B), 256, 0, st>>>(tokens, delim_ids, n_ids, w10, S, C, delta,
                                                        lam_num, lam_den, next_ws);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = post_launch(__func__, st);
   if (e != cudaSuccess) return e;
   k_dd_walk<<<B, 1024, 0, st>>>(next_ws, S, maxb, block_starts, n_blocks);
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int maxb, int maxp, int P,
                              int32_t* page_first, int32_t* page_block, int16_t* page_valid,
                              int32_t* n_pages, cudaStream_t st) {
   k_map_pages<<<B, 1024, 0, st>>>(bs, nb, maxb, maxp, P, page_first, page_block, page_valid, n_pages);
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
@@ -376,7 +376,7 @@ cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const 
     k_repack_digest<float><<<grid, 128, 0, st>>>(
         static_cast<const float*>(K), static_cast<const float*>(V), bs, nb, pf, S, Hkv, maxb, maxp,
         P, static_cast<float*>(Kp), static_cast<float*>(Vp), static_cast<float*>(dig));
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 }  // namespace dsk

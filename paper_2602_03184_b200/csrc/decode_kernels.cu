@@ -686,7 +686,7 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
     case 8: k_score_blocks<T, 8><<<grid, 256, 0, st>>>(qq, dd, nb, scores, Hq, Hkv, maxb); break;
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
@@ -703,12 +703,12 @@ cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const i
   const size_t smem = select_threshold_smem(maxb);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(k_select_threshold, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    allow_max_dyn_smem(k_select_threshold);
     attr_done = true;
   }
   k_select_threshold<<<dim3(Hq, B), kSelThreads, smem, st>>>(scores, bs, nb, Hq, maxb, budget, blk_lo,
                                                             blk_hi, sel_info);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = post_launch(__func__, st);
   if (e != cudaSuccess) return e;
   dim3 grid(Hkv, B);
 #define DSK_UNION(GG)                                                                            \
@@ -723,7 +723,7 @@ cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const i
     default: return cudaErrorInvalidValue;
   }
 #undef DSK_UNION
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 constexpr int kStages = 8;
@@ -740,14 +740,14 @@ static cudaError_t decode_attn_t(const void* q, const void* Kp, const void* Vp, 
                       NS * kMaxG + (size_t)NW * (kD + 2) * sizeof(float) + 64;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    allow_max_dyn_smem(kern);
     attr_done = true;
   }
   kern<<<dim3(n_split, Hkv, B), (NW + 1) * 32, smem, st>>>(
       static_cast<const T*>(q), static_cast<const T*>(Kp), static_cast<const T*>(Vp), pv, n_pages,
       wl_hdr, wl_count, wl, dense, Hq, Hkv, max_pages, P, scale_log2, part_o, part_lse, counters,
       n_split, o, lse);
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 template <typename T>
@@ -793,7 +793,7 @@ cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, 
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,
                          float* o, float* lse, cudaStream_t st) {
   k_merge_partials<<<rows, 128, 0, st>>>(o_parts, lse_parts, n_parts, rows, d, o, lse);
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 }  // namespace dsk

@@ -8,6 +8,23 @@ namespace dsk {
 struct WLEntry;
 
 int num_sms();
+int max_smem_optin();
+// Allow the largest dynamic smem the kernel can use (opt-in limit minus its
+// static smem).
+template <typename F>
+inline void allow_max_dyn_smem(F* kern) {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(kern)) == cudaSuccess)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         max_smem_optin() - (int)a.sharedSizeBytes);
+  cudaGetLastError();
+}
+// After every launch: returns cudaGetLastError(); with DYNSPLIT_DEBUG=1 in the
+// environment also synchronises the stream so asynchronous faults are
+// attributed to the launcher that caused them.  Errors are recorded for
+// dynsplit_last_error().
+cudaError_t post_launch(const char* where, cudaStream_t st);
 int decode_n_split(int B, int Hkv);
 size_t select_threshold_smem(int maxb);
 

@@ -318,7 +318,7 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
                       kRowsPerCta * kMaxW * sizeof(float);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(k_lse_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_dyn_smem(k_lse_band);
     attr_done = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
@@ -327,11 +327,11 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
   k_lse_band<<<grid, 128, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
                                       static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,
                                       scale_log2, part);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = post_launch(__func__, st);
   if (e != cudaSuccess) return e;
   k_score_reduce<<<dim3((S + 255) / 256, B), 256, 0, st>>>(tokens, delim_ids, n_ids, part, Ls, B, S,
                                                            Hq, W, out);
-  return cudaGetLastError();
+  return post_launch(__func__, st);
 }
 
 }  // namespace dsk

@@ -59,6 +59,7 @@ SIGNATURES = {
     "dynsplit_workspace_bytes": (_SZ, [_I, _PS, _PC, _I]),
     "dynsplit_status_string": (ctypes.c_char_p, [_I]),
     "dynsplit_version": (ctypes.c_char_p, []),
+    "dynsplit_last_error": (ctypes.c_char_p, []),
     "dynsplit_score_delimiters": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_weight_table": (_I, [_PS, _P, _P, _I, _P, _P, _P]),
     "dynsplit_segment": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
@@ -99,7 +100,8 @@ def lib():
 def _check(st: int, what: str):
     if st != OK:
         msg = lib().dynsplit_status_string(st).decode()
-        raise DynsplitError(f"{what}: {msg} ({st})")
+        detail = lib().dynsplit_last_error().decode() if st == 6 else ""
+        raise DynsplitError(f"{what}: {msg} ({st}) {detail}".rstrip())
 
 
 def _ptr(t: Optional[torch.Tensor]):

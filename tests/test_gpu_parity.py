@@ -47,7 +47,7 @@ def test_segment_parity(D, S, C, delta, lam):
     B = 3
     cfg = D.default_config(C=C, delta=delta, lambda_num=lam[0], lambda_den=lam[1])
     toks = np.stack([G.tokens(100 + b, S, inner_rate=0.1 + 0.1 * b) for b in range(B)])
-    w10 = np.stack([G.T7_W10, G.rng(b, 5).integers(0, 11, 13), np.full(13, 5)])[:B]
+    w10 = np.stack([G.T7_W10, G.rng(S, 5).integers(0, 11, 13), np.full(13, 5)])[:B]
     bs, nb = D.segment(t(toks), t(G.T7_IDS), t(w10.astype(np.uint8)), cfg)
     bs, nb = bs.cpu().numpy(), nb.cpu().numpy()
     mb = D.max_blocks(S, cfg)
