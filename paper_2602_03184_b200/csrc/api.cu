@@ -429,11 +429,10 @@ dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_con
     cnt = v.count;
     ent = v.entries;
   }
-  const int n_split = decode_n_split(s->B, s->Hkv);
   return cuda_status(launch_decode_attn(s->kv_dtype, s->Hq / s->Hkv, q, Kp, Vp, page_valid, n_pages,
                                         hdr, cnt, ent, dense, s->B, s->Hq, s->Hkv,
                                         dynsplit_max_pages(s->S, c), c->page_size, scale, part_o,
-                                        part_lse, counters, n_split, o, lse,
+                                        part_lse, counters, o, lse,
                                         static_cast<cudaStream_t>(stream)));
 }
 

@@ -2,8 +2,8 @@
 //   a5  k_score_blocks      V2F block score, sum_j max(q_j kmax_j, q_j kmin_j)
 //   a6  k_select_threshold  budgeted top-k via block-to-token mapping
 //       k_select_union      per-head selections -> GQA-union page worklist
-//   a7  k_decode_attn       split-K flash-decoding over the worklist's pages
-//   a8  (same kernel)       last CTA per (b, KV head) merges the splits by LSE
+//   (a7/a8 attention kernels live in attn_kernels.cu)
+
 //       k_merge_partials    standalone LSE merge (cross-GPU sequence split)
 #include "common.cuh"
 #include "kernels.h"
@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select_threshold(
 // Emits, in ascending block order, every page any of the G heads touches with
 // its per-head leading-row counts (the GQA union worklist: each KV page is
 // streamed from HBM once for all G heads), plus per-head ascending sel_blocks.
-// grid (Hkv, B), 512 threads.
+// grid (Hkv, B), 512 threads; each thread owns a contiguous run of blocks:
+// pass 1 counts, one block-wide scan, pass 2 writes.
 // ============================================================================
 template <int G>
 __global__ void __launch_bounds__(kSelThreads) k_select_union(
@@ -315,8 +316,12 @@ __global__ void __launch_bounds__(kSelThreads) k_select_union(
   const int tid = threadIdx.x;
   const int nb = n_blocks[b];
   const int lo = max(blk_lo, 0), hi = min(blk_hi, nb);
+  const int nr = max(hi - lo, 0);
+  const int per = (nr + kSelThreads - 1) / kSelThreads;
+  const int t0 = lo + tid * per, t1 = min(hi, t0 + per);
   const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
   const int32_t* pf = page_first + (size_t)b * (maxb + 1);
+  const float* sc = scores + ((size_t)b * Hq + hk * G) * maxb;
   const int pf_lo = lo < hi ? pf[lo] : 0;
   int m[G], keep[G], all[G];
   uint32_t T[G];
@@ -328,317 +333,69 @@ __global__ void __launch_bounds__(kSelThreads) k_select_union(
     T[g] = (uint32_t)si.z;
     all[g] = si.w;
   }
-  WLEntry* wlb = wl + ((size_t)b * Hkv + hk) * max_wl;
-  int carry[G + 1];
+  auto taken_of = [&](int g, int blk, int len) -> int {
+    const uint32_t key = float_key(sc[(size_t)g * maxb + blk]);
+    const bool sel = all[g] || key > T[g] || (key == T[g] && blk <= m[g]);
+    return sel ? ((blk == m[g]) ? keep[g] : len) : 0;
+  };
+  // pass 1: counts
+  int v[G + 1], tot[G + 1];
 #pragma unroll
-  for (int k = 0; k <= G; ++k) carry[k] = 0;
-  for (int c0 = lo; c0 < hi; c0 += kSelThreads) {
-    const int blk = c0 + tid;
-    const bool valid = blk < hi;
-    int len = 0, taken[G], v[G + 1], tot[G + 1];
-    if (valid) len = bs[blk + 1] - bs[blk];
+  for (int k = 0; k <= G; ++k) v[k] = 0;
+  for (int blk = t0; blk < t1; ++blk) {
+    const int len = bs[blk + 1] - bs[blk];
     int u = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      taken[g] = 0;
-      if (valid) {
-        const uint32_t key = float_key(scores[((size_t)b * Hq + hk * G + g) * maxb + blk]);
-        const bool sel = all[g] || key > T[g] || (key == T[g] && blk <= m[g]);
-        if (sel) taken[g] = (blk == m[g]) ? keep[g] : len;
-      }
-      v[g] = taken[g] > 0;
+      const int tk = taken_of(g, blk, len);
+      v[g] += tk > 0;
+      u = max(u, (tk + P - 1) / P);
+    }
+    v[G] += u;
+  }
+  block_excl_scan<G + 1, kSelThreads>(v, tot, sm_scan);
+  // pass 2: writes
+  WLEntry* wlb = wl + ((size_t)b * Hkv + hk) * max_wl;
+  for (int blk = t0; blk < t1; ++blk) {
+    const int len = bs[blk + 1] - bs[blk];
+    int taken[G], u = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      taken[g] = taken_of(g, blk, len);
       u = max(u, (taken[g] + P - 1) / P);
-    }
-    v[G] = u;
-    block_excl_scan<G + 1, kSelThreads>(v, tot, sm_scan);
-    if (valid) {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (taken[g] > 0 && sel_blocks)
-          sel_blocks[((size_t)b * Hq + hk * G + g) * max_sel + carry[g] + v[g]] = blk;
-      for (int jj = 0; jj < u; ++jj) {
-        WLEntry e;
-        e.page = pf[blk] - pf_lo + jj;
-        e.block = blk;
-        const int pv = min(P, len - P * jj);
-#pragma unroll
-        for (int g = 0; g < kMaxG; ++g) {
-          int r = 0;
-          if (g < G) r = min(max(taken[g] - P * jj, 0), pv);
-          e.rows[g] = (uint8_t)r;
-        }
-        wlb[carry[G] + v[G] + jj] = e;
+      if (taken[g] > 0) {
+        if (sel_blocks) sel_blocks[((size_t)b * Hq + hk * G + g) * max_sel + v[g]] = blk;
+        ++v[g];
       }
     }
+    const int page0 = pf[blk] - pf_lo;
+    for (int jj = 0; jj < u; ++jj) {
+      const int pv = min(P, len - P * jj);
+      uint32_t w0 = 0, w1 = 0;
 #pragma unroll
-    for (int k = 0; k <= G; ++k) carry[k] += tot[k];
+      for (int g = 0; g < G; ++g) {
+        const uint32_t r = (uint32_t)min(max(taken[g] - P * jj, 0), pv);
+        if (g < 4) w0 |= r << (8 * g);
+        else w1 |= r << (8 * (g - 4));
+      }
+      *reinterpret_cast<int4*>(wlb + v[G] + jj) = make_int4(page0 + jj, blk, (int)w0, (int)w1);
+    }
+    v[G] += u;
   }
   if (tid == 0) {
     if (hk == 0 && b == 0) {
       wl_count[-64] = 0x44534b57;  // "DSKW"
       wl_count[-63] = max_wl;
     }
-    wl_count[(size_t)b * Hkv + hk] = carry[G];
+    wl_count[(size_t)b * Hkv + hk] = tot[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const size_t o = (size_t)b * Hq + hk * G + g;
-      n_sel[o] = carry[g];
+      n_sel[o] = tot[g];
       marg_out[o] = all[g] ? -1 : m[g];
       keep_out[o] = all[g] ? 0 : keep[g];
     }
   }
-}
-
-// ============================================================================
-// a7 + a8: split-K flash-decoding over pages (dense mode: all pages).
-// grid (n_split, Hkv, B); NW consumer warps + 1 producer warp.
-// Producer (one lane): streams each page's valid rows of K and V with TMA 1-D
-// bulk copies (cp.async.bulk, 16-byte multiples, evict-first) into an NS-deep
-// smem ring guarded by full/empty mbarriers.
-// Consumers: warp w serves query head w % G of the group on pages
-// i = w/G (mod NW/G); lane l owns dims [4l, 4l+4).  QK partials of 16 rows
-// are transposed-reduced (16 shuffles), online softmax in the exp2 domain,
-// P.V accumulated in fp32.  Partials (o, lse) of each split go to the
-// workspace; the last CTA of a (b, KV head) merges them in split order.
-// ============================================================================
-DSK_DEVICE float transpose_reduce16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const bool up = lane & 16;
-    const float send = up ? v[k] : v[k + 8];
-    const float keep = up ? v[k + 8] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const bool up = lane & 8;
-    const float send = up ? v[k] : v[k + 4];
-    const float keep = up ? v[k + 4] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const bool up = lane & 4;
-    const float send = up ? v[k] : v[k + 2];
-    const float keep = up ? v[k + 2] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  {
-    const bool up = lane & 2;
-    const float send = up ? v[0] : v[1];
-    const float keep = up ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  return v[0];  // full dot product of row (lane >> 1) & 15
-}
-
-template <typename T, int G, int NW, int NS>
-__global__ void __launch_bounds__((NW + 1) * 32, 3) k_decode_attn(
-    const T* __restrict__ q, const T* __restrict__ Kp, const T* __restrict__ Vp,
-    const int16_t* __restrict__ page_valid, const int32_t* __restrict__ n_pages,
-    const int32_t* __restrict__ wl_hdr, const int32_t* __restrict__ wl_count,
-    const WLEntry* __restrict__ wl, int dense,
-    int Hq, int Hkv, int max_pages, int P, float scale_log2, float* __restrict__ part_o,
-    float* __restrict__ part_lse, int* __restrict__ counters, int n_split, float* __restrict__ o,
-    float* __restrict__ lse) {
-  constexpr int NIL = NW / G;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int stage_elems = P * kD;
-  T* smK = reinterpret_cast<T*>(smem);
-  T* smV = smK + (size_t)NS * stage_elems;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smV + (size_t)NS * stage_elems);
-  uint64_t* empty = full + NS;
-  uint8_t(*s_rows)[kMaxG] = reinterpret_cast<uint8_t(*)[kMaxG]>(empty + NS);
-  float* scratch = reinterpret_cast<float*>(s_rows + NS);  // NW * (kD + 2)
-  __shared__ int s_last;
-
-  const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bh = b * Hkv + hk;
-  const int cnt = dense ? n_pages[b] : wl_count[bh];
-  const int e_lo = (int)(((long long)split * cnt) / n_split);
-  const int e_hi = (int)(((long long)(split + 1) * cnt) / n_split);
-  const int n_it = e_hi - e_lo;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], G);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == NW) {  // ---------------------------------------------- producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      const int max_wl = dense ? 0 : wl_hdr[1];
-      const WLEntry* wlb = wl + (size_t)bh * max_wl;
-      const size_t head_base = (size_t)bh * max_pages;
-      for (int i = 0; i < n_it; ++i) {
-        const int st = i % NS;
-        if (i >= NS) mbar_wait(&empty[st], ((i / NS) - 1) & 1);
-        int page;
-        uint8_t rows[kMaxG];
-        if (dense) {
-          page = e_lo + i;
-          const int pv = page_valid[(size_t)b * max_pages + page];
-#pragma unroll
-          for (int g = 0; g < kMaxG; ++g) rows[g] = (uint8_t)pv;
-        } else {
-          const WLEntry e = wlb[e_lo + i];
-          page = e.page;
-#pragma unroll
-          for (int g = 0; g < kMaxG; ++g) rows[g] = e.rows[g];
-        }
-        int rmax = 0;
-#pragma unroll
-        for (int g = 0; g < G; ++g) rmax = max(rmax, (int)rows[g]);
-#pragma unroll
-        for (int g = 0; g < kMaxG; ++g) s_rows[st][g] = rows[g];
-        const uint32_t bytes = (uint32_t)rmax * kD * sizeof(T);
-        mbar_arrive_expect_tx(&full[st], 2 * bytes);
-        if (bytes) {
-          const size_t off = (head_base + page) * (size_t)stage_elems;
-          bulk_g2s(smK + (size_t)st * stage_elems, Kp + off, bytes, &full[st], pol);
-          bulk_g2s(smV + (size_t)st * stage_elems, Vp + off, bytes, &full[st], pol);
-        }
-      }
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------------ consumers
-  const int gj = warp % G, il = warp / G;
-  const int h = hk * G + gj;
-  float qv[4];
-  Vec<T>::load4(q + ((size_t)b * Hq + h) * kD + lane * 4, qv);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) qv[k] *= scale_log2;
-  float m = -CUDART_INF_F, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  const int myr = (lane >> 1) & 15;
-
-  for (int i = il; i < n_it; i += NIL) {
-    const int st = i % NS;
-    mbar_wait(&full[st], (i / NS) & 1);
-    const int rows = s_rows[st][gj];
-    const T* Ks = smK + (size_t)st * stage_elems;
-    const T* Vs = smV + (size_t)st * stage_elems;
-    for (int r0 = 0; r0 < rows; r0 += 16) {
-      const int nr = min(16, rows - r0);
-      float part[16];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        if (r < nr) {
-          float kv[4];
-          Vec<T>::load4(Ks + (r0 + r) * kD + lane * 4, kv);
-          part[r] = qv[0] * kv[0] + qv[1] * kv[1] + qv[2] * kv[2] + qv[3] * kv[3];
-        } else {
-          part[r] = 0.f;
-        }
-      }
-      float z = transpose_reduce16(part, lane);
-      z = (myr < nr) ? z : -CUDART_INF_F;
-      float mx = z;
-#pragma unroll
-      for (int o2 = 2; o2 < 32; o2 <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
-      const float mnew = fmaxf(m, mx);
-      const float p = (myr < nr) ? exp2f(z - mnew) : 0.f;
-      float ps = p;
-#pragma unroll
-      for (int o2 = 2; o2 < 32; o2 <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o2);
-      const float corr = exp2f(m - mnew);
-      l = l * corr + ps;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k] *= corr;
-      m = mnew;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        if (r < nr) {
-          const float pr = __shfl_sync(0xffffffffu, p, 2 * r);
-          float vv[4];
-          Vec<T>::load4(Vs + (r0 + r) * kD + lane * 4, vv);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] += pr * vv[k];
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
-
-  // merge the NIL page-interleaved warps of each head (fixed order)
-  if (NIL > 1) {
-    float* red = scratch + warp * (kD + 2);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) red[lane * 4 + k] = acc[k];
-    if (lane == 0) {
-      red[kD] = m;
-      red[kD + 1] = l;
-    }
-    named_bar_sync(1, NW * 32);
-    if (il == 0) {
-      for (int j = 1; j < NIL; ++j) {
-        const float* o2 = scratch + (j * G + gj) * (kD + 2);
-        const float m2 = o2[kD], l2 = o2[kD + 1];
-        const float mn = fmaxf(m, m2);
-        const float c1 = (mn == -CUDART_INF_F) ? 0.f : exp2f(m - mn);
-        const float c2 = (mn == -CUDART_INF_F) ? 0.f : exp2f(m2 - mn);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] = acc[k] * c1 + o2[lane * 4 + k] * c2;
-        l = l * c1 + l2 * c2;
-        m = mn;
-      }
-    }
-  }
-
-  const float LN2 = 0.69314718055994530942f;
-  const size_t row = (size_t)b * Hq + h;
-  if (n_split == 1) {
-    if (il == 0) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      float4 ov = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-      reinterpret_cast<float4*>(o + row * kD)[lane] = ov;
-      if (lane == 0) lse[row] = l > 0.f ? (m + log2f(l)) * LN2 : -CUDART_INF_F;
-    }
-    return;
-  }
-  if (il == 0) {
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    float4 ov = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    reinterpret_cast<float4*>(part_o + (row * n_split + split) * kD)[lane] = ov;
-    if (lane == 0) part_lse[row * n_split + split] = l > 0.f ? (m + log2f(l)) * LN2 : -CUDART_INF_F;
-  }
-  __threadfence();
-  named_bar_sync(1, NW * 32);
-  if (threadIdx.x == 0) s_last = (atomicAdd(&counters[bh], 1) == n_split - 1);
-  named_bar_sync(1, NW * 32);
-  if (!s_last) return;
-  __threadfence();
-  if (il == 0) {
-    const float* pl = part_lse + row * n_split;
-    float M = -CUDART_INF_F;
-    for (int s = 0; s < n_split; ++s) M = fmaxf(M, __ldcg(pl + s));
-    float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
-    float L = -CUDART_INF_F;
-    if (M != -CUDART_INF_F) {
-      float sum = 0.f;
-      for (int s = 0; s < n_split; ++s) sum += expf(__ldcg(pl + s) - M);
-      L = M + logf(sum);
-      for (int s = 0; s < n_split; ++s) {
-        const float w = expf(__ldcg(pl + s) - L);
-        const float4 po = __ldcg(reinterpret_cast<const float4*>(part_o + (row * n_split + s) * kD) + lane);
-        ov.x += w * po.x;
-        ov.y += w * po.y;
-        ov.z += w * po.z;
-        ov.w += w * po.w;
-      }
-    }
-    reinterpret_cast<float4*>(o + row * kD)[lane] = ov;
-    if (lane == 0) lse[row] = L;
-  }
-  if (threadIdx.x == 0) counters[bh] = 0;
 }
 
 // ============================================================================
@@ -724,70 +481,6 @@ cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const i
   }
 #undef DSK_UNION
   return post_launch(__func__, st);
-}
-
-constexpr int kStages = 8;
-
-template <typename T, int G, int NW>
-static cudaError_t decode_attn_t(const void* q, const void* Kp, const void* Vp, const int16_t* pv,
-                                 const int32_t* n_pages, const int32_t* wl_hdr,
-                                 const int32_t* wl_count, const WLEntry* wl, int dense, int B, int Hq, int Hkv, int max_pages, int P,
-                                 float scale_log2, float* part_o, float* part_lse, int* counters,
-                                 int n_split, float* o, float* lse, cudaStream_t st) {
-  constexpr int NS = (sizeof(T) == 2) ? kStages : kStages / 2;
-  auto kern = k_decode_attn<T, G, NW, NS>;
-  const size_t smem = (size_t)2 * NS * P * kD * sizeof(T) + 2 * NS * sizeof(uint64_t) +
-                      NS * kMaxG + (size_t)NW * (kD + 2) * sizeof(float) + 64;
-  static bool attr_done = false;
-  if (!attr_done) {
-    allow_max_dyn_smem(kern);
-    attr_done = true;
-  }
-  kern<<<dim3(n_split, Hkv, B), (NW + 1) * 32, smem, st>>>(
-      static_cast<const T*>(q), static_cast<const T*>(Kp), static_cast<const T*>(Vp), pv, n_pages,
-      wl_hdr, wl_count, wl, dense, Hq, Hkv, max_pages, P, scale_log2, part_o, part_lse, counters,
-      n_split, o, lse);
-  return post_launch(__func__, st);
-}
-
-template <typename T>
-static cudaError_t decode_attn_g(int G, const void* q, const void* Kp, const void* Vp,
-                                 const int16_t* pv, const int32_t* n_pages, const int32_t* wl_hdr,
-                                 const int32_t* wl_count, const WLEntry* wl, int dense, int B, int Hq, int Hkv,
-                                 int max_pages, int P, float scale_log2, float* part_o,
-                                 float* part_lse, int* counters, int n_split, float* o, float* lse,
-                                 cudaStream_t st) {
-#define DSK_ARGS q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv, max_pages, P, \
-                 scale_log2, part_o, part_lse, counters, n_split, o, lse, st
-  switch (G) {
-    case 1: return decode_attn_t<T, 1, 4>(DSK_ARGS);
-    case 2: return decode_attn_t<T, 2, 4>(DSK_ARGS);
-    case 4: return decode_attn_t<T, 4, 4>(DSK_ARGS);
-    case 8: return decode_attn_t<T, 8, 8>(DSK_ARGS);
-    default: return cudaErrorInvalidValue;
-  }
-#undef DSK_ARGS
-}
-
-int decode_n_split(int B, int Hkv) {
-  const int sms = num_sms();
-  int n = (sms * 3 + B * Hkv - 1) / (B * Hkv);
-  return max(1, min(kMaxSplit, n));
-}
-
-cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, const void* Vp,
-                               const int16_t* pv, const int32_t* n_pages, const int32_t* wl_hdr,
-                               const int32_t* wl_count, const WLEntry* wl, int dense, int B, int Hq, int Hkv,
-                               int max_pages, int P, float scale, float* part_o, float* part_lse,
-                               int* counters, int n_split, float* o, float* lse, cudaStream_t st) {
-  const float scale_log2 = scale * 1.4426950408889634f;
-  if (dtype == 0)
-    return decode_attn_g<bf16>(G, q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
-                               max_pages, P, scale_log2, part_o, part_lse, counters, n_split, o, lse,
-                               st);
-  return decode_attn_g<float>(G, q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
-                              max_pages, P, scale_log2, part_o, part_lse, counters, n_split, o, lse,
-                              st);
 }
 
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,

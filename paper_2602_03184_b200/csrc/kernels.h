@@ -25,7 +25,6 @@ inline void allow_max_dyn_smem(F* kern) {
 // attributed to the launcher that caused them.  Errors are recorded for
 // dynsplit_last_error().
 cudaError_t post_launch(const char* where, cudaStream_t st);
-int decode_n_split(int B, int Hkv);
 size_t select_threshold_smem(int maxb);
 
 // decode (decode_kernels.cu)
@@ -40,7 +39,7 @@ cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, 
                                const int16_t* pv, const int32_t* n_pages, const int32_t* wl_hdr,
                                const int32_t* wl_count, const WLEntry* wl, int dense, int B, int Hq, int Hkv,
                                int max_pages, int P, float scale, float* part_o, float* part_lse,
-                               int* counters, int n_split, float* o, float* lse, cudaStream_t st);
+                               int* counters, float* o, float* lse, cudaStream_t st);
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,
                          float* o, float* lse, cudaStream_t st);
 
