@@ -374,15 +374,15 @@ dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* s, const dynsp
   if (blk_lo < 0 || blk_hi < blk_lo) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < select_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   const int maxb = dynsplit_max_blocks(s->S, c);
-  if (select_threshold_smem(maxb) > 227 * 1024) return DYNSPLIT_ERR_UNSUPPORTED;
-  char* w = static_cast<char*>(ws);
-  int4* sel_info = reinterpret_cast<int4*>(w + align_up((size_t)s->B * s->Hq * maxb * 4));
+  // smem-resident keys (S up to ~300K), 8-bit page counts per block, 16-bit block lengths
+  if (select_smem_needed(maxb, s->Hq / s->Hkv) == (size_t)-1) return DYNSPLIT_ERR_UNSUPPORTED;
+  if ((c->C + c->delta + c->page_size - 1) / c->page_size > 255) return DYNSPLIT_ERR_UNSUPPORTED;
   WorklistView v = worklist_view(worklist, s);
   return cuda_status(launch_select(s->Hq / s->Hkv, scores, block_starts, n_blocks, page_first, s->B,
                                    s->Hq, s->Hkv, maxb, dynsplit_max_selected(budget, s->S, c),
                                    max_wl_of(s, c, budget), c->page_size, budget, blk_lo, blk_hi,
-                                   sel_info, sel_blocks, n_sel, marginal_block, marginal_keep,
-                                   v.count, v.entries, static_cast<cudaStream_t>(stream)));
+                                   sel_blocks, n_sel, marginal_block, marginal_keep, v.count,
+                                   v.entries, static_cast<cudaStream_t>(stream)));
 }
 
 dynsplit_status dynsplit_select(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,

@@ -30,15 +30,8 @@
 namespace dsk {
 
 constexpr int kScStride = kD + 4;  // merge scratch row: acc[kD], m, l (16-byte aligned rows)
+constexpr int kMinPagesPerSplit = 4;
 
-DSK_DEVICE float fma_bf16(unsigned short a, unsigned short b, float c) {
-  float r;
-  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(r) : "h"(a), "h"(b), "f"(c));
-  return r;
-}
-DSK_DEVICE void split_bf16x2(uint32_t w, unsigned short& lo, unsigned short& hi) {
-  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
-}
 DSK_DEVICE uint64_t pack2(float x, float y) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
@@ -107,8 +100,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = b * Hkv + hk;
   const int cnt = dense ? n_pages[b] : wl_count[bh];
-  const int e_lo = (int)(((long long)split * cnt) / n_split);
-  const int e_hi = (int)(((long long)(split + 1) * cnt) / n_split);
+  // splits actually used by this (b, KV head): at least kMinPagesPerSplit pages each
+  const int n_eff = max(1, min(n_split, (cnt + kMinPagesPerSplit - 1) / kMinPagesPerSplit));
+  if (split >= n_eff) return;
+  const int e_lo = (int)(((long long)split * cnt) / n_eff);
+  const int e_hi = (int)(((long long)(split + 1) * cnt) / n_eff);
   const int n_it = e_hi - e_lo;
 
   if (threadIdx.x == 0) {
@@ -317,7 +313,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
     const float4 o4 = make_float4(ov[0] * inv, ov[1] * inv, ov[2] * inv, ov[3] * inv);
     const float lse2 = L > 0.f ? (M + log2f(L)) * LN2 : -CUDART_INF_F;
     const size_t row = (size_t)b * Hq + hk * G + h;
-    if (n_split == 1) {
+    if (n_eff == 1) {
       reinterpret_cast<float4*>(o + row * kD)[lane] = o4;
       if (lane == 0) lse[row] = lse2;
     } else {
@@ -325,31 +321,48 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
       if (lane == 0) part_lse[row * n_split + split] = lse2;
     }
   }
-  if (n_split == 1) return;
+  if (n_eff == 1) return;
   __threadfence();
   named_bar_sync(1, NW * 32);
-  if (threadIdx.x == 0) s_last = (atomicAdd(&counters[bh], 1) == n_split - 1);
+  if (threadIdx.x == 0) s_last = (atomicAdd(&counters[bh], 1) == n_eff - 1);
   named_bar_sync(1, NW * 32);
   if (!s_last) return;
   __threadfence();
+  // Last CTA of (b, KV head): LSE merge of the n_eff splits.  Lanes hold the
+  // split lse values (n_eff <= 64), weights by warp reductions (fixed
+  // butterfly order), then o = sum_s w_s o_s in split order with 8 loads in
+  // flight per lane.
   for (int h = warp; h < G; h += NW) {
     const size_t row = (size_t)b * Hq + hk * G + h;
     const float* pl = part_lse + row * n_split;
-    float M = -CUDART_INF_F;
-    for (int s = 0; s < n_split; ++s) M = fmaxf(M, __ldcg(pl + s));
+    const float l0 = lane < n_eff ? __ldcg(pl + lane) : -CUDART_INF_F;
+    const float l1 = lane + 32 < n_eff ? __ldcg(pl + lane + 32) : -CUDART_INF_F;
+    const float M = warp_max(fmaxf(l0, l1));
     float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
     float L = -CUDART_INF_F;
     if (M != -CUDART_INF_F) {
-      float sum = 0.f;
-      for (int s = 0; s < n_split; ++s) sum += expf(__ldcg(pl + s) - M);
+      const float sum = warp_sum(expf(l0 - M) + expf(l1 - M));
       L = M + logf(sum);
-      for (int s = 0; s < n_split; ++s) {
-        const float w = expf(__ldcg(pl + s) - L);
-        const float4 po = __ldcg(reinterpret_cast<const float4*>(part_o + (row * n_split + s) * kD) + lane);
-        ov.x += w * po.x;
-        ov.y += w * po.y;
-        ov.z += w * po.z;
-        ov.w += w * po.w;
+      const float w0 = expf(l0 - L), w1 = expf(l1 - L);
+      const float4* po_base = reinterpret_cast<const float4*>(part_o + row * n_split * kD) + lane;
+      for (int s0 = 0; s0 < n_eff; s0 += 8) {
+        float4 po[8];
+        float w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int s = s0 + k;
+          w[k] = __shfl_sync(0xffffffffu, s < 32 ? w0 : w1, s & 31);
+          po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (s0 + k < n_eff) {
+            ov.x += w[k] * po[k].x;
+            ov.y += w[k] * po[k].y;
+            ov.z += w[k] * po[k].z;
+            ov.w += w[k] * po[k].w;
+          }
+        }
       }
     }
     reinterpret_cast<float4*>(o + row * kD)[lane] = ov;

@@ -62,6 +62,17 @@ template <> struct Vec<float> {
   }
 };
 
+// bf16 x bf16 -> fp32 fused multiply-add (FHFMA.BF16; the product is exact).
+DSK_DEVICE float fma_bf16(unsigned short a, unsigned short b, float c) {
+  float r;
+  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(r) : "h"(a), "h"(b), "f"(c));
+  return r;
+}
+// halves of a packed bf16x2 word (free: becomes .H0/.H1 operand selectors)
+DSK_DEVICE void split_bf16x2(uint32_t w, unsigned short& lo, unsigned short& hi) {
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+}
+
 // Order-preserving map fp32 -> uint32 (larger float -> larger key).
 DSK_DEVICE uint32_t float_key(float f) {
   uint32_t u = __float_as_uint(f);
@@ -92,6 +103,39 @@ DSK_DEVICE int warp_incl_scan(int v) {
     if (lane >= o) v += t;
   }
   return v;
+}
+
+// Block-wide exclusive scan of N ints per thread (NT threads); tot = totals.
+// sm: (NT/32 + 1) * N ints of shared memory.  Contains __syncthreads.
+template <int N, int NT>
+DSK_DEVICE void block_excl_scan(int (&v)[N], int (&tot)[N], int* sm) {
+  constexpr int NWARP = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) inc[k] = warp_incl_scan(v[k]);
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) sm[warp * N + k] = inc[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int x = lane < NWARP ? sm[lane * N + k] : 0;
+      const int s = warp_incl_scan(x);
+      if (lane < NWARP) sm[lane * N + k] = s - x;
+      if (lane == NWARP - 1) sm[NWARP * N + k] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int ex = sm[warp * N + k] + inc[k] - v[k];
+    tot[k] = sm[NWARP * N + k];
+    v[k] = ex;
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- smem / mbarrier / bulk copy

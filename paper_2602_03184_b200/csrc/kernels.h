@@ -25,14 +25,13 @@ inline void allow_max_dyn_smem(F* kern) {
 // attributed to the launcher that caused them.  Errors are recorded for
 // dynsplit_last_error().
 cudaError_t post_launch(const char* where, cudaStream_t st);
-size_t select_threshold_smem(int maxb);
-
-// decode (decode_kernels.cu)
+// decode (decode_kernels.cu, select_kernels.cu, attn_kernels.cu)
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
                                 float* scores, int B, int Hq, int Hkv, int maxb, cudaStream_t st);
+size_t select_smem_needed(int maxb, int G);  // (size_t)-1 if it cannot fit
 cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const int32_t* nb,
                           const int32_t* pf, int B, int Hq, int Hkv, int maxb, int max_sel,
-                          int max_wl, int P, int budget, int blk_lo, int blk_hi, int4* sel_info,
+                          int max_wl, int P, int budget, int blk_lo, int blk_hi,
                           int32_t* sel_blocks, int32_t* n_sel, int32_t* marg, int32_t* keep,
                           int32_t* wl_count, WLEntry* wl, cudaStream_t st);
 cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, const void* Vp,
