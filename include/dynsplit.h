@@ -76,7 +76,7 @@ typedef struct {
   int32_t delta;           /* maximum deviation Delta; 14 */
   int32_t lambda_num;      /* DD-Select mix lambda = num/den ("alpha"); 1/2 */
   int32_t lambda_den;
-  int32_t page_size;       /* P: fixed page length of the uniform mapping; 16 */
+  int32_t page_size;       /* P: fixed page length of the uniform mapping; 16 (power of 2, <= 64) */
 } dynsplit_config;
 
 /* Fills the defaults above. */

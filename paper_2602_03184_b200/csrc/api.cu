@@ -90,7 +90,8 @@ dynsplit_status check_cfg(const dynsplit_config* c) {
   if (c->C + c->delta > 65535) return DYNSPLIT_ERR_UNSUPPORTED;
   if (c->lambda_den < 1 || c->lambda_num < 0 || c->lambda_num > c->lambda_den)
     return DYNSPLIT_ERR_INVALID_ARGUMENT;
-  if (c->page_size < 1 || c->page_size > 64) return DYNSPLIT_ERR_UNSUPPORTED;
+  if (c->page_size < 1 || c->page_size > 64 || (c->page_size & (c->page_size - 1)))
+    return DYNSPLIT_ERR_UNSUPPORTED;  // P: power of two in [1, 64]
   if (c->W < 1 || c->R < 1 || !(c->alpha_pen >= 0.f)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return DYNSPLIT_OK;
 }
