@@ -26,6 +26,10 @@ HEADERS = ["common.cuh", "kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
+if os.environ.get("DYNSPLIT_DEBUG_BUILD"):   # phase timestamps / experiment switches
+    NVCC_FLAGS += ["-DDSK_DEBUG"]
+    BUILD = BUILD + "_debug"
+    LIB = os.path.join(LIBDIR, "libdynsplit_debug.so")
 
 
 def nvcc() -> str:

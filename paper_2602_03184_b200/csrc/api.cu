@@ -42,6 +42,15 @@ int max_smem_optin() {
   return cached;
 }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("DYNSPLIT_NO_PDL");
+    on = (e && *e && *e != '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 static thread_local char g_last_error[512] = "";
 const char* last_error();
 

@@ -26,11 +26,28 @@
 #include "kernels.h"
 
 #include <math_constants.h>
+#include <stdlib.h>
 
 namespace dsk {
 
 constexpr int kScStride = kD + 4;  // merge scratch row: acc[kD], m, l (16-byte aligned rows)
 constexpr int kMinPagesPerSplit = 4;
+
+// Optional per-CTA phase timestamps (debug only; dynsplit_debug_attn_timer).
+__device__ unsigned long long* g_attn_dbg = nullptr;
+__device__ int g_attn_nocompute = 0;  // debug: stream pages without computing
+DSK_DEVICE void astamp(int k) {
+#ifdef DSK_DEBUG
+  if (g_attn_dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const size_t cta = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    g_attn_dbg[cta * 8 + k] = t;
+  }
+#else
+  (void)k;
+#endif
+}
 
 DSK_DEVICE uint64_t pack2(float x, float y) {
   uint64_t r;
@@ -76,7 +93,7 @@ template <> struct QK<float> {
 };
 
 template <typename T, int G, int NW, int NS>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
+__global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
     const T* __restrict__ q, const T* __restrict__ Kp, const T* __restrict__ Vp,
     const int16_t* __restrict__ page_valid, const int32_t* __restrict__ n_pages,
     const int32_t* __restrict__ wl_hdr, const int32_t* __restrict__ wl_count,
@@ -99,14 +116,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
   const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = b * Hkv + hk;
-  const int cnt = dense ? n_pages[b] : wl_count[bh];
-  // splits actually used by this (b, KV head): at least kMinPagesPerSplit pages each
-  const int n_eff = max(1, min(n_split, (cnt + kMinPagesPerSplit - 1) / kMinPagesPerSplit));
-  if (split >= n_eff) return;
-  const int e_lo = (int)(((long long)split * cnt) / n_eff);
-  const int e_hi = (int)(((long long)(split + 1) * cnt) / n_eff);
-  const int n_it = e_hi - e_lo;
 
+  if (threadIdx.x == 0) astamp(0);
+  // prologue independent of the preceding kernel (PDL overlap): barriers, q
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -119,28 +131,46 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
     const uint4* src = reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD);
     for (int c = threadIdx.x; c < QCH; c += blockDim.x) reinterpret_cast<uint4*>(s_q)[c] = src[c];
   }
+  pdl_trigger();
+  pdl_wait();  // the worklist is the previous kernel's output
+  if (threadIdx.x == 0) astamp(1);
+
+  const int cnt = dense ? n_pages[b] : wl_count[bh];
+  // splits actually used by this (b, KV head): at least kMinPagesPerSplit pages each
+  const int n_eff = max(1, min(n_split, (cnt + kMinPagesPerSplit - 1) / kMinPagesPerSplit));
+  if (split >= n_eff) return;
+  const int e_lo = (int)(((long long)split * cnt) / n_eff);
+  const int e_hi = (int)(((long long)(split + 1) * cnt) / n_eff);
+  const int n_it = e_hi - e_lo;
+
+  // producer warp: first batch of 32 worklist entries before the CTA barrier
+  const int max_wl = dense ? 0 : wl_hdr[1];
+  const WLEntry* wlb = wl + (size_t)bh * max_wl + e_lo;
+  auto load_entry = [&](int idx, int& page, uint32_t& r0, uint32_t& r1) {
+    page = 0;
+    r0 = r1 = 0;
+    if (idx < n_it) {
+      if (dense) {
+        page = e_lo + idx;
+        const uint32_t pv = (uint32_t)page_valid[(size_t)b * max_pages + page];
+        r0 = r1 = pv * 0x01010101u;
+      } else {
+        const int4 e = *reinterpret_cast<const int4*>(wlb + idx);
+        page = e.x;
+        r0 = (uint32_t)e.z;
+        r1 = (uint32_t)e.w;
+      }
+    }
+  };
+  int page = 0;
+  uint32_t r0 = 0, r1 = 0;
+  if (warp == NW) load_entry(lane, page, r0, r1);
   __syncthreads();
 
   if (warp == NW) {  // ---------------------------------------------- producer
     const uint64_t pol = policy_evict_first();
-    const int max_wl = dense ? 0 : wl_hdr[1];
-    const WLEntry* wlb = wl + (size_t)bh * max_wl + e_lo;
     for (int base = 0; base < n_it; base += 32) {
-      const int idx = base + lane;
-      int page = 0;
-      uint32_t r0 = 0, r1 = 0;
-      if (idx < n_it) {
-        if (dense) {
-          page = e_lo + idx;
-          const uint32_t pv = (uint32_t)page_valid[(size_t)b * max_pages + page];
-          r0 = r1 = pv * 0x01010101u;
-        } else {
-          const int4 e = *reinterpret_cast<const int4*>(wlb + idx);
-          page = e.x;
-          r0 = (uint32_t)e.z;
-          r1 = (uint32_t)e.w;
-        }
-      }
+      if (base) load_entry(base + lane, page, r0, r1);
       const int nk = min(32, n_it - base);
       for (int k = 0; k < nk; ++k) {
         const int i = base + k, st = i % NS;
@@ -189,6 +219,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
   for (int i = warp; i < n_it; i += NW) {
     const int st = i % NS;
     mbar_wait(&full[st], (i / NS) & 1);
+    if (threadIdx.x == 0 && i == 0) astamp(2);
+#ifdef DSK_DEBUG
+    if (g_attn_nocompute) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      continue;
+    }
+#endif
     const uint32_t ra = s_rows[st][0], rc = s_rows[st][1];
     int rmax = 0, myrows[HPL];
 #pragma unroll
@@ -276,6 +314,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
 
   // ---- merge the NW warps (fixed order); the ring is free once all are here
   named_bar_sync(1, NW * 32);
+  if (threadIdx.x == 0) astamp(3);
   float* sc = reinterpret_cast<float*>(smem);  // [NW][G][kD + 2]
 #pragma unroll
   for (int h = 0; h < G; ++h)
@@ -322,21 +361,32 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
     }
   }
   if (n_eff == 1) return;
-  __threadfence();
+  // Split ticket: the CTA barrier orders every thread's partial writes before
+  // thread 0's acq_rel atomic (cumulative release at gpu scope); the last CTA
+  // acquires them through the same atomic (no full fences).
   named_bar_sync(1, NW * 32);
-  if (threadIdx.x == 0) s_last = (atomicAdd(&counters[bh], 1) == n_eff - 1);
+  if (threadIdx.x == 0) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(counters + bh) : "memory");
+    s_last = (old == n_eff - 1);
+  }
   named_bar_sync(1, NW * 32);
+  if (threadIdx.x == 0) astamp(4);
   if (!s_last) return;
-  __threadfence();
   // Last CTA of (b, KV head): LSE merge of the n_eff splits.  Lanes hold the
   // split lse values (n_eff <= 64), weights by warp reductions (fixed
-  // butterfly order), then o = sum_s w_s o_s in split order with 8 loads in
-  // flight per lane.
+  // butterfly order), then o = sum_s w_s o_s in split order, 16 loads in
+  // flight per lane (the first batch issued before the weights are known).
   for (int h = warp; h < G; h += NW) {
     const size_t row = (size_t)b * Hq + hk * G + h;
     const float* pl = part_lse + row * n_split;
+    const float4* po_base = reinterpret_cast<const float4*>(part_o + row * n_split * kD) + lane;
     const float l0 = lane < n_eff ? __ldcg(pl + lane) : -CUDART_INF_F;
     const float l1 = lane + 32 < n_eff ? __ldcg(pl + lane + 32) : -CUDART_INF_F;
+    float4 po[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      po[k] = k < n_eff ? __ldcg(po_base + (size_t)k * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float M = warp_max(fmaxf(l0, l1));
     float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
     float L = -CUDART_INF_F;
@@ -344,23 +394,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
       const float sum = warp_sum(expf(l0 - M) + expf(l1 - M));
       L = M + logf(sum);
       const float w0 = expf(l0 - L), w1 = expf(l1 - L);
-      const float4* po_base = reinterpret_cast<const float4*>(part_o + row * n_split * kD) + lane;
-      for (int s0 = 0; s0 < n_eff; s0 += 8) {
-        float4 po[8];
-        float w[8];
+      for (int s0 = 0; s0 < n_eff; s0 += 16) {
+        if (s0) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int s = s0 + k;
-          w[k] = __shfl_sync(0xffffffffu, s < 32 ? w0 : w1, s & 31);
-          po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 0; k < 16; ++k) {
+            const int s = s0 + k;
+            po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (s0 + k < n_eff) {
-            ov.x += w[k] * po[k].x;
-            ov.y += w[k] * po[k].y;
-            ov.z += w[k] * po[k].z;
-            ov.w += w[k] * po[k].w;
+        for (int k = 0; k < 16; ++k) {
+          const int s = s0 + k;
+          const float w = __shfl_sync(0xffffffffu, s < 32 ? w0 : w1, s & 31);
+          if (s < n_eff) {
+            ov.x += w * po[k].x;
+            ov.y += w * po[k].y;
+            ov.z += w * po[k].z;
+            ov.w += w * po[k].w;
           }
         }
       }
@@ -368,33 +418,43 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_decode_attn(
     reinterpret_cast<float4*>(o + row * kD)[lane] = ov;
     if (lane == 0) lse[row] = L;
   }
-  if (threadIdx.x == 0) counters[bh] = 0;
+  if (threadIdx.x == 0) {
+    counters[bh] = 0;
+    astamp(5);
+  }
 }
 
 // ============================================================================
 // host launcher
 // ============================================================================
-constexpr int kNW = 4;
-
-template <typename T, int G>
+template <typename T, int G, int NW, int NS>
 static size_t attn_smem(int P) {
-  constexpr int NS = sizeof(T) == 2 ? 8 : 4;
   const size_t ring = (size_t)2 * NS * P * kD * sizeof(T);
-  const size_t merge = (size_t)kNW * G * kScStride * sizeof(float);
+  const size_t merge = (size_t)NW * G * kScStride * sizeof(float);
   return (ring > merge ? ring : merge) + 2 * NS * sizeof(uint64_t) + NS * 8 +
-         (size_t)G * kD * sizeof(T) + (size_t)kNW * 16 * G * sizeof(float2);
+         (size_t)G * kD * sizeof(T) + (size_t)NW * 16 * G * sizeof(float2);
 }
 
-template <typename T, int G>
+// Consumer warps per CTA: DYNSPLIT_ATTN_NW in {4, 8} (default 4: more CTAs beat more warps).
+static int attn_nw() {
+  static int nw = 0;
+  if (!nw) {
+    const char* e = getenv("DYNSPLIT_ATTN_NW");
+    nw = (e && atoi(e) == 8) ? 8 : 4;
+  }
+  return nw;
+}
+
+template <typename T, int G, int NW>
 struct AttnLaunch {
   static constexpr int NS = sizeof(T) == 2 ? 8 : 4;
   static int occupancy(int P) {
     static int occ = 0, lastP = -1;
     if (occ == 0 || lastP != P) {
-      auto kern = k_decode_attn<T, G, kNW, NS>;
+      auto kern = k_decode_attn<T, G, NW, NS>;
       allow_max_dyn_smem(kern);
       int n = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (kNW + 1) * 32, attn_smem<T, G>(P)) !=
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (NW + 1) * 32, attn_smem<T, G, NW, NS>(P)) !=
               cudaSuccess ||
           n < 1) {
         cudaGetLastError();
@@ -412,13 +472,35 @@ struct AttnLaunch {
                          float* o, float* lse, cudaStream_t st) {
     const int occ = occupancy(P);
     const int n_split = max(1, min(kMaxSplit, (num_sms() * occ) / max(1, B * Hkv)));
-    k_decode_attn<T, G, kNW, NS><<<dim3(n_split, Hkv, B), (kNW + 1) * 32, attn_smem<T, G>(P), st>>>(
-        static_cast<const T*>(q), static_cast<const T*>(Kp), static_cast<const T*>(Vp), pv, n_pages,
-        wl_hdr, wl_count, wl, dense, Hq, Hkv, max_pages, P, scale_log2, part_o, part_lse, counters,
-        n_split, o, lse);
+    launch_ex(k_decode_attn<T, G, NW, NS>, dim3(n_split, Hkv, B), dim3((NW + 1) * 32),
+              attn_smem<T, G, NW, NS>(P), st, 1, static_cast<const T*>(q), static_cast<const T*>(Kp),
+              static_cast<const T*>(Vp), pv, n_pages, wl_hdr, wl_count, wl, dense, Hq, Hkv,
+              max_pages, P, scale_log2, part_o, part_lse, counters, n_split, o, lse);
     return post_launch("k_decode_attn", st);
   }
 };
+
+template <typename T, int G>
+static cudaError_t attn_run(const void* q, const void* Kp, const void* Vp, const int16_t* pv,
+                            const int32_t* n_pages, const int32_t* wl_hdr, const int32_t* wl_count,
+                            const WLEntry* wl, int dense, int B, int Hq, int Hkv, int max_pages, int P,
+                            float sl2, float* part_o, float* part_lse, int* counters, float* o,
+                            float* lse, cudaStream_t st) {
+  if (attn_nw() == 4)
+    return AttnLaunch<T, G, 4>::run(q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
+                                    max_pages, P, sl2, part_o, part_lse, counters, o, lse, st);
+  return AttnLaunch<T, G, 8>::run(q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
+                                  max_pages, P, sl2, part_o, part_lse, counters, o, lse, st);
+}
+
+}  // namespace dsk
+extern "C" int dynsplit_debug_attn_timer(void* dev_ptr) {
+  return (int)cudaMemcpyToSymbol(dsk::g_attn_dbg, &dev_ptr, sizeof(void*));
+}
+extern "C" int dynsplit_debug_attn_nocompute(int on) {
+  return (int)cudaMemcpyToSymbol(dsk::g_attn_nocompute, &on, sizeof(int));
+}
+namespace dsk {
 
 cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, const void* Vp,
                                const int16_t* pv, const int32_t* n_pages, const int32_t* wl_hdr,
@@ -430,17 +512,17 @@ cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, 
                  part_o, part_lse, counters, o, lse, st
   if (dtype == 0) {
     switch (G) {
-      case 1: return AttnLaunch<bf16, 1>::run(DSK_ARGS);
-      case 2: return AttnLaunch<bf16, 2>::run(DSK_ARGS);
-      case 4: return AttnLaunch<bf16, 4>::run(DSK_ARGS);
-      case 8: return AttnLaunch<bf16, 8>::run(DSK_ARGS);
+      case 1: return attn_run<bf16, 1>(DSK_ARGS);
+      case 2: return attn_run<bf16, 2>(DSK_ARGS);
+      case 4: return attn_run<bf16, 4>(DSK_ARGS);
+      case 8: return attn_run<bf16, 8>(DSK_ARGS);
     }
   } else {
     switch (G) {
-      case 1: return AttnLaunch<float, 1>::run(DSK_ARGS);
-      case 2: return AttnLaunch<float, 2>::run(DSK_ARGS);
-      case 4: return AttnLaunch<float, 4>::run(DSK_ARGS);
-      case 8: return AttnLaunch<float, 8>::run(DSK_ARGS);
+      case 1: return attn_run<float, 1>(DSK_ARGS);
+      case 2: return attn_run<float, 2>(DSK_ARGS);
+      case 4: return attn_run<float, 4>(DSK_ARGS);
+      case 8: return attn_run<float, 8>(DSK_ARGS);
     }
   }
 #undef DSK_ARGS

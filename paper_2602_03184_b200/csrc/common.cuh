@@ -187,6 +187,12 @@ DSK_DEVICE uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Programmatic dependent launch: wait until the preceding kernel in the
+// stream has completed (and its writes are visible) / allow the next kernel
+// to be scheduled.  Both are no-ops for a normal launch.
+DSK_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DSK_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 DSK_DEVICE void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

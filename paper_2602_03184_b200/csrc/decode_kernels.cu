@@ -113,6 +113,10 @@ __global__ void __launch_bounds__(256) k_score_blocks(const T* __restrict__ q,
     if (blk < hi) DD::load_k(dbase + (size_t)blk * 2 * kD + hl * 8, kb[u]);
     else DD::zero_k(kb[u]);
   }
+  // the digests are the resident cache; q (and the scores buffer) belong to
+  // the step -> wait for the preceding kernel (PDL) before touching them
+  pdl_trigger();
+  pdl_wait();
   typename DD::Q qv[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) DD::load_q(q + ((size_t)b * Hq + hk * G + g) * kD + hl * 8, qv[g]);
@@ -184,10 +188,10 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
   const T* qq = static_cast<const T*>(q);
   const T* dd = static_cast<const T*>(dig);
   switch (G) {
-    case 1: k_score_blocks<T, 1><<<grid, 256, 0, st>>>(qq, dd, nb, scores, Hq, Hkv, maxb); break;
-    case 2: k_score_blocks<T, 2><<<grid, 256, 0, st>>>(qq, dd, nb, scores, Hq, Hkv, maxb); break;
-    case 4: k_score_blocks<T, 4><<<grid, 256, 0, st>>>(qq, dd, nb, scores, Hq, Hkv, maxb); break;
-    case 8: k_score_blocks<T, 8><<<grid, 256, 0, st>>>(qq, dd, nb, scores, Hq, Hkv, maxb); break;
+    case 1: launch_ex(k_score_blocks<T, 1>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
+    case 2: launch_ex(k_score_blocks<T, 2>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
+    case 4: launch_ex(k_score_blocks<T, 4>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
+    case 8: launch_ex(k_score_blocks<T, 8>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
     default: return cudaErrorInvalidValue;
   }
   return post_launch(__func__, st);

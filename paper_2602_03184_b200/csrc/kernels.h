@@ -18,7 +18,38 @@ inline void allow_max_dyn_smem(F* kern) {
     cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          max_smem_optin() - (int)a.sharedSizeBytes);
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                       cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaGetLastError();
+}
+// Launch with programmatic stream serialization (PDL) and an optional
+// cluster shape; DYNSPLIT_NO_PDL=1 disables PDL (A/B measurements).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 // After every launch: returns cudaGetLastError(); with DYNSPLIT_DEBUG=1 in the
 // environment also synchronises the stream so asynchronous faults are

@@ -7,7 +7,7 @@
 // keeps its first `need` tokens (identical to the per-token stable sort of
 // the oracle).
 //
-// One thread-block cluster of G CTAs (1024 threads each) per (b, KV head);
+// One thread-block cluster of G CTAs (512 threads each) per (b, KV head);
 // CTA c of the cluster owns query head hk*G + c:
 //   1. block lengths -> smem (all blocks), total;
 //   2. the head's marginal block, exactly:
@@ -35,11 +35,25 @@ namespace cg = cooperative_groups;
 
 namespace dsk {
 
-constexpr int kSelNT = 1024;
+constexpr int kSelNT = 512;
 constexpr int kSelW = kSelNT / 32;
 constexpr int kBkt = 2048;
 constexpr int kBPT = kBkt / kSelNT;
 constexpr int kCap = 512;
+
+// Optional phase timestamps (debug only; set by dynsplit_debug_select_timer).
+__device__ unsigned long long* g_sel_dbg = nullptr;
+DSK_DEVICE void stamp(int k) {
+#ifdef DSK_DEBUG
+  if (g_sel_dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sel_dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + k] = t;
+  }
+#else
+  (void)k;
+#endif
+}
 
 DSK_DEVICE float key_to_float(uint32_t k) {
   const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
@@ -49,11 +63,11 @@ DSK_DEVICE int bucket_of(uint32_t k, float mn, float inv) {
   return min(max((int)((key_to_float(k) - mn) * inv), 0), kBkt - 1);
 }
 
-// dynamic smem: K[mb4] u32 | CA[kCap] u64 | HI[kBkt] u32 | slen[mb4] u16 | sumk[rg4] u16
+// dynamic smem: K[mb4] u32 | K0[mb4] u32 | CA[kCap] u64 | HI[kBkt] u32 | slen[mb4] u16 | sumk[rg4] u16
 static size_t select_smem_bytes(int maxb, int G) {
   const size_t mb4 = ((size_t)maxb + 3) & ~(size_t)3;
   const size_t rg4 = ((size_t)(maxb + G - 1) / G + 3) & ~(size_t)3;
-  return mb4 * 4 + (size_t)kCap * 8 + (size_t)kBkt * 4 + mb4 * 2 + rg4 * 2;
+  return 2 * mb4 * 4 + (size_t)kCap * 8 + (size_t)kBkt * 4 + mb4 * 2 + rg4 * 2;
 }
 
 // block-wide inclusive scan of one int; returns (inclusive prefix, total)
@@ -85,7 +99,8 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   extern __shared__ __align__(16) unsigned char smem[];
   const int mb4 = (maxb + 3) & ~3;
   uint32_t* K = reinterpret_cast<uint32_t*>(smem);
-  uint64_t* CA = reinterpret_cast<uint64_t*>(K + mb4);
+  uint32_t* K0 = K + mb4;  // immutable copy of the keys (read by peers in the union)
+  uint64_t* CA = reinterpret_cast<uint64_t*>(K0 + mb4);
   uint32_t* HI = reinterpret_cast<uint32_t*>(CA + kCap);
   uint16_t* slen = reinterpret_cast<uint16_t*>(HI + kBkt);
   uint16_t* sumk = slen + mb4;
@@ -109,15 +124,22 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   const float* sc0 = scores + ((size_t)b * Hq + hk * G) * maxb;
   const float* sc = sc0 + (size_t)c * maxb + lo;
 
-  // ---- 1. lengths, keys of this CTA's head, total
+  stamp(0);
+  // ---- 1. lengths (the resident plan), then -- after the preceding kernel
+  //         (PDL) -- the keys of this CTA's head, total
   int t = 0;
   for (int i = tid; i < nr; i += kSelNT) {
     const int len = bs[lo + i + 1] - bs[lo + i];
     slen[i] = (uint16_t)len;
     t += len;
-    K[i] = float_key(sc[i]);
   }
+  stamp(1);
+  pdl_trigger();
+  pdl_wait();
+  stamp(2);
+  for (int i = tid; i < nr; i += kSelNT) K[i] = K0[i] = float_key(sc[i]);
   const int total = cta_scan(t, red_i).y;
+  stamp(3);
 
   // ---- 2. threshold of head c
   if (total <= budget) {
@@ -148,7 +170,8 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
       for (int i = tid; i < kBkt; i += kSelNT) HI[i] = 0;
       __syncthreads();
       if (warp == 0) {
-        float a = red_f[0][lane], x = red_f[1][lane];
+        float a = lane < kSelW ? red_f[0][lane] : CUDART_INF_F;
+        float x = lane < kSelW ? red_f[1][lane] : -CUDART_INF_F;
         a = -warp_max(-a);
         x = warp_max(x);
         if (lane == 0) {
@@ -265,7 +288,9 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
       break;
     }
   }
+  stamp(4);
   cluster.sync();
+  stamp(5);
 
   // ---- 3. union over this CTA's 1/G of the blocks
   int m[G], keep[G], all[G];
@@ -278,6 +303,9 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
     T[g] = (uint32_t)peer[2];
     all[g] = peer[3];
   }
+  const uint32_t* pk[G];  // every head's keys, from the peers' shared memory (DSMEM)
+#pragma unroll
+  for (int g = 0; g < G; ++g) pk[g] = cluster.map_shared_rank(K0, g);
   const int r0 = (int)(((long long)c * nr) / G), r1 = (int)(((long long)(c + 1) * nr) / G);
   const int nrg = r1 - r0;
   for (int i = tid; i < nrg; i += kSelNT) {
@@ -286,7 +314,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
     int u = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const uint32_t key = float_key(sc0[(size_t)g * maxb + blk]);
+      const uint32_t key = pk[g][r0 + i];
       if (all[g] || key > T[g] || (key == T[g] && blk <= m[g])) {
         mask |= 1u << g;
         const int tk = (blk == m[g]) ? keep[g] : len;
@@ -308,7 +336,9 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
     v[G] += s & 0xffu;
   }
   __shared__ int s_scan[(kSelNT / 32 + 1) * (G + 1)];
+  stamp(6);
   block_excl_scan<G + 1, kSelNT>(v, tot, s_scan);
+  stamp(7);
   if (tid <= G) s_tot[tid] = tot[tid];
   cluster.sync();
   int base[G + 1], all_tot[G + 1];
@@ -370,8 +400,16 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
       wl_count[(size_t)b * Hkv + hk] = all_tot[G];
     }
   }
+  stamp(8);
   cluster.sync();  // peers may still be reading this CTA's s_info / s_tot
+  stamp(9);
 }
+
+}  // namespace dsk
+extern "C" int dynsplit_debug_select_timer(void* dev_ptr) {
+  return (int)cudaMemcpyToSymbol(dsk::g_sel_dbg, &dev_ptr, sizeof(void*));
+}
+namespace dsk {
 
 size_t select_smem_needed(int maxb, int G) {
   const size_t s = select_smem_bytes(maxb, G);
@@ -389,20 +427,9 @@ static cudaError_t run_select(int B, int Hkv, size_t smem, const float* scores, 
     allow_max_dyn_smem(k_select<G>);
     attr = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(Hkv * G, B);
-  cfg.blockDim = dim3(kSelNT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = G;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_select<G>, scores, bs, nb, pf, Hq, Hkv, maxb, max_sel, max_wl, Pshift,
-                     budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep, wl_count, wl);
+  launch_ex(k_select<G>, dim3(Hkv * G, B), dim3(kSelNT), smem, st, G, scores, bs, nb, pf, Hq, Hkv,
+            maxb, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep,
+            wl_count, wl);
   return post_launch("k_select", st);
 }
 

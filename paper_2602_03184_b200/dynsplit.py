@@ -16,7 +16,8 @@ from typing import Optional
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit.so")
+LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit_debug.so" if os.environ.get("DYNSPLIT_DEBUG_BUILD")
+                        else "libdynsplit.so")
 
 OK = 0
 BF16, FP32 = 0, 1
