@@ -41,7 +41,7 @@ WORKLOAD = "C3 per-GPU shard: Llama-3-8B decode (32 layers, 32Q/8KV, d=128, bf16
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq", type=int, default=131072)
@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
 
@@ -68,29 +69,50 @@ def measured_peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled through NVML every
+    ~2 ms while the timed region runs (nvidia-smi as a fallback)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.sm = []
+        self.mask = 0
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            p = self._nvml
+            self.sm.append(float(p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)))
+            self.mask |= int(p.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            return
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        self.sm.append(float(out[0]))
+        self.max_mhz = float(out[1])
+        self.mask |= int(out[2], 16)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -102,16 +124,11 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.sm)}
 
 
 # ---------------------------------------------------------------------------
@@ -399,12 +416,16 @@ def main():
         starts = O.segment(G.tokens(args.seed * 7919 + 0, S), G.T7_IDS, G.T7_W10, 32, 14)
         heads = min(args.cpu_sample_heads, Hq)
         lb = oracle_layer_bytes(qh, Kh, starts, budget, Hkv, g)
+        ts = []
         with cpu_threads_limit():
-            ts = [time_oracle(qh, Kh, Vh, starts, budget, heads) for _ in range(2)]
-        sec = min(ts)
+            t_start = time.perf_counter()
+            while not ts or (time.perf_counter() - t_start < args.cpu_seconds and len(ts) < 50):
+                ts.append(time_oracle(qh, Kh, Vh, starts, budget, heads))
+        sec = float(np.mean(ts))
         cpu = {"value": lb * heads / Hq / sec / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"oracle decode step of layer 0, sequence 0 ({heads}/{Hq} heads) at S={S}, "
-                         f"budget {budget}; {sec:.2f} s per sample"}
+               "sample": f"{len(ts)} oracle decode steps of layer 0, sequence 0 ({heads}/{Hq} heads) "
+                         f"at S={S}, budget {budget}; mean {sec:.2f} s each, "
+                         f"{sum(ts):.1f} s total, 1 thread"}
 
     if rank == 0:
         peak, peak_src = measured_peak_hbm()

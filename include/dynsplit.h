@@ -200,9 +200,10 @@ dynsplit_status dynsplit_score_blocks(const dynsplit_shape* shape, const dynspli
  * Equivalently blocks are visited by (score desc, index asc) and taken whole
  * while the budget lasts; the block that reaches the budget ("marginal") keeps
  * its first marginal_keep tokens.  If all tokens fit: marginal = -1, keep = 0.
- * Only blocks in [blk_lo, blk_hi) compete (seq-split shards; pass 0 and
- * INT32_MAX for the whole sequence); worklist page ids are then relative to
- * page_first[b, blk_lo].
+ * All blocks compete (the selection is global); the worklist only holds the
+ * pages of blocks in [blk_lo, blk_hi), with page ids relative to
+ * page_first[b, blk_lo] (a sequence-split shard; pass 0 and INT32_MAX for
+ * the whole sequence).  sel_blocks / n_sel always cover every block.
  *   scores          fp32 [B, Hq, max_blocks]
  *   sel_blocks      (out) int32 [B, Hq, max_sel] ascending block ids (may be NULL)
  *   n_sel, marginal_block, marginal_keep (out) int32 [B, Hq]

@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = 1 << Pshift;
   const int nb = n_blocks[b];
-  const int lo = max(blk_lo, 0), hi = min(blk_hi, nb);
+  // every block of the sequence competes; worklist entries are emitted only
+  // for blocks in the output range [olo, ohi) (a sequence-split shard)
+  const int lo = 0, hi = nb;
+  const int olo = min(max(blk_lo, 0), nb), ohi = max(min(blk_hi, nb), olo);
   const int nr = max(hi - lo, 0);
   const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
   const int32_t* pf = page_first + (size_t)b * (maxb + 1);
@@ -333,7 +336,8 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
     const uint32_t s = sumk[i];
 #pragma unroll
     for (int g = 0; g < G; ++g) v[g] += (s >> (8 + g)) & 1u;
-    v[G] += s & 0xffu;
+    const int blk = lo + r0 + i;
+    if (blk >= olo && blk < ohi) v[G] += s & 0xffu;
   }
   __shared__ int s_scan[(kSelNT / 32 + 1) * (G + 1)];
   stamp(6);
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
 #pragma unroll
   for (int k = 0; k <= G; ++k) v[k] += base[k];
   WLEntry* wlb = wl + ((size_t)b * Hkv + hk) * max_wl;
-  const int pf_lo = nr > 0 ? pf[lo] : 0;
+  const int pf_lo = olo < nb ? pf[olo] : 0;
   for (int i = t0; i < t1; ++i) {
     const int blk = lo + r0 + i, len = slen[r0 + i];
     const uint32_t s = sumk[i];
@@ -371,7 +375,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
         ++v[g];
       }
     }
-    if (u) {
+    if (u && blk >= olo && blk < ohi) {
       const int page0 = pf[blk] - pf_lo;
       for (int jj = 0; jj < u; ++jj) {
         const int pv = min(P, len - (jj << Pshift));

@@ -268,7 +268,8 @@ def repack_digest(K, V, block_starts, n_blocks, page_first, cfg: Config, out=Non
 
 
 def build_blocks(tokens, delim_ids, K, V, cfg: Config, static_w10=None, Qs=None, Ks=None,
-                 Hq: Optional[int] = None, return_scores: bool = False) -> PagedLayer:
+                 Hq: Optional[int] = None, return_scores: bool = False,
+                 Hkv: Optional[int] = None) -> PagedLayer:
     """Rows a1-a4 through dynsplit_build_blocks (one C call).
 
     static_w10: host uint8 sequence (e.g. Table 7) -> static mode; else Qs/Ks
@@ -280,7 +281,9 @@ def build_blocks(tokens, delim_ids, K, V, cfg: Config, static_w10=None, Qs=None,
         Hkv, d = K.shape[2], K.shape[3]
         dt = _dtype_code(K)
     else:
-        Hkv, d, dt = (Ks.shape[3] if Ks is not None else 1), 128, BF16
+        d, dt = 128, BF16
+        if Hkv is None:
+            Hkv = Ks.shape[3] if Ks is not None else (Hq or 1)
     if Hq is None:
         Hq = Qs.shape[3] if Qs is not None else Hkv
     Ls = Qs.shape[0] if Qs is not None else 1
