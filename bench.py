@@ -59,6 +59,16 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/traffic.json), or None."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return float(j[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_peak_hbm():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -453,7 +463,7 @@ def main():
             "bytes_per_step": step_bytes,
             "union_factor": union_rows / (L * B * Hkv * budget),
             "roofline": {"bound": "hbm", "kernel": "k_decode_attn (a7+a8)", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_decode_attn"),
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": attn_bytes_per_launch,
                          "avg_launch_us": attn_ms * 1e3,
