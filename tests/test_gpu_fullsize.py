@@ -1,0 +1,83 @@
+"""Full-size parity at BASELINE.json's sizes, in the launch configuration
+bench.py times (same C-ABI calls, same grids): config 3 per-GPU shard
+(128K, 32Q/8KV, budget 4096, bf16), config 4 heads (40 MHA) at 128K and the
+config 5 prefill scoring at 64K on sampled candidates.
+
+Outputs the oracle can compute directly (plans, page maps, every head's
+selection and attention output) are compared in full; digests and delimiter
+scores on samples."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dynsplit_oracle as O
+from synth import generators as G
+from tests import helpers as H
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+DEV = "cuda:0"
+
+
+def t(x, dtype=None):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(DEV, dtype=dtype)
+
+
+@pytest.mark.parametrize("Hq,Hkv,budget", [(32, 8, 4096), (40, 40, 4096)])
+def test_decode_128k(Hq, Hkv, budget):
+    from paper_2602_03184_b200 import dynsplit as D
+    S, d = 131072, 128
+    cfg = D.default_config()
+    toks = G.tokens(2000, S)
+    q, K, V = G.decode_qkv(2001, S, Hq, Hkv, d)
+    starts = O.segment(toks, G.T7_IDS, G.T7_W10, cfg.C, cfg.delta)
+    q = H.certify_queries(2001, q[None], K[None], [starts], budget)[0]
+    layer = D.build_blocks(t(toks[None]), t(G.T7_IDS), t(K[None], torch.bfloat16),
+                           t(V[None], torch.bfloat16), cfg, static_w10=G.T7_W10, Hq=Hq)
+    qt = t(q[None], torch.bfloat16)
+    sel = D.select(qt, layer, budget)
+    o, lse = D.decode_attn(qt, layer, sel.worklist)
+    o_d, lse_d = D.decode_attn(qt, layer, None)
+    torch.cuda.synchronize()
+    nb = int(layer.n_blocks[0])
+    assert layer.block_starts[0, : nb + 1].tolist() == starts
+    pf, pb, pv = O.page_map(starts, cfg.page_size)
+    assert layer.page_first[0, : nb + 1].tolist() == pf.tolist()
+    assert layer.page_valid[0, : int(pf[-1])].tolist() == pv.tolist()
+    kmax, kmin = O.digests(K, starts)
+    r = G.rng(5, 6)
+    sample = r.choice(nb, size=64, replace=False)
+    dig = layer.digests[0].float().cpu().numpy()
+    assert np.array_equal(dig[:, sample, 0], kmax[:, sample]) and np.array_equal(dig[:, sample, 1], kmin[:, sample])
+    res = O.decode_step(q, K, V, starts, budget)
+    ns = sel.n_sel.cpu().numpy()[0]
+    sb = sel.sel_blocks.cpu().numpy()[0]
+    for h in range(Hq):
+        assert sb[h, : ns[h]].tolist() == res["sel_blocks"][h], h
+        assert int(sel.marginal_block[0, h]) == res["marginal"][h]
+        assert int(sel.marginal_keep[0, h]) == res["keep"][h]
+    err = H.row_rel_err(o[0].cpu().numpy(), res["o"])
+    assert np.all(err <= 2e-3), err.max()
+    assert np.all(np.abs(lse[0].cpu().numpy() - res["lse"]) <= 1e-4 * np.maximum(1, np.abs(res["lse"])))
+    g = Hq // Hkv
+    for h in (0, Hq - 1):                               # dense baseline on two heads
+        od, ld = O.dense_attention(q[h], K[:, h // g], V[:, h // g], 1 / np.sqrt(d))
+        assert H.row_rel_err(o_d[0, h].cpu().numpy()[None], od[None])[0] <= 2e-3
+        assert abs(float(lse_d[0, h]) - ld) <= 1e-4 * max(1, abs(ld))
+
+
+def test_prefill_scoring_64k_sampled():
+    from paper_2602_03184_b200 import dynsplit as D
+    S, Hq, Hkv, d = 65536, 32, 8, 128
+    cfg = D.default_config()
+    toks = G.tokens(2100, S)
+    Qs, Ks = G.scoring_qk(2101, 1, S, Hq, Hkv, d)
+    s = D.score_delimiters(t(toks[None]), t(G.T7_IDS), t(Qs[:, None], torch.bfloat16),
+                           t(Ks[:, None], torch.bfloat16), cfg).cpu().numpy()[0]
+    dset = set(G.T7_IDS.tolist())
+    cands = np.array([i for i in range(S - 1) if int(toks[i]) in dset])
+    r = G.rng(7, 8)
+    sample = np.concatenate([cands[:4], cands[-4:], r.choice(cands, size=8, replace=False)])
+    ref = O.score_delimiters(toks, G.T7_IDS, Qs, Ks, cfg.W, cfg.R, cfg.alpha_pen, candidates=sample.tolist())
+    for i in sample:
+        assert abs(s[i] - ref[i]) <= 2e-4, (i, s[i], ref[i])
+    assert np.isnan(s[S - 1]) and np.sum(~np.isnan(s)) == len(cands)
