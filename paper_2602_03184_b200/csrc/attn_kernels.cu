@@ -5,19 +5,24 @@
 //
 // grid (n_split, Hkv, B) sized to one resident wave; NW consumer warps + 1
 // producer warp per CTA.
-//  * Producer warp: loads 32 worklist entries at a time (coalesced), then lane
-//    0 streams each page's valid rows of K and V (rows_max x 256 B, TMA 1-D
-//    bulk copies, L2 evict-first) into an NS-deep smem ring (full/empty
-//    mbarriers).  Padding rows of a page are never read from HBM.
+//  * Producer warp: loads 32 worklist entries at a time (coalesced), then
+//    streams each page's valid rows of K and V with 16-byte cp.async
+//    (LDGSTS, completion on the stage's full mbarrier via
+//    cp.async.mbarrier.arrive.noinc) into 16-byte padded smem rows of an
+//    NS-deep ring (full/empty mbarriers).  Padding rows of a page are never
+//    read from HBM.  (1-D TMA bulk copies cannot pad rows; one bulk copy per
+//    row was measured slower than LDGSTS.)
 //  * Consumer warp w takes pages i = w (mod NW) and handles ALL G query heads
 //    of the KV group on them, so each K/V byte is read from HBM once:
+//    bf16 caches: QK and PV as mma.sync m16n8k16 tiles (see the consumer);
+//    fp32 caches: CUDA-core path --
 //      QK:  lane (hg = lane/16, r = lane%16) computes the full 128-dim dot of
-//           row r with heads hg, hg+2, ...; 16-byte chunks are visited in the
-//           rotated order (c + r) mod 16, so the 16 rows hit 16 distinct bank
-//           groups (conflict-free), bf16 x bf16 -> fp32 with FHFMA.BF16
-//           (no conversions), fp32 q with FFMA for fp32 caches.
-//      softmax: per head over the 16 lanes of its group (4 xor-shuffles),
-//           exp2 domain, online max/sum.
+//           row r with heads hg, hg+2, ...; the padded K rows put the 16 rows
+//           in distinct bank groups, so all lanes read the same 16-byte chunk
+//           (conflict-free) and q is a broadcast read (FFMA, two chains).
+//      softmax: per head over the 16 lanes of its group, exp2 domain; the
+//           running max moves (and l, acc are rescaled) only when a logit
+//           exceeds it by more than 2^8, detected with one warp vote.
 //      PV:  lane owns dims [4 lane, 4 lane + 4) for all G heads, P from a
 //           per-warp smem slab (float2 (p, p) pairs) and FFMA2.
 //  * Warps are merged in fixed order; each CTA writes its split's (o, lse);
@@ -36,6 +41,19 @@ constexpr int kMinPagesPerSplit = 4;
 // Optional per-CTA phase timestamps (debug only; dynsplit_debug_attn_timer).
 __device__ unsigned long long* g_attn_dbg = nullptr;
 __device__ int g_attn_nocompute = 0;  // debug: stream pages without computing
+__device__ int g_attn_noload = 0;     // debug: compute on stale smem without loading pages
+__device__ unsigned long long* g_attn_pages = nullptr;  // debug: per-page (arrive, done) times of CTA 0
+DSK_DEVICE void pstamp(int warp, int i, int k) {
+#ifdef DSK_DEBUG
+  if (g_attn_pages && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_attn_pages[(i * 2 + k)] = t;
+  }
+#else
+  (void)warp; (void)i; (void)k;
+#endif
+}
 DSK_DEVICE void astamp(int k) {
 #ifdef DSK_DEBUG
   if (g_attn_dbg) {
@@ -67,7 +85,8 @@ DSK_DEVICE void ffma2(float& a0, float& a1, float b0, float b1, uint64_t cc) {
 template <typename T> struct QK;
 template <> struct QK<bf16> {
   static constexpr int kChunks = kD * 2 / 16;  // 16 chunks of 8 bf16
-  static DSK_DEVICE float dot(uint4 qc, uint4 kc, float acc) {
+  // a0 += even elements, a1 += odd elements (two independent FHFMA chains)
+  static DSK_DEVICE void dot2(uint4 qc, uint4 kc, float& a0, float& a1) {
     const uint32_t qs[4] = {qc.x, qc.y, qc.z, qc.w};
     const uint32_t ks[4] = {kc.x, kc.y, kc.z, kc.w};
 #pragma unroll
@@ -75,22 +94,54 @@ template <> struct QK<bf16> {
       unsigned short ql, qh, kl, kh;
       split_bf16x2(qs[e], ql, qh);
       split_bf16x2(ks[e], kl, kh);
-      acc = fma_bf16(ql, kl, acc);
-      acc = fma_bf16(qh, kh, acc);
+      a0 = fma_bf16(ql, kl, a0);
+      a1 = fma_bf16(qh, kh, a1);
     }
-    return acc;
   }
 };
 template <> struct QK<float> {
   static constexpr int kChunks = kD * 4 / 16;  // 32 chunks of 4 fp32
-  static DSK_DEVICE float dot(uint4 qc, uint4 kc, float acc) {
-    acc = fmaf(__uint_as_float(qc.x), __uint_as_float(kc.x), acc);
-    acc = fmaf(__uint_as_float(qc.y), __uint_as_float(kc.y), acc);
-    acc = fmaf(__uint_as_float(qc.z), __uint_as_float(kc.z), acc);
-    acc = fmaf(__uint_as_float(qc.w), __uint_as_float(kc.w), acc);
-    return acc;
+  static DSK_DEVICE void dot2(uint4 qc, uint4 kc, float& a0, float& a1) {
+    a0 = fmaf(__uint_as_float(qc.x), __uint_as_float(kc.x), a0);
+    a1 = fmaf(__uint_as_float(qc.y), __uint_as_float(kc.y), a1);
+    a0 = fmaf(__uint_as_float(qc.z), __uint_as_float(kc.z), a0);
+    a1 = fmaf(__uint_as_float(qc.w), __uint_as_float(kc.w), a1);
   }
 };
+
+// Ring geometry: a stage holds max(P, 16) padded rows (the bf16 tensor-core
+// path consumes 16-row tiles); NS stages for P <= 16, fewer for larger pages
+// so that the ring's size does not grow with P.
+__host__ __device__ inline int attn_stage_rows(int P) { return P < 16 ? 16 : P; }
+__host__ __device__ inline int attn_stages(int NS, int P) {
+  const int n = NS * 16 / attn_stage_rows(P);
+  return n < 2 ? 2 : n;
+}
+
+// ---------------------------------------------------------------- mma.sync helpers (bf16 path)
+DSK_DEVICE void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+DSK_DEVICE void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+// c += A * B for one m16n8k16 tile whose A rows 8..15 are zero (a1 = a3 = 0):
+// a0 = A[g][2t, 2t+1], a2 = A[g][2t+8, 2t+9]; b0/b1 the usual col-major B halves.
+DSK_DEVICE void mma_rows8(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+DSK_DEVICE void mma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+DSK_DEVICE uint32_t bf16x2_bits(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
 
 template <typename T, int G, int NW, int NS>
 __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
@@ -100,17 +151,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
     const WLEntry* __restrict__ wl, int dense, int Hq, int Hkv, int max_pages, int P,
     float scale_log2, float* __restrict__ part_o, float* __restrict__ part_lse,
     int* __restrict__ counters, int n_split, float* __restrict__ o, float* __restrict__ lse) {
-  constexpr int CH = QK<T>::kChunks;
-  constexpr int HPL = (G + 1) / 2;  // heads per QK lane
+  constexpr bool kTC = sizeof(T) == 2;  // bf16: QK and PV on the tensor cores (mma.sync)
   extern __shared__ __align__(128) unsigned char smem[];
-  const size_t stage_bytes = (size_t)P * kD * sizeof(T);
+  // K and V rows are staged with a 16-byte pad (row stride ROW + 16): the 8
+  // or 16 rows a warp reads together then sit in distinct bank groups, which
+  // makes ldmatrix (bf16) and the same-chunk row reads of the fp32 path
+  // conflict-free.  A stage holds max(P, 16) rows; rows of a 16-row tile
+  // beyond the page's valid rows are masked (K) or multiplied by p = 0 (V,
+  // zero-initialised once so that it never holds a non-finite pattern).
+  constexpr int ROW = kD * (int)sizeof(T);
+  constexpr int KROW = ROW + 16;
+  const int ns = attn_stages(NS, P);
+  const size_t kstage = (size_t)attn_stage_rows(P) * KROW, hbm_page = (size_t)P * ROW;
   unsigned char* ringK = smem;
-  unsigned char* ringV = smem + NS * stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * NS * stage_bytes);
-  uint64_t* empty = full + NS;
-  uint32_t(*s_rows)[2] = reinterpret_cast<uint32_t(*)[2]>(empty + NS);
-  T* s_q = reinterpret_cast<T*>(s_rows + NS);                      // [G][kD]
-  float2* pbuf = reinterpret_cast<float2*>(s_q + G * kD);          // [NW][16][G]
+  unsigned char* ringV = smem + ns * kstage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ringV + ns * kstage);
+  uint64_t* empty = full + ns;
+  uint32_t(*s_rows)[2] = reinterpret_cast<uint32_t(*)[2]>(empty + ns);
+  T* s_q = reinterpret_cast<T*>(s_rows + ns);                      // [G][kD]
+  float2* pbuf = reinterpret_cast<float2*>(s_q + G * kD);          // [NW][16][G] (fp32 path)
   __shared__ int s_last;
 
   const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
@@ -120,8 +179,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
   if (threadIdx.x == 0) astamp(0);
   // prologue independent of the preceding kernel (PDL overlap): barriers, q
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 33);  // 32 cp.async lanes (noinc) + the producer's row-count arrive
       mbar_init(&empty[s], 1);
     }
     fence_mbar_init();
@@ -130,6 +189,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
     constexpr int QCH = G * kD * (int)sizeof(T) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD);
     for (int c = threadIdx.x; c < QCH; c += blockDim.x) reinterpret_cast<uint4*>(s_q)[c] = src[c];
+    if (kTC) {
+      const int nz = (int)(ns * kstage / 16);
+      for (int c = threadIdx.x; c < nz; c += blockDim.x)
+        reinterpret_cast<uint4*>(ringV)[c] = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
   pdl_trigger();
   pdl_wait();  // the worklist is the previous kernel's output
@@ -168,39 +232,194 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
   __syncthreads();
 
   if (warp == NW) {  // ---------------------------------------------- producer
-    const uint64_t pol = policy_evict_first();
     for (int base = 0; base < n_it; base += 32) {
       if (base) load_entry(base + lane, page, r0, r1);
       const int nk = min(32, n_it - base);
       for (int k = 0; k < nk; ++k) {
-        const int i = base + k, st = i % NS;
+        const int i = base + k, st = i % ns;
         const int pg = __shfl_sync(0xffffffffu, page, k);
         const uint32_t a = __shfl_sync(0xffffffffu, r0, k);
         const uint32_t c = __shfl_sync(0xffffffffu, r1, k);
-        if (lane == 0) {
-          if (i >= NS) mbar_wait(&empty[st], ((i / NS) - 1) & 1);
-          int rmax = 0;
+        int rmax = 0;
 #pragma unroll
-          for (int g = 0; g < G; ++g) rmax = max(rmax, (int)(((g < 4 ? a : c) >> (8 * (g & 3))) & 0xffu));
+        for (int g = 0; g < G; ++g) rmax = max(rmax, (int)(((g < 4 ? a : c) >> (8 * (g & 3))) & 0xffu));
+#ifdef DSK_DEBUG
+        if (g_attn_noload) rmax = 0;
+#endif
+        if (lane == 0) {
+          if (i >= ns) mbar_wait(&empty[st], ((i / ns) - 1) & 1);
           s_rows[st][0] = a;
           s_rows[st][1] = c;
-          const uint32_t bytes = (uint32_t)rmax * kD * sizeof(T);
-          mbar_arrive_expect_tx(&full[st], 2 * bytes);
-          if (bytes) {
-            const size_t off = ((size_t)bh * max_pages + pg) * stage_bytes;
-            bulk_g2s(ringK + st * stage_bytes, reinterpret_cast<const unsigned char*>(Kp) + off, bytes,
-                     &full[st], pol);
-            bulk_g2s(ringV + st * stage_bytes, reinterpret_cast<const unsigned char*>(Vp) + off, bytes,
-                     &full[st], pol);
-          }
+          mbar_arrive(&full[st]);  // releases s_rows
         }
         __syncwarp();
+        // the page's valid K and V rows into the padded ring with 16-byte
+        // cp.async (512 contiguous bytes per warp instruction, L2
+        // evict-first); every lane then arrives (noinc) on the full barrier
+        // once its copies have landed.
+        const size_t off = ((size_t)bh * max_pages + pg) * hbm_page;
+        constexpr int CPR = ROW / 16;  // 16-byte chunks per row
+        const unsigned char* kg = reinterpret_cast<const unsigned char*>(Kp) + off;
+        const unsigned char* vg = reinterpret_cast<const unsigned char*>(Vp) + off;
+        unsigned char* ks = ringK + st * kstage;
+        unsigned char* vs = ringV + st * kstage;
+        for (int e = lane; e < rmax * CPR; e += 32) {
+          const int rr = e / CPR, cc = e % CPR;
+          cp_async16_cg(ks + (size_t)rr * KROW + cc * 16, kg + (size_t)rr * ROW + cc * 16);
+          cp_async16_cg(vs + (size_t)rr * KROW + cc * 16, vg + (size_t)rr * ROW + cc * 16);
+        }
+        cp_async_mbar_arrive_noinc(&full[st]);
       }
     }
     return;
   }
 
   // ------------------------------------------------------------------ consumers
+  float* sc = reinterpret_cast<float*>(smem);  // merge scratch [NW][G][kScStride], reuses the ring
+  if constexpr (kTC) {
+    // bf16: per 16-row tile of a page, two m16n8k16 tensor-core products.
+    //   QK: S[head][key] with M = the G query heads (rows G..15 zero), N =
+    //       16 keys, K = 128 dims: A = q (registers, loaded once), B = K rows
+    //       by ldmatrix (padded rows: conflict-free), 4 chains of 4 k-steps.
+    //       Lane (g = lane / 4, t = lane % 4) gets head g at keys
+    //       {2t, 2t+1, 2t+8, 2t+9}.
+    //   softmax: quad shuffles per head, exp2 domain, conditional rescale
+    //       (the running max moves only when a logit exceeds it by > 2^8).
+    //   PV: O^T[dim][head] with M = 16 dims x 8 tiles, N = 8 heads, K = 16
+    //       keys: A = V^T by ldmatrix.trans of the V rows, B = P^T, which is
+    //       exactly the QK output fragment, split into bf16 hi + lo parts
+    //       (p = hi + lo to 2^-17 relative: fp32-level accuracy of P V);
+    //       fp32 accumulation.  Lane holds dims {16j + g, 16j + g + 8} of
+    //       heads {2t, 2t+1}.
+    const int g = lane >> 2, t = lane & 3;
+    uint32_t qa[8][2];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qa[ks][0] = qa[ks][1] = 0u;
+      if (g < G) {
+        const uint32_t* qw = reinterpret_cast<const uint32_t*>(s_q + (size_t)g * kD + ks * 16 + 2 * t);
+        qa[ks][0] = qw[0];
+        qa[ks][1] = qw[4];
+      }
+    }
+    float m_run = -CUDART_INF_F, l_run = 0.f;
+    float acc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    // ldmatrix.x4 lane address: matrix mi = lane / 8 covers keys 8 (mi / 2) + 0..7
+    // and 16-byte column block mi % 2 (K: B halves of the two key tiles;
+    // V with .trans: the four A quarters of a 16-dim tile)
+    const int mi = lane >> 3, lr = lane & 7;
+    const uint32_t koff = (uint32_t)(((mi >> 1) * 8 + lr) * KROW + (mi & 1) * 16);
+    const uint32_t voff = koff;
+    const uint32_t ringK_s = smem_u32(ringK), ringV_s = smem_u32(ringV);
+    for (int i = warp; i < n_it; i += NW) {
+      const int st = i % ns;
+      pstamp(warp, i, 0);
+      mbar_wait(&full[st], (i / ns) & 1);
+      pstamp(warp, i, 1);
+      if (threadIdx.x == 0 && i == 0) astamp(2);
+#ifdef DSK_DEBUG
+      if (g_attn_nocompute) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        continue;
+      }
+#endif
+      const uint32_t ra = s_rows[st][0], rc = s_rows[st][1];
+      int rmax = 0;
+#pragma unroll
+      for (int h = 0; h < G; ++h) rmax = max(rmax, (int)(((h < 4 ? ra : rc) >> (8 * (h & 3))) & 0xffu));
+      const int myrows = g < G ? (int)(((g < 4 ? ra : rc) >> (8 * (g & 3))) & 0xffu) : 0;
+      __syncwarp();  // lanes leave the barrier wait independently; .aligned ldmatrix/mma need the full warp
+      for (int r0 = 0; r0 < rmax; r0 += 16) {
+        const uint32_t kb = ringK_s + (uint32_t)(st * kstage + r0 * KROW) + koff;
+        const uint32_t vb = ringV_s + (uint32_t)(st * kstage + r0 * KROW) + voff;
+        float s[4][4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s[c][0] = s[c][1] = s[c][2] = s[c][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t bk[4];
+          ldsm_x4(bk, kb + ks * 32);
+          mma_rows8(s[(ks & 1) * 2 + 0], qa[ks][0], qa[ks][1], bk[0], bk[1]);
+          mma_rows8(s[(ks & 1) * 2 + 1], qa[ks][0], qa[ks][1], bk[2], bk[3]);
+        }
+        const int k0 = r0 + 2 * t;
+        float z[4];
+        z[0] = k0 < myrows ? (s[0][0] + s[2][0]) * scale_log2 : -CUDART_INF_F;
+        z[1] = k0 + 1 < myrows ? (s[0][1] + s[2][1]) * scale_log2 : -CUDART_INF_F;
+        z[2] = k0 + 8 < myrows ? (s[1][0] + s[3][0]) * scale_log2 : -CUDART_INF_F;
+        z[3] = k0 + 9 < myrows ? (s[1][1] + s[3][1]) * scale_log2 : -CUDART_INF_F;
+        const float zmax = fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3]));
+        if (__any_sync(0xffffffffu, zmax > m_run + 8.f)) {
+          float mx = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          const float mnew = fmaxf(m_run, mx);
+          const float corr = (mnew == -CUDART_INF_F || m_run == mnew) ? 1.f : exp2f(m_run - mnew);
+          m_run = mnew;
+          l_run *= corr;
+          const float c0 = __shfl_sync(0xffffffffu, corr, 8 * t);      // head 2t
+          const float c1 = __shfl_sync(0xffffffffu, corr, 8 * t + 4);  // head 2t + 1
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc[j][0] *= c0;
+            acc[j][1] *= c1;
+            acc[j][2] *= c0;
+            acc[j][3] *= c1;
+          }
+        }
+        float p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          p[k] = z[k] == -CUDART_INF_F ? 0.f : exp2f(z[k] - m_run);
+          l_run += p[k];
+        }
+        const __nv_bfloat162 h01 = __floats2bfloat162_rn(p[0], p[1]);
+        const __nv_bfloat162 h23 = __floats2bfloat162_rn(p[2], p[3]);
+        const __nv_bfloat162 l01 = __floats2bfloat162_rn(p[0] - __low2float(h01), p[1] - __high2float(h01));
+        const __nv_bfloat162 l23 = __floats2bfloat162_rn(p[2] - __low2float(h23), p[3] - __high2float(h23));
+        const uint32_t bh0 = bf16x2_bits(h01), bh1 = bf16x2_bits(h23);
+        const uint32_t bl0 = bf16x2_bits(l01), bl1 = bf16x2_bits(l23);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t av[4];
+          ldsm_x4_t(av, vb + j * 32);
+          // ldmatrix order (keys lo, dims lo), (keys lo, dims hi), (keys hi, dims lo),
+          // (keys hi, dims hi) -> A quarters a0, a1, a2, a3 of V^T
+          const uint32_t a[4] = {av[0], av[1], av[2], av[3]};
+          mma_16816(acc[j], a, bh0, bh1);
+          mma_16816(acc[j], a, bl0, bl1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      pstamp(warp, 64 + i, 0);
+    }
+    // ---- per-warp state to the merge scratch (the ring is free once all are here)
+    named_bar_sync(1, NW * 32);
+    if (threadIdx.x == 0) astamp(3);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int h = 2 * t + e;
+      if (h < G) {
+        float* row = sc + (warp * G + h) * kScStride + g;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          row[16 * j] = acc[j][e];
+          row[16 * j + 8] = acc[j][2 + e];
+        }
+      }
+    }
+    if (g < G && t == 0) {
+      sc[(warp * G + g) * kScStride + kD] = m_run;
+      sc[(warp * G + g) * kScStride + kD + 1] = l_run;
+    }
+  } else {
+  constexpr int CH = QK<T>::kChunks;
+  constexpr int HPL = (G + 1) / 2;  // heads per QK lane
   const int r = lane & 15, hg = lane >> 4;
   float m[HPL], l[HPL];
 #pragma unroll
@@ -217,8 +436,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
   const unsigned char* qbase = reinterpret_cast<const unsigned char*>(s_q);
 
   for (int i = warp; i < n_it; i += NW) {
-    const int st = i % NS;
-    mbar_wait(&full[st], (i / NS) & 1);
+    const int st = i % ns;
+    pstamp(warp, i, 0);
+    mbar_wait(&full[st], (i / ns) & 1);
+    pstamp(warp, i, 1);
     if (threadIdx.x == 0 && i == 0) astamp(2);
 #ifdef DSK_DEBUG
     if (g_attn_nocompute) {
@@ -236,59 +457,77 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
       const int h = hg + 2 * j;
       myrows[j] = h < G ? (int)(((h < 4 ? ra : rc) >> (8 * (h & 3))) & 0xffu) : 0;
     }
-    const unsigned char* Ks = ringK + st * stage_bytes;
-    const T* Vs = reinterpret_cast<const T*>(ringV + st * stage_bytes);
+    const unsigned char* Ks = ringK + st * kstage;
+    const unsigned char* Vs = ringV + st * kstage;
     for (int r0 = 0; r0 < rmax; r0 += 16) {
       const int nr = min(16, rmax - r0);
       const bool rowok = r < nr;
-      float dot[HPL];
+      // QK: two independent accumulation chains per head (even/odd elements)
+      float dot0[HPL], dot1[HPL];
 #pragma unroll
-      for (int j = 0; j < HPL; ++j) dot[j] = 0.f;
+      for (int j = 0; j < HPL; ++j) dot0[j] = dot1[j] = 0.f;
       if (rowok) {
-        const unsigned char* krow = Ks + (size_t)(r0 + r) * kD * sizeof(T);
+        const unsigned char* krow = Ks + (size_t)(r0 + r) * KROW;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-          const int off = ((c + r) & (CH - 1)) * 16;
+          const int off = c * 16;
           const uint4 kc = *reinterpret_cast<const uint4*>(krow + off);
 #pragma unroll
           for (int j = 0; j < HPL; ++j) {
             const int h = hg + 2 * j;
             if (h < G) {
               const uint4 qc = *reinterpret_cast<const uint4*>(qbase + (size_t)h * kD * sizeof(T) + off);
-              dot[j] = QK<T>::dot(qc, kc, dot[j]);
+              QK<T>::dot2(qc, kc, dot0[j], dot1[j]);
             }
           }
         }
       }
-      float p[HPL], corr[HPL];
+      // online softmax with conditional rescaling: the running max m only
+      // moves (full 16-lane max + rescale of l and acc) when some logit
+      // exceeds it by more than 2^8 (log2 domain); otherwise p = exp2(z - m)
+      // directly and every lane keeps its own partial sum l (reduced at the end).
+      float z[HPL];
+      bool any_valid = false;
+#pragma unroll
+      for (int j = 0; j < HPL; ++j) {
+        const bool valid = rowok && (r0 + r) < myrows[j];
+        z[j] = valid ? (dot0[j] + dot1[j]) * scale_log2 : -CUDART_INF_F;
+        any_valid |= z[j] > m[j] + 8.f;
+      }
+      if (__any_sync(0xffffffffu, any_valid)) {
+        float corr[HPL];
+#pragma unroll
+        for (int j = 0; j < HPL; ++j) {
+          float mx = z[j];
+#pragma unroll
+          for (int o2 = 1; o2 < 16; o2 <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+          const float mnew = fmaxf(m[j], mx);
+          corr[j] = (mnew == -CUDART_INF_F || m[j] == mnew) ? 1.f : exp2f(m[j] - mnew);
+          l[j] *= corr[j];
+          m[j] = mnew;
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const float ch = __shfl_sync(0xffffffffu, corr[h >> 1], (h & 1) * 16);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[h][k] *= ch;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < HPL; ++j) {
         const int h = hg + 2 * j;
-        const bool valid = rowok && (r0 + r) < myrows[j];
-        const float z = valid ? dot[j] * scale_log2 : -CUDART_INF_F;
-        float mx = z;
-#pragma unroll
-        for (int o2 = 1; o2 < 16; o2 <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
-        const float mnew = fmaxf(m[j], mx);
-        corr[j] = (mnew == -CUDART_INF_F) ? 1.f : exp2f(m[j] - mnew);
-        p[j] = valid ? exp2f(z - mnew) : 0.f;
-        float ps = p[j];
-#pragma unroll
-        for (int o2 = 1; o2 < 16; o2 <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o2);
-        l[j] = l[j] * corr[j] + ps;
-        m[j] = mnew;
-        if (h < G) pb[r * G + h] = make_float2(p[j], p[j]);
+        const float pj = z[j] == -CUDART_INF_F ? 0.f : exp2f(z[j] - m[j]);
+        l[j] += pj;
+        if (h < G) pb[r * G + h] = make_float2(pj, pj);
       }
       __syncwarp();
+      // fully unrolled over the 16 rows of the slab (predicated) so the V and
+      // P loads of several rows are in flight at once
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const float ch = __shfl_sync(0xffffffffu, corr[h >> 1], (h & 1) * 16);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[h][k] *= ch;
-      }
-      for (int rr = 0; rr < nr; ++rr) {
+      for (int rr = 0; rr < 16; ++rr) {
+        if (rr >= nr) break;
         float v[4];
-        Vec<T>::load4(Vs + (size_t)(r0 + rr) * kD + lane * 4, v);
+        Vec<T>::load4(reinterpret_cast<const T*>(Vs + (size_t)(r0 + rr) * KROW) + lane * 4, v);
         const float2* prow = pb + rr * G;
 #pragma unroll
         for (int h = 0; h < G; h += 2) {
@@ -310,16 +549,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
       __syncwarp();
     }
     if (lane == 0) mbar_arrive(&empty[st]);
+    pstamp(warp, 64 + i, 0);
   }
 
-  // ---- merge the NW warps (fixed order); the ring is free once all are here
+  // ---- per-warp state to the merge scratch (the ring is free once all are here)
   named_bar_sync(1, NW * 32);
   if (threadIdx.x == 0) astamp(3);
-  float* sc = reinterpret_cast<float*>(smem);  // [NW][G][kD + 2]
 #pragma unroll
   for (int h = 0; h < G; ++h)
     *reinterpret_cast<float4*>(sc + (warp * G + h) * kScStride + lane * 4) =
         make_float4(acc[h][0], acc[h][1], acc[h][2], acc[h][3]);
+#pragma unroll
+  for (int j = 0; j < HPL; ++j) {
+#pragma unroll
+    for (int o2 = 1; o2 < 16; o2 <<= 1) l[j] += __shfl_xor_sync(0xffffffffu, l[j], o2);
+  }
   if (r == 0) {
 #pragma unroll
     for (int j = 0; j < HPL; ++j) {
@@ -330,6 +574,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
       }
     }
   }
+  }  // fp32 path
+  // ---- merge the NW warps (fixed order)
   named_bar_sync(1, NW * 32);
   const float LN2 = 0.69314718055994530942f;
   for (int h = warp; h < G; h += NW) {
@@ -429,9 +675,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
 // ============================================================================
 template <typename T, int G, int NW, int NS>
 static size_t attn_smem(int P) {
-  const size_t ring = (size_t)2 * NS * P * kD * sizeof(T);
+  const int ns = attn_stages(NS, P);
+  const size_t ring = (size_t)ns * 2 * attn_stage_rows(P) * (kD * sizeof(T) + 16);
   const size_t merge = (size_t)NW * G * kScStride * sizeof(float);
-  return (ring > merge ? ring : merge) + 2 * NS * sizeof(uint64_t) + NS * 8 +
+  return (ring > merge ? ring : merge) + 2 * ns * sizeof(uint64_t) + ns * 8 +
          (size_t)G * kD * sizeof(T) + (size_t)NW * 16 * G * sizeof(float2);
 }
 
@@ -496,6 +743,12 @@ static cudaError_t attn_run(const void* q, const void* Kp, const void* Vp, const
 }  // namespace dsk
 extern "C" int dynsplit_debug_attn_timer(void* dev_ptr) {
   return (int)cudaMemcpyToSymbol(dsk::g_attn_dbg, &dev_ptr, sizeof(void*));
+}
+extern "C" int dynsplit_debug_attn_pages(void* dev_ptr) {
+  return (int)cudaMemcpyToSymbol(dsk::g_attn_pages, &dev_ptr, sizeof(void*));
+}
+extern "C" int dynsplit_debug_attn_noload(int on) {
+  return (int)cudaMemcpyToSymbol(dsk::g_attn_noload, &on, sizeof(int));
 }
 extern "C" int dynsplit_debug_attn_nocompute(int on) {
   return (int)cudaMemcpyToSymbol(dsk::g_attn_nocompute, &on, sizeof(int));

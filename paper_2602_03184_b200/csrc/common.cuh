@@ -155,13 +155,16 @@ DSK_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 DSK_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase
+// completes (or ~1 ms) instead of spinning and stealing issue slots from the
+// warps that do the work.
 DSK_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
   return ok != 0;
 }
 DSK_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -176,6 +179,23 @@ DSK_DEVICE void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, u
       " [%0], [%1], %2, [%3], %4;"
       ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// 16-byte cp.async (LDGSTS, bypassing L1) with an L2 cache policy.
+DSK_DEVICE void cp_async16_hint(void* dst_smem, const void* src_gmem, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+               ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "l"(policy) : "memory");
+}
+// 16-byte cp.async (LDGSTS, bypassing L1) without a cache policy.  (ptxas
+// 12.9 mis-encodes two back-to-back hinted LDGSTS with an odd uniform
+// descriptor register -> illegal instruction; the un-hinted form is safe.)
+DSK_DEVICE void cp_async16_cg(void* dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem)
+               : "memory");
+}
+// Arrive on `bar` when all of this thread's prior cp.async have completed
+// (does not increment the expected count: the barrier's count includes it).
+DSK_DEVICE void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 DSK_DEVICE uint64_t policy_evict_first() {
   uint64_t p;
