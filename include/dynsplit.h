@@ -89,7 +89,9 @@ int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* cfg);
 int32_t dynsplit_max_pages(int32_t S, const dynsplit_config* cfg);
 /* Upper bound on blocks one head selects under `budget` tokens. */
 int32_t dynsplit_max_selected(int32_t budget, int32_t S, const dynsplit_config* cfg);
-/* Bytes of the opaque worklist produced by dynsplit_select. */
+/* Bytes of the opaque worklist produced by dynsplit_select (room for every
+ * page of every (b, KV head): B * Hkv * max_pages 16-byte entries + 512 B;
+ * `budget` is accepted for API stability and does not change the size). */
 size_t dynsplit_worklist_bytes(const dynsplit_shape* shape, const dynsplit_config* cfg,
                                int32_t budget);
 /* Bytes of workspace needed by `op` (a dynsplit_op).  0 on invalid input. */

@@ -115,12 +115,12 @@ inline dynsplit_status cuda_status(cudaError_t e) {
     if (_s != DYNSPLIT_OK) return _s;            \
   } while (0)
 
+// Worklist capacity per (b, KV head): every page of the sequence (the union
+// of the selected pages is a subset).  Budget-independent, so the attention
+// kernel knows each (b, KV head)'s entry base without reading the header.
 inline int max_wl_of(const dynsplit_shape* s, const dynsplit_config* c, int budget) {
-  const int g = s->Hq / s->Hkv;
-  const int maxp = dynsplit_max_pages(s->S, c);
-  const long long per_head = (long long)budget / c->page_size + dynsplit_max_selected(budget, s->S, c) + 1;
-  const long long v = (long long)g * per_head;
-  return (int)(v < maxp ? v : maxp);
+  (void)budget;
+  return dynsplit_max_pages(s->S, c);
 }
 
 struct WorklistView {

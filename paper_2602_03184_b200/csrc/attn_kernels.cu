@@ -3,16 +3,18 @@
 // splits (Step 3 of KV selection; "split-K ... log-sum-exp merge",
 // north star).
 //
-// grid (n_split, Hkv, B) sized to one resident wave; NW consumer warps + 1
-// producer warp per CTA.
-//  * Producer warp: loads 32 worklist entries at a time (coalesced), then
-//    streams each page's valid rows of K and V with 16-byte cp.async
-//    (LDGSTS, completion on the stage's full mbarrier via
-//    cp.async.mbarrier.arrive.noinc) into 16-byte padded smem rows of an
-//    NS-deep ring (full/empty mbarriers).  Padding rows of a page are never
-//    read from HBM.  (1-D TMA bulk copies cannot pad rows; one bulk copy per
-//    row was measured slower than LDGSTS.)
-//  * Consumer warp w takes pages i = w (mod NW) and handles ALL G query heads
+// grid (n_split, Hkv, B) sized to one resident wave; NW warps per CTA, no
+// producer warp and no inter-warp barriers in the main loop:
+//  * warp w takes the split's pages i = w (mod NW) and runs its own load
+//    pipeline: the page's valid K and V rows go into 16-byte padded smem rows
+//    of a private `depth`-stage ring with 16-byte cp.async (LDGSTS, 512
+//    contiguous bytes per warp instruction), page j + depth is issued while
+//    page j is computed, completion by cp.async.wait_group.  Padding rows of
+//    a page are never read from HBM.  (Measured alternatives: a producer warp
+//    + mbarrier ring spent half of all issued instructions in the consumers'
+//    try_wait loops and could not keep the consumers fed; 1-D TMA bulk copies
+//    cannot pad rows and one bulk copy per row is slower than LDGSTS.)
+//  * A warp handles ALL G query heads
 //    of the KV group on them, so each K/V byte is read from HBM once:
 //    bf16 caches: QK and PV as mma.sync m16n8k16 tiles (see the consumer);
 //    fp32 caches: CUDA-core path --
@@ -109,13 +111,28 @@ template <> struct QK<float> {
   }
 };
 
-// Ring geometry: a stage holds max(P, 16) padded rows (the bf16 tensor-core
-// path consumes 16-row tiles); NS stages for P <= 16, fewer for larger pages
-// so that the ring's size does not grow with P.
+// Ring geometry: every consumer warp owns a private ring of `depth` stages;
+// a stage holds max(P, 16) padded K rows followed by as many V rows (the bf16
+// tensor-core path consumes 16-row tiles).  The depth is D for P <= 16 bf16
+// pages and shrinks (>= 1) so that the CTA's rings stay within kRingBudget.
+constexpr int kRingBudget = 72 * 1024;
 __host__ __device__ inline int attn_stage_rows(int P) { return P < 16 ? 16 : P; }
-__host__ __device__ inline int attn_stages(int NS, int P) {
-  const int n = NS * 16 / attn_stage_rows(P);
-  return n < 2 ? 2 : n;
+__host__ __device__ inline size_t attn_stage_bytes(int row_bytes, int P) {
+  return (size_t)2 * attn_stage_rows(P) * (row_bytes + 16);
+}
+__host__ __device__ inline int attn_depth(int D, int NW, int row_bytes, int P) {
+  const int n = (int)(kRingBudget / ((size_t)NW * attn_stage_bytes(row_bytes, P)));
+  return n < 1 ? 1 : (n > D ? D : n);
+}
+DSK_DEVICE void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// wait until at most n of this thread's most recent cp.async groups are pending
+DSK_DEVICE void cp_async_wait_pending(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+  }
 }
 
 // ---------------------------------------------------------------- mma.sync helpers (bf16 path)
@@ -143,8 +160,8 @@ DSK_DEVICE void mma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, ui
 }
 DSK_DEVICE uint32_t bf16x2_bits(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
 
-template <typename T, int G, int NW, int NS>
-__global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
+template <typename T, int G, int NW, int D>
+__global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
     const T* __restrict__ q, const T* __restrict__ Kp, const T* __restrict__ Vp,
     const int16_t* __restrict__ page_valid, const int32_t* __restrict__ n_pages,
     const int32_t* __restrict__ wl_hdr, const int32_t* __restrict__ wl_count,
@@ -161,14 +178,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
   // zero-initialised once so that it never holds a non-finite pattern).
   constexpr int ROW = kD * (int)sizeof(T);
   constexpr int KROW = ROW + 16;
-  const int ns = attn_stages(NS, P);
-  const size_t kstage = (size_t)attn_stage_rows(P) * KROW, hbm_page = (size_t)P * ROW;
-  unsigned char* ringK = smem;
-  unsigned char* ringV = smem + ns * kstage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ringV + ns * kstage);
-  uint64_t* empty = full + ns;
-  uint32_t(*s_rows)[2] = reinterpret_cast<uint32_t(*)[2]>(empty + ns);
-  T* s_q = reinterpret_cast<T*>(s_rows + ns);                      // [G][kD]
+  const int nd = attn_depth(D, NW, ROW, P);
+  const size_t kstage = (size_t)attn_stage_rows(P) * KROW, stage = 2 * kstage;
+  const size_t hbm_page = (size_t)P * ROW;
+  uint32_t(*s_rows)[2] = reinterpret_cast<uint32_t(*)[2]>(smem + (size_t)NW * nd * stage);  // [NW][D]
+  T* s_q = reinterpret_cast<T*>(s_rows + NW * D);                  // [G][kD]
   float2* pbuf = reinterpret_cast<float2*>(s_q + G * kD);          // [NW][16][G] (fp32 path)
   __shared__ int s_last;
 
@@ -177,102 +191,107 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
   const int bh = b * Hkv + hk;
 
   if (threadIdx.x == 0) astamp(0);
-  // prologue independent of the preceding kernel (PDL overlap): barriers, q
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ns; ++s) {
-      mbar_init(&full[s], 33);  // 32 cp.async lanes (noinc) + the producer's row-count arrive
-      mbar_init(&empty[s], 1);
-    }
-    fence_mbar_init();
-  }
+  // prologue independent of the preceding kernel (PDL overlap): q, V ring reset
   {
     constexpr int QCH = G * kD * (int)sizeof(T) / 16;
     const uint4* src = reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD);
     for (int c = threadIdx.x; c < QCH; c += blockDim.x) reinterpret_cast<uint4*>(s_q)[c] = src[c];
     if (kTC) {
-      const int nz = (int)(ns * kstage / 16);
-      for (int c = threadIdx.x; c < nz; c += blockDim.x)
-        reinterpret_cast<uint4*>(ringV)[c] = make_uint4(0u, 0u, 0u, 0u);
+      const int nz = (int)(kstage / 16);
+      for (int s2 = 0; s2 < NW * nd; ++s2) {
+        uint4* vz = reinterpret_cast<uint4*>(smem + s2 * stage + kstage);
+        for (int c = threadIdx.x; c < nz; c += blockDim.x) vz[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
     }
   }
   pdl_trigger();
   pdl_wait();  // the worklist is the previous kernel's output
   if (threadIdx.x == 0) astamp(1);
 
+  // Pages are dealt round-robin: split s of n_eff takes worklist entries
+  // e = s + k n_eff, k = 0, 1, ...; warp w takes k = w + j NW.  Entry e of
+  // (b, KV head) bh sits at wl[e * B * Hkv + bh] (interleaved layout; the
+  // buffer holds >= max_pages entries per bh), so each warp's first 32
+  // entries are loaded together with the page count, speculating
+  // n_eff == n_split (true whenever cnt >= kMinPagesPerSplit * n_split).
+  const size_t BH = (size_t)gridDim.z * Hkv;
+  int e_page = 0;
+  uint32_t e_r0 = 0, e_r1 = 0;
+  auto load_batch = [&](int j0, int stride) {  // entries of this warp's pages j0 + lane
+    const int e = split + (warp + (j0 + lane) * NW) * stride;
+    e_page = 0;
+    e_r0 = e_r1 = 0;
+    if (e < max_pages) {
+      if (dense) {
+        e_page = e;
+        const uint32_t pv = (uint32_t)page_valid[(size_t)b * max_pages + e];
+        e_r0 = e_r1 = pv * 0x01010101u;
+      } else {
+        const int4 en = *reinterpret_cast<const int4*>(wl + (size_t)e * BH + bh);
+        e_page = en.x;
+        e_r0 = (uint32_t)en.z;
+        e_r1 = (uint32_t)en.w;
+      }
+    }
+  };
+  load_batch(0, n_split);
   const int cnt = dense ? n_pages[b] : wl_count[bh];
   // splits actually used by this (b, KV head): at least kMinPagesPerSplit pages each
   const int n_eff = max(1, min(n_split, (cnt + kMinPagesPerSplit - 1) / kMinPagesPerSplit));
   if (split >= n_eff) return;
-  const int e_lo = (int)(((long long)split * cnt) / n_eff);
-  const int e_hi = (int)(((long long)(split + 1) * cnt) / n_eff);
-  const int n_it = e_hi - e_lo;
-
-  // producer warp: first batch of 32 worklist entries before the CTA barrier
-  const int max_wl = dense ? 0 : wl_hdr[1];
-  const WLEntry* wlb = wl + (size_t)bh * max_wl + e_lo;
-  auto load_entry = [&](int idx, int& page, uint32_t& r0, uint32_t& r1) {
-    page = 0;
-    r0 = r1 = 0;
-    if (idx < n_it) {
-      if (dense) {
-        page = e_lo + idx;
-        const uint32_t pv = (uint32_t)page_valid[(size_t)b * max_pages + page];
-        r0 = r1 = pv * 0x01010101u;
-      } else {
-        const int4 e = *reinterpret_cast<const int4*>(wlb + idx);
-        page = e.x;
-        r0 = (uint32_t)e.z;
-        r1 = (uint32_t)e.w;
-      }
-    }
-  };
-  int page = 0;
-  uint32_t r0 = 0, r1 = 0;
-  if (warp == NW) load_entry(lane, page, r0, r1);
-  __syncthreads();
-
-  if (warp == NW) {  // ---------------------------------------------- producer
-    for (int base = 0; base < n_it; base += 32) {
-      if (base) load_entry(base + lane, page, r0, r1);
-      const int nk = min(32, n_it - base);
-      for (int k = 0; k < nk; ++k) {
-        const int i = base + k, st = i % ns;
-        const int pg = __shfl_sync(0xffffffffu, page, k);
-        const uint32_t a = __shfl_sync(0xffffffffu, r0, k);
-        const uint32_t c = __shfl_sync(0xffffffffu, r1, k);
-        int rmax = 0;
-#pragma unroll
-        for (int g = 0; g < G; ++g) rmax = max(rmax, (int)(((g < 4 ? a : c) >> (8 * (g & 3))) & 0xffu));
+  if (n_eff != n_split) load_batch(0, n_eff);
+  const int n_it = (cnt - split + n_eff - 1) / n_eff;  // this split's pages
 #ifdef DSK_DEBUG
-        if (g_attn_noload) rmax = 0;
+  if (g_attn_dbg) {  // debug timeline: wait for the entry loads before stamping
+    if (__shfl_sync(0xffffffffu, e_page, 0) < 0) e_page = 0;
+    if (threadIdx.x == 0) astamp(6);
+  }
 #endif
-        if (lane == 0) {
-          if (i >= ns) mbar_wait(&empty[st], ((i / ns) - 1) & 1);
-          s_rows[st][0] = a;
-          s_rows[st][1] = c;
-          mbar_arrive(&full[st]);  // releases s_rows
-        }
-        __syncwarp();
-        // the page's valid K and V rows into the padded ring with 16-byte
-        // cp.async (512 contiguous bytes per warp instruction, L2
-        // evict-first); every lane then arrives (noinc) on the full barrier
-        // once its copies have landed.
-        const size_t off = ((size_t)bh * max_pages + pg) * hbm_page;
-        constexpr int CPR = ROW / 16;  // 16-byte chunks per row
-        const unsigned char* kg = reinterpret_cast<const unsigned char*>(Kp) + off;
-        const unsigned char* vg = reinterpret_cast<const unsigned char*>(Vp) + off;
-        unsigned char* ks = ringK + st * kstage;
-        unsigned char* vs = ringV + st * kstage;
-        for (int e = lane; e < rmax * CPR; e += 32) {
-          const int rr = e / CPR, cc = e % CPR;
-          cp_async16_cg(ks + (size_t)rr * KROW + cc * 16, kg + (size_t)rr * ROW + cc * 16);
-          cp_async16_cg(vs + (size_t)rr * KROW + cc * 16, vg + (size_t)rr * ROW + cc * 16);
-        }
-        cp_async_mbar_arrive_noinc(&full[st]);
+  __syncthreads();  // s_q and the zeroed V rings are visible to every warp
+
+  // ---- per-warp load pipeline: warp w issues page j + depth with 16-byte
+  // cp.async (LDGSTS) into its own ring while it computes page j;
+  // completion by cp.async.wait_group, no barriers between warps.
+  const int n_mine = n_it > warp ? (n_it - warp + NW - 1) / NW : 0;
+  unsigned char* wring = smem + (size_t)warp * nd * stage;
+  auto issue = [&](int j) {
+    if (j < n_mine) {
+      if ((j & 31) == 0 && j) load_batch(j, n_eff);
+      const int pg = __shfl_sync(0xffffffffu, e_page, j & 31);
+      const uint32_t a = __shfl_sync(0xffffffffu, e_r0, j & 31);
+      const uint32_t c = __shfl_sync(0xffffffffu, e_r1, j & 31);
+      int rmax = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) rmax = max(rmax, (int)(((g < 4 ? a : c) >> (8 * (g & 3))) & 0xffu));
+#ifdef DSK_DEBUG
+      if (g_attn_noload) rmax = 0;
+#endif
+      const int st = j % nd;
+      if (lane == 0) {
+        s_rows[warp * D + st][0] = a;
+        s_rows[warp * D + st][1] = c;
+      }
+      // valid rows only (padding rows of a page are never read from HBM);
+      // lane -> fixed 16-byte column chunk, RPI rows per warp instruction
+      constexpr int CPR = ROW / 16;
+      constexpr int RPI = 32 / CPR;
+      const size_t off = ((size_t)bh * max_pages + pg) * hbm_page;
+      const int cc = lane % CPR, r0 = lane / CPR;
+      const unsigned char* kg = reinterpret_cast<const unsigned char*>(Kp) + off + r0 * ROW + cc * 16;
+      const unsigned char* vg = reinterpret_cast<const unsigned char*>(Vp) + off + r0 * ROW + cc * 16;
+      unsigned char* ks = wring + st * stage + r0 * KROW + cc * 16;
+      for (int rr = r0; rr < rmax; rr += RPI) {
+        cp_async16_cg(ks, kg);
+        cp_async16_cg(ks + kstage, vg);
+        ks += RPI * KROW;
+        kg += RPI * ROW;
+        vg += RPI * ROW;
       }
     }
-    return;
-  }
+    cp_async_commit_group();
+  };
+  for (int j = 0; j < nd; ++j) issue(j);
+  if (threadIdx.x == 0) astamp(7);
 
   // ------------------------------------------------------------------ consumers
   float* sc = reinterpret_cast<float*>(smem);  // merge scratch [NW][G][kScStride], reuses the ring
@@ -312,29 +331,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
     const int mi = lane >> 3, lr = lane & 7;
     const uint32_t koff = (uint32_t)(((mi >> 1) * 8 + lr) * KROW + (mi & 1) * 16);
     const uint32_t voff = koff;
-    const uint32_t ringK_s = smem_u32(ringK), ringV_s = smem_u32(ringV);
-    for (int i = warp; i < n_it; i += NW) {
-      const int st = i % ns;
+    const uint32_t wring_s = smem_u32(wring);
+    for (int j = 0; j < n_mine; ++j) {
+      const int i = warp + j * NW, st = j % nd;
       pstamp(warp, i, 0);
-      mbar_wait(&full[st], (i / ns) & 1);
+      cp_async_wait_pending(nd - 1);  // this lane's copies of page j have landed
+      __syncwarp();                   // ... and every lane's
       pstamp(warp, i, 1);
-      if (threadIdx.x == 0 && i == 0) astamp(2);
+      if (threadIdx.x == 0 && j == 0) astamp(2);
 #ifdef DSK_DEBUG
       if (g_attn_nocompute) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        issue(j + nd);
         continue;
       }
 #endif
-      const uint32_t ra = s_rows[st][0], rc = s_rows[st][1];
+      const uint32_t ra = s_rows[warp * D + st][0], rc = s_rows[warp * D + st][1];
       int rmax = 0;
 #pragma unroll
       for (int h = 0; h < G; ++h) rmax = max(rmax, (int)(((h < 4 ? ra : rc) >> (8 * (h & 3))) & 0xffu));
       const int myrows = g < G ? (int)(((g < 4 ? ra : rc) >> (8 * (g & 3))) & 0xffu) : 0;
-      __syncwarp();  // lanes leave the barrier wait independently; .aligned ldmatrix/mma need the full warp
       for (int r0 = 0; r0 < rmax; r0 += 16) {
-        const uint32_t kb = ringK_s + (uint32_t)(st * kstage + r0 * KROW) + koff;
-        const uint32_t vb = ringV_s + (uint32_t)(st * kstage + r0 * KROW) + voff;
+        const uint32_t kb = wring_s + (uint32_t)(st * stage + r0 * KROW) + koff;
+        const uint32_t vb = wring_s + (uint32_t)(st * stage + kstage + r0 * KROW) + voff;
         float s[4][4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) s[c][0] = s[c][1] = s[c][2] = s[c][3] = 0.f;
@@ -392,8 +410,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
           mma_16816(acc[j], a, bl0, bl1);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      __syncwarp();  // the stage is free
+      issue(j + nd);
       pstamp(warp, 64 + i, 0);
     }
     // ---- per-warp state to the merge scratch (the ring is free once all are here)
@@ -435,20 +453,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
   float2* pb = pbuf + warp * 16 * G;
   const unsigned char* qbase = reinterpret_cast<const unsigned char*>(s_q);
 
-  for (int i = warp; i < n_it; i += NW) {
-    const int st = i % ns;
+  for (int jp = 0; jp < n_mine; ++jp) {
+    const int i = warp + jp * NW, st = jp % nd;
     pstamp(warp, i, 0);
-    mbar_wait(&full[st], (i / ns) & 1);
+    cp_async_wait_pending(nd - 1);
+    __syncwarp();
     pstamp(warp, i, 1);
-    if (threadIdx.x == 0 && i == 0) astamp(2);
+    if (threadIdx.x == 0 && jp == 0) astamp(2);
 #ifdef DSK_DEBUG
     if (g_attn_nocompute) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      issue(jp + nd);
       continue;
     }
 #endif
-    const uint32_t ra = s_rows[st][0], rc = s_rows[st][1];
+    const uint32_t ra = s_rows[warp * D + st][0], rc = s_rows[warp * D + st][1];
     int rmax = 0, myrows[HPL];
 #pragma unroll
     for (int g = 0; g < G; ++g) rmax = max(rmax, (int)(((g < 4 ? ra : rc) >> (8 * (g & 3))) & 0xffu));
@@ -457,8 +475,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
       const int h = hg + 2 * j;
       myrows[j] = h < G ? (int)(((h < 4 ? ra : rc) >> (8 * (h & 3))) & 0xffu) : 0;
     }
-    const unsigned char* Ks = ringK + st * kstage;
-    const unsigned char* Vs = ringV + st * kstage;
+    const unsigned char* Ks = wring + st * stage;
+    const unsigned char* Vs = Ks + kstage;
     for (int r0 = 0; r0 < rmax; r0 += 16) {
       const int nr = min(16, rmax - r0);
       const bool rowok = r < nr;
@@ -548,7 +566,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
       }
       __syncwarp();
     }
-    if (lane == 0) mbar_arrive(&empty[st]);
+    issue(jp + nd);
     pstamp(warp, 64 + i, 0);
   }
 
@@ -673,16 +691,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW >= 8 ? 2 : 3) k_decode_attn(
 // ============================================================================
 // host launcher
 // ============================================================================
-template <typename T, int G, int NW, int NS>
+template <typename T, int G, int NW, int D>
 static size_t attn_smem(int P) {
-  const int ns = attn_stages(NS, P);
-  const size_t ring = (size_t)ns * 2 * attn_stage_rows(P) * (kD * sizeof(T) + 16);
+  const int row = kD * (int)sizeof(T);
+  const size_t ring = (size_t)NW * attn_depth(D, NW, row, P) * attn_stage_bytes(row, P);
   const size_t merge = (size_t)NW * G * kScStride * sizeof(float);
-  return (ring > merge ? ring : merge) + 2 * ns * sizeof(uint64_t) + ns * 8 +
-         (size_t)G * kD * sizeof(T) + (size_t)NW * 16 * G * sizeof(float2);
+  return (ring > merge ? ring : merge) + (size_t)NW * D * 8 + (size_t)G * kD * sizeof(T) +
+         (size_t)NW * 16 * G * sizeof(float2);
 }
 
-// Consumer warps per CTA: DYNSPLIT_ATTN_NW in {4, 8} (default 4: more CTAs beat more warps).
+// Warps per CTA: DYNSPLIT_ATTN_NW in {4, 8} (default 4: 3 CTAs per SM).
 static int attn_nw() {
   static int nw = 0;
   if (!nw) {
@@ -694,14 +712,14 @@ static int attn_nw() {
 
 template <typename T, int G, int NW>
 struct AttnLaunch {
-  static constexpr int NS = sizeof(T) == 2 ? 8 : 4;
+  static constexpr int D = 2;  // pages in flight per warp while it computes one
   static int occupancy(int P) {
     static int occ = 0, lastP = -1;
     if (occ == 0 || lastP != P) {
-      auto kern = k_decode_attn<T, G, NW, NS>;
+      auto kern = k_decode_attn<T, G, NW, D>;
       allow_max_dyn_smem(kern);
       int n = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (NW + 1) * 32, attn_smem<T, G, NW, NS>(P)) !=
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, NW * 32, attn_smem<T, G, NW, D>(P)) !=
               cudaSuccess ||
           n < 1) {
         cudaGetLastError();
@@ -719,8 +737,8 @@ struct AttnLaunch {
                          float* o, float* lse, cudaStream_t st) {
     const int occ = occupancy(P);
     const int n_split = max(1, min(kMaxSplit, (num_sms() * occ) / max(1, B * Hkv)));
-    launch_ex(k_decode_attn<T, G, NW, NS>, dim3(n_split, Hkv, B), dim3((NW + 1) * 32),
-              attn_smem<T, G, NW, NS>(P), st, 1, static_cast<const T*>(q), static_cast<const T*>(Kp),
+    launch_ex(k_decode_attn<T, G, NW, D>, dim3(n_split, Hkv, B), dim3(NW * 32),
+              attn_smem<T, G, NW, D>(P), st, 1, static_cast<const T*>(q), static_cast<const T*>(Kp),
               static_cast<const T*>(Vp), pv, n_pages, wl_hdr, wl_count, wl, dense, Hq, Hkv,
               max_pages, P, scale_log2, part_o, part_lse, counters, n_split, o, lse);
     return post_launch("k_decode_attn", st);

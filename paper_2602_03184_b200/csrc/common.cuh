@@ -207,6 +207,10 @@ DSK_DEVICE uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Bulk prefetch of [src, src + bytes) into L2 (bytes % 16 == 0, 16-byte aligned).
+DSK_DEVICE void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // Programmatic dependent launch: wait until the preceding kernel in the
 // stream has completed (and its writes are visible) / allow the next kernel
 // to be scheduled.  Both are no-ops for a normal launch.

@@ -85,6 +85,21 @@ template <> struct DigestDot<float> {
   }
 };
 
+// Optional per-CTA phase timestamps (debug only; dynsplit_debug_score_timer).
+__device__ unsigned long long* g_score_dbg = nullptr;
+DSK_DEVICE void sstamp(int k) {
+#ifdef DSK_DEBUG
+  if (g_score_dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const size_t cta = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    g_score_dbg[cta * 4 + k] = t;
+  }
+#else
+  (void)k;
+#endif
+}
+
 template <typename T, int G>
 __global__ void __launch_bounds__(256) k_score_blocks(const T* __restrict__ q,
                                                       const T* __restrict__ dig,
@@ -101,11 +116,21 @@ __global__ void __launch_bounds__(256) k_score_blocks(const T* __restrict__ q,
   if (lo >= hi) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int half = lane >> 4, hl = lane & 15;
+  sstamp(0);
 
   const T* dbase = dig + ((size_t)b * Hkv + hk) * (size_t)maxb * 2 * kD;
   float* sbase = scores + ((size_t)b * Hq + hk * G) * maxb;
   constexpr int U = 4;
-  // first batch of digest loads before the (independent) q loads
+  // The digests are the resident cache: before waiting for the preceding
+  // kernel (PDL), pull this CTA's whole digest range towards L2 (bulk
+  // prefetch, 4 KiB per request) and issue the first batch of loads, so the
+  // HBM reads overlap the preceding kernel's tail.
+  {
+    const unsigned char* dp = reinterpret_cast<const unsigned char*>(dbase + (size_t)lo * 2 * kD);
+    const uint32_t bytes = (uint32_t)(hi - lo) * 2 * kD * (uint32_t)sizeof(T);
+    for (uint32_t off = threadIdx.x * 4096u; off < bytes; off += blockDim.x * 4096u)
+      prefetch_l2_bulk(dp + off, min(4096u, bytes - off));
+  }
   typename DD::K kb[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -117,6 +142,7 @@ __global__ void __launch_bounds__(256) k_score_blocks(const T* __restrict__ q,
   // the step -> wait for the preceding kernel (PDL) before touching them
   pdl_trigger();
   pdl_wait();
+  sstamp(1);
   typename DD::Q qv[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) DD::load_q(q + ((size_t)b * Hq + hk * G + g) * kD + hl * 8, qv[g]);
@@ -147,7 +173,14 @@ __global__ void __launch_bounds__(256) k_score_blocks(const T* __restrict__ q,
       }
     }
   }
+  sstamp(2);
 }
+
+}  // namespace dsk
+extern "C" int dynsplit_debug_score_timer(void* dev_ptr) {
+  return (int)cudaMemcpyToSymbol(dsk::g_score_dbg, &dev_ptr, sizeof(void*));
+}
+namespace dsk {
 
 // ============================================================================
 // a8 standalone: merge n_parts (o, lse) partials, fixed part order.

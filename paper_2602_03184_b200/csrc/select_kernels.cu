@@ -30,6 +30,7 @@
 
 #include <cooperative_groups.h>
 #include <math_constants.h>
+#include <stdlib.h>
 
 namespace cg = cooperative_groups;
 
@@ -359,7 +360,8 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   }
 #pragma unroll
   for (int k = 0; k <= G; ++k) v[k] += base[k];
-  WLEntry* wlb = wl + ((size_t)b * Hkv + hk) * max_wl;
+  // interleaved layout: entry e of (b, KV head) bh at wl[e * B * Hkv + bh]
+  const size_t BH = (size_t)gridDim.y * Hkv, bh = (size_t)b * Hkv + hk;
   const int pf_lo = olo < nb ? pf[olo] : 0;
   for (int i = t0; i < t1; ++i) {
     const int blk = lo + r0 + i, len = slen[r0 + i];
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
           if (g < 4) w0 |= r << (8 * g);
           else w1 |= r << (8 * (g - 4));
         }
-        *reinterpret_cast<int4*>(wlb + v[G] + jj) = make_int4(page0 + jj, blk, (int)w0, (int)w1);
+        *reinterpret_cast<int4*>(wl + (v[G] + jj) * BH + bh) = make_int4(page0 + jj, blk, (int)w0, (int)w1);
       }
       v[G] += u;
     }
@@ -406,6 +408,378 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   }
   stamp(8);
   cluster.sync();  // peers may still be reading this CTA's s_info / s_tot
+  stamp(9);
+}
+
+// ============================================================================
+// Register-resident variant for n_blocks <= 8192 (128K context at C = 32,
+// Delta = 14), the decode-step configuration.  Same result as k_select, fewer
+// dependent steps:
+//  * thread t owns blocks i = k * 512 + t (k < 16): its keys and lengths stay
+//    in registers through every pass, so each pass is 16 independent smem
+//    operations instead of a dependent loop over smem;
+//  * the block lengths, page-first table and histogram reset are done before
+//    the PDL wait (they belong to the resident plan);
+//  * a boundary bucket with <= 32 candidates is resolved by one warp ranking
+//    them with shuffles (no sort); larger ones narrow the bucket and repeat;
+//  * each head's selection is published as a bitmask (one ballot word per 32
+//    blocks); the cluster exchanges the G bitmasks once through DSMEM, then
+//    every CTA computes the union page counts for all blocks (16 contiguous
+//    blocks per thread, one block-wide scan) and writes 1/G of the worklist;
+//    sel_blocks positions are popcount prefixes of the head's own bitmask;
+//  * split cluster barriers (arrive early, wait late).
+// ============================================================================
+constexpr int kRK = 16;
+constexpr int kRMax = kSelNT * kRK;  // 8192 blocks
+constexpr int kRW = kRMax / 32;      // 256 selection words per head
+constexpr int kRC = 32;              // candidates ranked by one warp
+
+DSK_DEVICE void cluster_arrive_rel() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+DSK_DEVICE void cluster_wait_acq() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// exclusive block-wide prefix of one int with a single __syncthreads; buf[kSelW]
+// must not be reused until after the next block barrier.  Returns (exclusive, total).
+DSK_DEVICE int2 cta_excl1(int v, int* buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int inc = warp_incl_scan(v);
+  if (lane == 31) buf[warp] = inc;
+  __syncthreads();
+  int before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSelW; ++w) {
+    const int x = buf[w];
+    before += w < warp ? x : 0;
+    tot += x;
+  }
+  return make_int2(before + inc - v, tot);
+}
+
+// dynamic smem: slen[kRMax] u16 | spf[kRMax] i32 | skey0[kRMax] u32 | sbits[G][kRW] u32 | spre[kRW] i32
+static size_t select_reg_smem_bytes(int G) {
+  return (size_t)kRMax * 2 + (size_t)kRMax * 4 * 2 + (size_t)G * kRW * 4 + (size_t)kRW * 4;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
+    const float* __restrict__ scores, const int32_t* __restrict__ block_starts,
+    const int32_t* __restrict__ n_blocks, const int32_t* __restrict__ page_first, int Hq, int Hkv,
+    int maxb, int max_sel, int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
+    int32_t* __restrict__ sel_blocks, int32_t* __restrict__ n_sel, int32_t* __restrict__ marg_out,
+    int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* slen = reinterpret_cast<uint16_t*>(smem);
+  int32_t* spf = reinterpret_cast<int32_t*>(slen + kRMax);
+  uint32_t* skey0 = reinterpret_cast<uint32_t*>(spf + kRMax);  // the head's keys (the narrowing passes kill entries of key[])
+  uint32_t(*sbits)[kRW] = reinterpret_cast<uint32_t(*)[kRW]>(skey0 + kRMax);
+  int32_t* spre = reinterpret_cast<int32_t*>(sbits[G]);
+  __shared__ uint32_t HI[kBkt];
+  __shared__ uint64_t CA[kRC];
+  __shared__ int CL[kRC];
+  __shared__ float red_f[2][kSelW];
+  __shared__ int red_t[kSelW];
+  __shared__ int scan_buf[2][kSelW];
+  __shared__ int s_info[4];     // marginal, keep, threshold key, all_fit of this CTA's head
+  __shared__ int s_pinfo[G][4]; // the same for every head of the cluster
+  __shared__ int s_bnd, s_need, s_nc;
+
+  const int c = (int)cluster.block_rank();
+  const int hk = blockIdx.x / G, b = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = 1 << Pshift;
+  const int nb = n_blocks[b];
+  const int olo = min(max(blk_lo, 0), nb), ohi = max(min(blk_hi, nb), olo);
+  const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
+  const int32_t* pf = page_first + (size_t)b * (maxb + 1);
+  const float* sc = scores + ((size_t)b * Hq + hk * G + c) * maxb;
+
+  stamp(0);
+  // ---- 0. resident plan (overlaps the preceding kernel under PDL)
+  int len[kRK];
+  int tsum = 0;
+#pragma unroll
+  for (int k = 0; k < kRK; ++k) {
+    const int i = k * kSelNT + tid;
+    len[k] = 0;
+    if (i < nb) {
+      len[k] = bs[i + 1] - bs[i];
+      spf[i] = pf[i];
+    }
+    slen[i] = (uint16_t)len[k];  // 0 beyond nb (the union pass reads whole words)
+    tsum += len[k];
+  }
+  for (int j = tid; j < kBkt; j += kSelNT) HI[j] = 0;
+  if (tid == 0) s_nc = 0;
+  stamp(1);
+  pdl_trigger();
+  pdl_wait();
+  stamp(2);
+  // ---- 1. keys of this CTA's head
+  uint32_t key[kRK];
+#pragma unroll
+  for (int k = 0; k < kRK; ++k) {
+    const int i = k * kSelNT + tid;
+    key[k] = i < nb ? float_key(__ldcg(sc + i)) : 0u;
+    skey0[i] = key[k];
+  }
+  stamp(3);
+
+  // ---- 2. threshold: marginal block (index, keep) and its key
+  int need = budget;
+  bool first = true;
+  for (;;) {
+    float mn = CUDART_INF_F, mx = -CUDART_INF_F;
+#pragma unroll
+    for (int k = 0; k < kRK; ++k) {
+      if (key[k]) {
+        const float f = key_to_float(key[k]);
+        mn = fminf(mn, f);
+        mx = fmaxf(mx, f);
+      }
+    }
+    mn = -warp_max(-mn);
+    mx = warp_max(mx);
+    const int ts = first ? warp_sum_i(tsum) : 0;
+    if (lane == 0) {
+      red_f[0][warp] = mn;
+      red_f[1][warp] = mx;
+      red_t[warp] = ts;
+    }
+    __syncthreads();
+    int total = 0;
+#pragma unroll
+    for (int w = 0; w < kSelW; ++w) {
+      mn = fminf(mn, red_f[0][w]);
+      mx = fmaxf(mx, red_f[1][w]);
+      total += red_t[w];
+    }
+    if (first && total <= budget) {
+      if (tid == 0) {
+        s_info[0] = -1;
+        s_info[1] = 0;
+        s_info[2] = 0;
+        s_info[3] = 1;
+      }
+      break;
+    }
+    first = false;
+    if (!(mx > mn)) {
+      // every live key is equal: index order (i = k * 512 + t is chunk k, thread t)
+      int carry = 0;
+#pragma unroll 1
+      for (int k = 0; k < kRK && carry < need; ++k) {
+        int v = 0;
+#pragma unroll
+        for (int kk = 0; kk < kRK; ++kk)
+          if (kk == k) v = key[kk] ? len[kk] : 0;
+        const int2 pre = cta_excl1(v, scan_buf[k & 1]);
+        const int before = carry + pre.x;
+        if (v > 0 && before < need && before + v >= need) {
+          uint32_t kk0 = 0;
+#pragma unroll
+          for (int kk = 0; kk < kRK; ++kk)
+            if (kk == k) kk0 = key[kk];
+          s_info[0] = k * kSelNT + tid;
+          s_info[1] = need - before;
+          s_info[2] = (int)kk0;
+          s_info[3] = 0;
+        }
+        carry += pre.y;
+      }
+      break;
+    }
+    const float inv = (float)kBkt / (mx - mn);
+#pragma unroll
+    for (int k = 0; k < kRK; ++k)
+      if (key[k]) atomicAdd(&HI[bucket_of(key[k], mn, inv)], (uint32_t)len[k]);
+    __syncthreads();
+    {  // suffix scan: thread tid owns buckets kBkt-1-4tid downwards
+      const int j0 = kBkt - 1 - tid * kBPT;
+      int h[kBPT], loc = 0;
+#pragma unroll
+      for (int k = 0; k < kBPT; ++k) {
+        h[k] = (int)HI[j0 - k];
+        loc += h[k];
+      }
+      int above = cta_excl1(loc, scan_buf[0]).x;
+#pragma unroll
+      for (int k = 0; k < kBPT; ++k) {
+        if (above < need && above + h[k] >= need) {
+          s_bnd = j0 - k;
+          s_need = need - above;
+        }
+        above += h[k];
+      }
+    }
+    __syncthreads();
+    const int bnd = s_bnd;
+    need = s_need;
+#pragma unroll
+    for (int k = 0; k < kRK; ++k) {
+      if (key[k]) {
+        if (bucket_of(key[k], mn, inv) == bnd) {
+          const int p = atomicAdd(&s_nc, 1);
+          if (p < kRC) {
+            CA[p] = ((uint64_t)key[k] << 32) | (uint64_t)(0xffffffffu - (uint32_t)(k * kSelNT + tid));
+            CL[p] = len[k];
+          }
+        } else {
+          key[k] = 0;  // above (already counted in need) or below: no longer live
+        }
+      }
+    }
+    for (int j = tid; j < kBkt; j += kSelNT) HI[j] = 0;  // for a narrowing pass
+    __syncthreads();
+    const int nc = s_nc;
+    __syncthreads();  // everyone has read s_nc
+    if (nc > kRC) {
+      if (tid == 0) s_nc = 0;
+      continue;  // narrow to the boundary bucket
+    }
+    if (warp == 0) {
+      // rank the candidates: order (key desc, index asc) == CA desc
+      const uint64_t mine = lane < nc ? CA[lane] : 0ull;
+      const int ml = lane < nc ? CL[lane] : 0;
+      int before = 0;
+      for (int j = 0; j < nc; ++j) {
+        const uint64_t o = __shfl_sync(0xffffffffu, mine, j);
+        const int ol = __shfl_sync(0xffffffffu, ml, j);
+        before += (o > mine) ? ol : 0;
+      }
+      if (lane < nc && before < need && before + ml >= need) {
+        s_info[0] = (int)(0xffffffffu - (uint32_t)(mine & 0xffffffffull));
+        s_info[1] = need - before;
+        s_info[2] = (int)(uint32_t)(mine >> 32);
+        s_info[3] = 0;
+      }
+    }
+    break;
+  }
+  __syncthreads();
+  stamp(4);
+
+  // ---- 3. this head's selection bitmask (ballot words), published to the cluster
+  const int m_c = s_info[0], keep_c = s_info[1], all_c = s_info[3];
+  const uint32_t T_c = (uint32_t)s_info[2];
+#pragma unroll
+  for (int k = 0; k < kRK; ++k) {
+    const int i = k * kSelNT + tid;
+    const uint32_t k0 = skey0[i];
+    const bool sel = i < nb && (all_c || k0 > T_c || (k0 == T_c && i <= m_c));
+    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0) sbits[c][k * kSelW + warp] = word;
+  }
+  __syncthreads();
+  cluster_arrive_rel();  // s_info and sbits[c] are visible to the peers
+  stamp(5);
+
+  // ---- 4. sel_blocks of this head (ascending): popcount prefix over its words
+  {
+    const int x = tid < kRW ? __popc(sbits[c][tid]) : 0;
+    const int2 pre = cta_excl1(x, scan_buf[1]);
+    if (tid < kRW) spre[tid] = pre.x;
+    __syncthreads();
+    if (sel_blocks) {
+      int32_t* out = sel_blocks + ((size_t)b * Hq + hk * G + c) * max_sel;
+      const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+      for (int k = 0; k < kRK; ++k) {
+        const uint32_t word = sbits[c][k * kSelW + warp];
+        if ((word >> lane) & 1u) out[spre[k * kSelW + warp] + __popc(word & lt)] = k * kSelNT + tid;
+      }
+    }
+    if (tid == 0) {
+      const size_t o = (size_t)b * Hq + hk * G + c;
+      n_sel[o] = pre.y;
+      marg_out[o] = all_c ? -1 : m_c;
+      keep_out[o] = all_c ? 0 : keep_c;
+    }
+  }
+
+  // ---- 5. the peers' selections (DSMEM), then the union worklist
+  cluster_wait_acq();
+  stamp(6);
+  for (int j = tid; j < G * kRW; j += kSelNT) {
+    const int g = j / kRW, w = j % kRW;
+    if (g != c) sbits[g][w] = cluster.map_shared_rank(&sbits[g][0], g)[w];
+  }
+  if (tid < G * 4) s_pinfo[tid / 4][tid % 4] = cluster.map_shared_rank(s_info, tid / 4)[tid % 4];
+  __syncthreads();
+  cluster_arrive_rel();  // done reading the peers' shared memory
+  int mg[G], kg[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    mg[g] = s_pinfo[g][3] ? -1 : s_pinfo[g][0];
+    kg[g] = s_pinfo[g][1];
+  }
+  // thread tid: blocks [16 tid, 16 tid + 16) -> bits (tid & 1) * 16.. of word tid / 2
+  const int blk0 = tid * kRK;
+  uint32_t hb[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) hb[g] = (sbits[g][tid >> 1] >> ((tid & 1) * 16)) & 0xffffu;
+  uint32_t anyb = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) anyb |= hb[g];
+  // blocks outside the output range [olo, ohi) emit no worklist entries
+  const int jlo = min(max(olo - blk0, 0), kRK), jhi = min(max(ohi - blk0, 0), kRK);
+  anyb &= ((jhi >= 32 ? 0u : (1u << jhi)) - 1u) & ~((1u << jlo) - 1u);
+  // union page count of block blk0 + j (rolled loops over the set bits only:
+  // this kernel runs once per layer, so code size is latency)
+  auto union_pages = [&](int j, int ln) {
+    int u = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if ((hb[g] >> j) & 1u) {
+        const int tk = blk0 + j == mg[g] ? kg[g] : ln;
+        u = max(u, (tk + P - 1) >> Pshift);
+      }
+    }
+    return u;
+  };
+  int tot_pages = 0;
+#pragma unroll 1
+  for (uint32_t bits = anyb; bits; bits &= bits - 1u) {
+    const int j = __ffs(bits) - 1;
+    tot_pages += union_pages(j, slen[blk0 + j]);
+  }
+  const int2 wpre = cta_excl1(tot_pages, scan_buf[0]);
+  stamp(7);
+  if ((tid % G) == c && tot_pages) {
+    // interleaved layout: entry e of (b, KV head) bh at wl[e * B * Hkv + bh]
+  const size_t BH = (size_t)gridDim.y * Hkv, bh = (size_t)b * Hkv + hk;
+    const int pf_lo = olo < nb ? spf[olo] : 0;
+    int v = wpre.x;
+#pragma unroll 1
+    for (uint32_t bits = anyb; bits; bits &= bits - 1u) {
+      const int j = __ffs(bits) - 1;
+      const int blk = blk0 + j, ln = slen[blk];
+      const int u = union_pages(j, ln);
+      const int page0 = spf[blk] - pf_lo;
+#pragma unroll 1
+      for (int jj = 0; jj < u; ++jj) {
+        const int pv = min(P, ln - (jj << Pshift));
+        uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int tk = ((hb[g] >> j) & 1u) ? (blk == mg[g] ? kg[g] : ln) : 0;
+          const uint32_t r = (uint32_t)min(max(tk - (jj << Pshift), 0), pv);
+          if (g < 4) w0 |= r << (8 * g);
+          else w1 |= r << (8 * (g - 4));
+        }
+        *reinterpret_cast<int4*>(wl + (v + jj) * BH + bh) = make_int4(page0 + jj, blk, (int)w0, (int)w1);
+      }
+      v += u;
+    }
+  }
+  if (tid == 0 && c == 0) {
+    if (hk == 0 && b == 0) {
+      wl_count[-64] = 0x44534b57;  // "DSKW"
+      wl_count[-63] = max_wl;
+    }
+    wl_count[(size_t)b * Hkv + hk] = wpre.y;
+  }
+  stamp(8);
+  cluster_wait_acq();  // peers may still be reading this CTA's s_info / sbits
   stamp(9);
 }
 
@@ -429,7 +803,15 @@ static cudaError_t run_select(int B, int Hkv, size_t smem, const float* scores, 
   static bool attr = false;
   if (!attr) {
     allow_max_dyn_smem(k_select<G>);
+    allow_max_dyn_smem(k_select_reg<G>);
     attr = true;
+  }
+  static const bool force_generic = getenv("DYNSPLIT_SELECT_GENERIC") != nullptr;  // A/B only
+  if (maxb <= kRMax && !force_generic) {
+    launch_ex(k_select_reg<G>, dim3(Hkv * G, B), dim3(kSelNT), select_reg_smem_bytes(G), st, G, scores,
+              bs, nb, pf, Hq, Hkv, maxb, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks,
+              n_sel, marg, keep, wl_count, wl);
+    return post_launch("k_select_reg", st);
   }
   launch_ex(k_select<G>, dim3(Hkv * G, B), dim3(kSelNT), smem, st, G, scores, bs, nb, pf, Hq, Hkv,
             maxb, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep,

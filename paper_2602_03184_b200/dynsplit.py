@@ -442,7 +442,8 @@ def worklist_rows(worklist: torch.Tensor, shape: Shape, G: int):
     """Host-side reading of a worklist (metrics only): per (b, KV head) the
     number of page entries and of rows streamed (max over the G heads of each
     entry's row count).  Layout: 256-byte header, int32 counts [B*Hkv] padded to
-    256 bytes, then 16-byte entries {int32 page, int32 block, uint8 rows[8]}."""
+    256 bytes, then 16-byte entries {int32 page, int32 block, uint8 rows[8]},
+    interleaved: entry e of (b, KV head) bh at index e * B * Hkv + bh."""
     import numpy as np
     raw = worklist.cpu().numpy()
     nbh = shape.B * shape.Hkv
@@ -450,7 +451,7 @@ def worklist_rows(worklist: torch.Tensor, shape: Shape, G: int):
     max_wl = int(hdr[1])
     counts = raw[256:256 + 4 * nbh].view(np.int32).copy()
     off = 256 + ((4 * nbh + 255) // 256) * 256
-    ent = raw[off: off + 16 * nbh * max_wl].reshape(nbh, max_wl, 16)
+    ent = raw[off: off + 16 * nbh * max_wl].reshape(max_wl, nbh, 16).transpose(1, 0, 2)
     rows = ent[:, :, 8:8 + G].max(axis=2).astype(np.int64)
     streamed = np.array([rows[i, : counts[i]].sum() for i in range(nbh)])
     return counts, streamed

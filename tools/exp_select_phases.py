@@ -35,6 +35,6 @@ lib.dynsplit_debug_select_timer(ctypes.c_void_p(0))
 t = dbg.view(-1, 16).cpu().numpy()[:, :10].astype(np.float64)
 t0 = t[:, 0].min()
 rel = (t - t0) / 1e3
-names = ["start", "lens", "pdl_wait", "keys+total", "threshold", "csync1", "union_sumk", "scan", "csync2+writes", "csync3"]
+names = ["start", "lens", "pdl_wait", "keys+total", "threshold", "csync1", "union_sumk", "scan", "csync2+writes", "csync3"] if os.environ.get("DYNSPLIT_SELECT_GENERIC") else ["start", "plan", "pdl_wait", "keys", "threshold", "bits+arrive", "wait+peers", "union_scan", "writes", "final_wait"]
 for k, n in enumerate(names):
     print(f"{n:14s} min {rel[:, k].min():7.2f} med {np.median(rel[:, k]):7.2f} max {rel[:, k].max():7.2f} us")
