@@ -787,6 +787,16 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
 extern "C" int dynsplit_debug_select_timer(void* dev_ptr) {
   return (int)cudaMemcpyToSymbol(dsk::g_sel_dbg, &dev_ptr, sizeof(void*));
 }
+// Test hook: 1 forces the generic k_select for every shape (parity of the two
+// select kernels); 0 restores the default dispatch.  Initial value from
+// DYNSPLIT_SELECT_GENERIC.
+namespace dsk {
+static bool g_select_generic = getenv("DYNSPLIT_SELECT_GENERIC") != nullptr;
+}
+extern "C" int dynsplit_debug_select_generic(int on) {
+  dsk::g_select_generic = on != 0;
+  return 0;
+}
 namespace dsk {
 
 size_t select_smem_needed(int maxb, int G) {
@@ -806,8 +816,7 @@ static cudaError_t run_select(int B, int Hkv, size_t smem, const float* scores, 
     allow_max_dyn_smem(k_select_reg<G>);
     attr = true;
   }
-  static const bool force_generic = getenv("DYNSPLIT_SELECT_GENERIC") != nullptr;  // A/B only
-  if (maxb <= kRMax && !force_generic) {
+  if (maxb <= kRMax && !g_select_generic) {
     launch_ex(k_select_reg<G>, dim3(Hkv * G, B), dim3(kSelNT), select_reg_smem_bytes(G), st, G, scores,
               bs, nb, pf, Hq, Hkv, maxb, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks,
               n_sel, marg, keep, wl_count, wl);

@@ -349,3 +349,66 @@ def test_dynamic_build_blocks_parity(D):
         kmax, kmin = O.digests(K[b], st_ref)
         dig = layer.digests[b, :, :nb].float().cpu().numpy()
         assert np.array_equal(dig[:, :, 0], kmax) and np.array_equal(dig[:, :, 1], kmin)
+
+
+# ---------------------------------------------------------------- the two a6 kernels agree
+def _wl_entries(wl, B, Hkv):
+    raw = wl.cpu().numpy()
+    nbh = B * Hkv
+    max_wl = int(raw[:256].view(np.int32)[1])
+    counts = raw[256:256 + 4 * nbh].view(np.int32).copy()
+    off = 256 + ((4 * nbh + 255) // 256) * 256
+    ent = raw[off: off + 16 * nbh * max_wl].reshape(max_wl, nbh, 16)
+    return counts, [ent[: counts[i], i].copy() for i in range(nbh)]
+
+
+@pytest.mark.parametrize("kind,S,Hq,Hkv,budget", [
+    ("float", 8192, 32, 8, 1024),      # C3 head layout
+    ("int", 3000, 16, 2, 300),         # integer scores: many exact ties
+    ("zero", 2500, 8, 4, 200),         # q = 0: every score equal -> index order
+    ("float", 1500, 8, 8, 100000),     # everything fits
+    ("float", 40, 4, 4, 5),            # a handful of blocks
+])
+def test_select_kernels_agree(D, kind, S, Hq, Hkv, budget):
+    """k_select_reg (register-resident, <= 8192 blocks) and the generic
+    k_select produce bit-identical selections, marginals and worklists."""
+    import ctypes
+    B, d = 2, 128
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(900 + b, S) for b in range(B)])
+    if kind == "int":
+        qs, Ks, Vs = zip(*[G.decode_qkv_integer(910 + b, S, Hq, Hkv, d) for b in range(B)])
+    else:
+        qs, Ks, Vs = zip(*[G.decode_qkv(910 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    if kind == "zero":
+        q = np.zeros_like(q)
+    layer = _build(D, toks, K, V, cfg, "bf16", Hq)
+    qt = t(q, torch.bfloat16)
+    lib = D.lib()
+    lib.dynsplit_debug_select_generic.argtypes = [ctypes.c_int]
+    reg = D.select(qt, layer, budget)
+    torch.cuda.synchronize()
+    try:
+        lib.dynsplit_debug_select_generic(1)
+        gen = D.select(qt, layer, budget)
+        torch.cuda.synchronize()
+    finally:
+        lib.dynsplit_debug_select_generic(0)
+    for name in ("n_sel", "marginal_block", "marginal_keep"):
+        assert torch.equal(getattr(reg, name), getattr(gen, name)), name
+    ns = reg.n_sel.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            assert torch.equal(reg.sel_blocks[b, h, : ns[b, h]], gen.sel_blocks[b, h, : ns[b, h]])
+    cf, ef = _wl_entries(reg.worklist, B, Hkv)
+    cr, er = _wl_entries(gen.worklist, B, Hkv)
+    assert np.array_equal(cf, cr)
+    for a, c in zip(ef, er):
+        assert np.array_equal(a, c)
+    if kind == "zero":   # all scores equal: whole blocks in index order
+        for b in range(B):
+            st = layer.block_starts[b, : int(layer.n_blocks[b]) + 1].cpu().numpy()
+            m = int(np.searchsorted(st, budget - 1, side="right")) - 1
+            assert reg.marginal_block[b].tolist() == [m] * Hq
+            assert reg.marginal_keep[b].tolist() == [budget - int(st[m])] * Hq

@@ -78,17 +78,29 @@ def main():
             for l in range(L):
                 D.decode_attn(qs[l], layers[l], sels[l][4], out=outs[l], ws=ws_dec)
 
-        def full():
-            score()
-            selfs()
-            attn()
+        def full():  # the step as two kernels a5 | a6 per layer, interleaved with a7
+            for l in range(L):
+                D.score_blocks(qs[l], layers[l], out=scores[l])
+                D.select_from_scores(scores[l], layers[l], budget, Hq, out=sels[l], ws=ws_sel)
+                D.decode_attn(qs[l], layers[l], sels[l][4], out=outs[l], ws=ws_dec)
 
-        t_s, t_f, t_a, t_all = (time_graph(f) / L for f in (score, selfs, attn, full))
+        def fsel():
+            for l in range(L):
+                sb, ns, mg, kp, wl = sels[l]
+                D.select(qs[l], layers[l], budget, out=(sb, ns, mg, kp, wl, None), ws=ws_sel)
+
+        def fused():  # the step as bench.py runs it: dynsplit_select (a5+a6), then a7, per layer
+            for l in range(L):
+                sb, ns, mg, kp, wl = sels[l]
+                D.select(qs[l], layers[l], budget, out=(sb, ns, mg, kp, wl, None), ws=ws_sel)
+                D.decode_attn(qs[l], layers[l], sels[l][4], out=outs[l], ws=ws_dec)
+
+        t_s, t_f, t_a, t_all, t_fs, t_fu = (time_graph(f) / L for f in (score, selfs, attn, full, fsel, fused))
         rows = sum(int(D.worklist_rows(sels[l][4], shape, Hq // Hkv)[1].sum()) for l in range(L)) / L
         mbytes = rows * 2 * d * 2 / 2**20
-        print(f"budget {budget:6d}: score {t_s:6.1f} us | select {t_f:6.1f} us | attn {t_a:6.1f} us "
-              f"({mbytes:6.1f} MiB, {mbytes * 2**20 / (t_a * 1e-6) / 1e9:6.0f} GB/s) | layer {t_all:6.1f} us")
-
+        print(f"budget {budget:6d}: score {t_s:5.1f} | select {t_f:5.1f} | select() {t_fs:5.1f} | attn {t_a:5.1f} us "
+              f"({mbytes:6.1f} MiB, {mbytes * 2**20 / (t_a * 1e-6) / 1e9:5.0f} GB/s) | layer: 3-kernel {t_all:5.1f} "
+              f"bench step {t_fu:5.1f} us")
 
 if __name__ == "__main__":
     main()

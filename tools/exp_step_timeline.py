@@ -40,10 +40,17 @@ ws_sel = D.workspace(D.workspace_bytes(D.OP_SELECT, shape, cfg, budget), dev, "s
 ws_dec = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "decode")
 
 
+FUSED = True  # dynsplit_select (a5 + a6 through one ABI call)
+
+
 def step():
     for l in range(L):
-        D.score_blocks(qs[l], layers[l], out=scores[l])
-        D.select_from_scores(scores[l], layers[l], budget, Hq, out=sels[l], ws=ws_sel)
+        if FUSED:
+            sb, ns, mg, kp, wl = sels[l]
+            D.select(qs[l], layers[l], budget, out=(sb, ns, mg, kp, wl, None), ws=ws_sel)
+        else:
+            D.score_blocks(qs[l], layers[l], out=scores[l])
+            D.select_from_scores(scores[l], layers[l], budget, Hq, out=sels[l], ws=ws_sel)
         D.decode_attn(qs[l], layers[l], sels[l][4], out=outs[l], ws=ws_dec)
 
 
