@@ -56,7 +56,8 @@ typedef enum {
   DYNSPLIT_OP_SEGMENT = 1,
   DYNSPLIT_OP_BUILD_BLOCKS = 2,
   DYNSPLIT_OP_SELECT = 3,
-  DYNSPLIT_OP_DECODE_ATTN = 4
+  DYNSPLIT_OP_DECODE_ATTN = 4,
+  DYNSPLIT_OP_DECODE_LAYER = 5
 } dynsplit_op;
 
 typedef struct {
@@ -246,6 +247,23 @@ dynsplit_status dynsplit_decode_attn(const dynsplit_shape* shape, const dynsplit
                                      const void* worklist, float scale, float* o, float* lse,
                                      void* ws, size_t ws_bytes, void* stream);
 
+/* Decode, rows a5-a8 of one layer in one call (the device-resident decode
+ * step): dynsplit_score_blocks, the a6 selection of
+ * dynsplit_select_from_scores over the whole sequence, then
+ * dynsplit_decode_attn on its worklist.
+ * Arguments as in dynsplit_select / dynsplit_decode_attn (q, digests, plan,
+ * Kp, Vp resident on the device); n_sel, marginal_block, marginal_keep (out)
+ * int32 [B, Hq]; worklist (out) as in dynsplit_select; o, lse (out) as in
+ * dynsplit_decode_attn.  Block scores and sel_blocks are not returned.
+ * Workspace: DYNSPLIT_OP_DECODE_LAYER (= DECODE_ATTN + SELECT). */
+dynsplit_status dynsplit_decode_layer(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                      int32_t budget, const void* q, const void* digests,
+                                      const int32_t* block_starts, const int32_t* n_blocks,
+                                      const int32_t* page_first, const void* Kp, const void* Vp,
+                                      float scale, int32_t* n_sel, int32_t* marginal_block,
+                                      int32_t* marginal_keep, void* worklist, float* o, float* lse,
+                                      void* ws, size_t ws_bytes, void* stream);
+
 /* Row a8 standalone (cross-GPU merge of sequence-split shards):
  *   o_parts fp32 [n_parts, rows, d], lse_parts fp32 [n_parts, rows] ->
  *   lse = log sum_s exp(lse_s), o = sum_s exp(lse_s - lse) o_s, fixed part order. */
@@ -255,8 +273,9 @@ dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_p
 
 /* One full decode step (a5-a8) with HOST query and outputs: copies q_host
  * (pinned, kv dtype [B, Hq, d]) to the workspace, runs select + decode_attn,
- * and copies o/lse back to o_host/lse_host (pinned).  Asynchronous like every
- * other entry point: synchronise `stream` before reading o_host.
+ * (dynsplit_decode_layer) and copies o/lse back to o_host/lse_host (pinned).
+ * Asynchronous like every other entry point: synchronise `stream` before
+ * reading o_host.  page_valid is accepted for API stability (unused).
  * Workspace: dynsplit_workspace_bytes(DYNSPLIT_OP_SELECT) +
  * dynsplit_workspace_bytes(DYNSPLIT_OP_DECODE_ATTN) + q/o/lse staging
  * (see dynsplit_step_host_workspace_bytes). */

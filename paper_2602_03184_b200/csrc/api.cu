@@ -157,6 +157,10 @@ size_t build_ws(const dynsplit_shape* s) {
   // scoring partials + delim scores (if not returned) + segment next[]
   return score_ws(s) + align_up((size_t)s->B * s->S * 4) + segment_ws(s);
 }
+// dynsplit_decode_layer: decode workspace (counters at offset 0) then select's.
+size_t layer_ws(const dynsplit_shape* s, const dynsplit_config* c) {
+  return decode_ws(s) + select_ws(s, c);
+}
 size_t step_host_extra(const dynsplit_shape* s) {
   return align_up((size_t)s->B * s->Hq * kD * esize(s)) + align_up((size_t)s->B * s->Hq * kD * 4) +
          align_up((size_t)s->B * s->Hq * 4) + 3 * align_up((size_t)s->B * s->Hq * 4);
@@ -218,6 +222,7 @@ size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* s, const dynsp
     case DYNSPLIT_OP_BUILD_BLOCKS: return build_ws(s);
     case DYNSPLIT_OP_SELECT: return select_ws(s, c);
     case DYNSPLIT_OP_DECODE_ATTN: return decode_ws(s);
+    case DYNSPLIT_OP_DECODE_LAYER: return layer_ws(s, c);
     default: return 0;
   }
 }
@@ -368,13 +373,14 @@ dynsplit_status dynsplit_score_blocks(const dynsplit_shape* s, const dynsplit_co
                                          static_cast<cudaStream_t>(stream)));
 }
 
-dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* s, const dynsplit_config* c,
-                                            int32_t budget, const float* scores,
-                                            const int32_t* block_starts, const int32_t* n_blocks,
-                                            const int32_t* page_first, int32_t blk_lo,
-                                            int32_t blk_hi, int32_t* sel_blocks, int32_t* n_sel,
-                                            int32_t* marginal_block, int32_t* marginal_keep,
-                                            void* worklist, void* ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+// a6 (shared by dynsplit_select_from_scores and dynsplit_decode_layer).
+static dynsplit_status select_impl(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,
+                                   const float* scores, const int32_t* block_starts,
+                                   const int32_t* n_blocks, const int32_t* page_first, int32_t blk_lo,
+                                   int32_t blk_hi, int32_t* sel_blocks, int32_t* n_sel,
+                                   int32_t* marginal_block, int32_t* marginal_keep, void* worklist,
+                                   void* ws, size_t ws_bytes, void* stream) {
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (budget < 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
@@ -394,6 +400,19 @@ dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* s, const dynsp
                                    sel_blocks, n_sel, marginal_block, marginal_keep, v.count,
                                    v.entries, static_cast<cudaStream_t>(stream)));
 }
+extern "C" {
+
+dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* s, const dynsplit_config* c,
+                                            int32_t budget, const float* scores,
+                                            const int32_t* block_starts, const int32_t* n_blocks,
+                                            const int32_t* page_first, int32_t blk_lo,
+                                            int32_t blk_hi, int32_t* sel_blocks, int32_t* n_sel,
+                                            int32_t* marginal_block, int32_t* marginal_keep,
+                                            void* worklist, void* ws, size_t ws_bytes, void* stream) {
+  return select_impl(s, c, budget, scores, block_starts, n_blocks, page_first, blk_lo, blk_hi,
+                     sel_blocks, n_sel, marginal_block, marginal_keep, worklist, ws, ws_bytes, stream);
+}
+
 
 dynsplit_status dynsplit_select(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,
                                 const void* q, const void* digests, const int32_t* block_starts,
@@ -446,6 +465,28 @@ dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_con
                                         static_cast<cudaStream_t>(stream)));
 }
 
+dynsplit_status dynsplit_decode_layer(const dynsplit_shape* s, const dynsplit_config* c,
+                                      int32_t budget, const void* q, const void* digests,
+                                      const int32_t* block_starts, const int32_t* n_blocks,
+                                      const int32_t* page_first, const void* Kp, const void* Vp,
+                                      float scale, int32_t* n_sel, int32_t* marginal_block,
+                                      int32_t* marginal_keep, void* worklist, float* o, float* lse,
+                                      void* ws, size_t ws_bytes, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!q || !digests || !Kp || !Vp || !o || !lse || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < layer_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  char* w = static_cast<char*>(ws);
+  char* ws_dec = w;  // counters first: shape-independent offset
+  char* ws_sel = w + decode_ws(s);
+  float* sc = reinterpret_cast<float*>(ws_sel);
+  DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
+  DSK_TRY(select_impl(s, c, budget, sc, block_starts, n_blocks, page_first, 0, 0x7fffffff, nullptr,
+                      n_sel, marginal_block, marginal_keep, worklist, ws_sel, select_ws(s, c), stream));
+  return dynsplit_decode_attn(s, c, q, Kp, Vp, nullptr, nullptr, worklist, scale, o, lse, ws_dec,
+                              decode_ws(s), stream);
+}
+
 dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_parts,
                                         int32_t n_parts, int32_t rows, int32_t d, float* o,
                                         float* lse, void* stream) {
@@ -481,10 +522,11 @@ dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* s, const dynspli
   int32_t* keep = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(marg) + align_up((size_t)s->B * s->Hq * 4));
   if (cudaMemcpyAsync(q_dev, q_host, qbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return DYNSPLIT_ERR_CUDA;
-  DSK_TRY(dynsplit_select(s, c, budget, q_dev, digests, block_starts, n_blocks, page_first, nullptr,
-                          nullptr, nsel, marg, keep, worklist, ws_sel, select_ws(s, c), stream));
-  DSK_TRY(dynsplit_decode_attn(s, c, q_dev, Kp, Vp, page_valid, nullptr, worklist, scale, o_dev,
-                               lse_dev, ws_dec, decode_ws(s), stream));
+  (void)page_valid;
+  (void)ws_sel;
+  DSK_TRY(dynsplit_decode_layer(s, c, budget, q_dev, digests, block_starts, n_blocks, page_first, Kp,
+                                Vp, scale, nsel, marg, keep, worklist, o_dev, lse_dev, ws_dec,
+                                layer_ws(s, c), stream));
   if (cudaMemcpyAsync(o_host, o_dev, (size_t)s->B * s->Hq * kD * 4, cudaMemcpyDeviceToHost, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(lse_host, lse_dev, (size_t)s->B * s->Hq * 4, cudaMemcpyDeviceToHost, st) !=

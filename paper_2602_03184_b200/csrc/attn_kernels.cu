@@ -114,14 +114,15 @@ template <> struct QK<float> {
 // Ring geometry: every consumer warp owns a private ring of `depth` stages;
 // a stage holds max(P, 16) padded K rows followed by as many V rows (the bf16
 // tensor-core path consumes 16-row tiles).  The depth is D for P <= 16 bf16
-// pages and shrinks (>= 1) so that the CTA's rings stay within kRingBudget.
-constexpr int kRingBudget = 72 * 1024;
+// pages and shrinks (>= 1) so that the CTA's rings stay within the budget:
+// 72 KiB with 4 warps (3 CTAs per SM), 210 KiB with more (one CTA per SM).
+__host__ __device__ inline size_t attn_ring_budget(int NW) { return NW <= 4 ? 72 * 1024 : 210 * 1024; }
 __host__ __device__ inline int attn_stage_rows(int P) { return P < 16 ? 16 : P; }
 __host__ __device__ inline size_t attn_stage_bytes(int row_bytes, int P) {
   return (size_t)2 * attn_stage_rows(P) * (row_bytes + 16);
 }
 __host__ __device__ inline int attn_depth(int D, int NW, int row_bytes, int P) {
-  const int n = (int)(kRingBudget / ((size_t)NW * attn_stage_bytes(row_bytes, P)));
+  const int n = (int)(attn_ring_budget(NW) / ((size_t)NW * attn_stage_bytes(row_bytes, P)));
   return n < 1 ? 1 : (n > D ? D : n);
 }
 DSK_DEVICE void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -700,19 +701,22 @@ static size_t attn_smem(int P) {
          (size_t)NW * 16 * G * sizeof(float2);
 }
 
-// Warps per CTA: DYNSPLIT_ATTN_NW in {4, 8} (default 4: 3 CTAs per SM).
+// Warps per CTA: DYNSPLIT_ATTN_NW in {4, 8, 12}.  Default 8 (one CTA per SM,
+// 3-deep rings): measured best at 128K / budget 4096 (15.4 us vs 17.7 with
+// 4 warps x 3 CTAs per SM): fewer split partials to merge.
 static int attn_nw() {
   static int nw = 0;
   if (!nw) {
     const char* e = getenv("DYNSPLIT_ATTN_NW");
-    nw = (e && atoi(e) == 8) ? 8 : 4;
+    const int v = e ? atoi(e) : 8;
+    nw = (v == 4 || v == 12) ? v : 8;
   }
   return nw;
 }
 
 template <typename T, int G, int NW>
 struct AttnLaunch {
-  static constexpr int D = 2;  // pages in flight per warp while it computes one
+  static constexpr int D = 2;  // pages in flight per warp while it computes one (3 measured slower)
   static int occupancy(int P) {
     static int occ = 0, lastP = -1;
     if (occ == 0 || lastP != P) {
@@ -754,6 +758,9 @@ static cudaError_t attn_run(const void* q, const void* Kp, const void* Vp, const
   if (attn_nw() == 4)
     return AttnLaunch<T, G, 4>::run(q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
                                     max_pages, P, sl2, part_o, part_lse, counters, o, lse, st);
+  if (attn_nw() == 12)
+    return AttnLaunch<T, G, 12>::run(q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
+                                     max_pages, P, sl2, part_o, part_lse, counters, o, lse, st);
   return AttnLaunch<T, G, 8>::run(q, Kp, Vp, pv, n_pages, wl_hdr, wl_count, wl, dense, B, Hq, Hkv,
                                   max_pages, P, sl2, part_o, part_lse, counters, o, lse, st);
 }

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit_debug.so" if os.environ.get("D
 
 OK = 0
 BF16, FP32 = 0, 1
-OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN = range(5)
+OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN, OP_DECODE_LAYER = range(6)
 INT32_MAX = 0x7FFFFFFF
 
 
@@ -74,6 +74,8 @@ SIGNATURES = {
     "dynsplit_select": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_decode_attn": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, ctypes.c_float, _P, _P, _P,
                                   _SZ, _P]),
+    "dynsplit_decode_layer": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, ctypes.c_float, _P, _P,
+                                   _P, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_merge_partials": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
     "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
@@ -405,6 +407,28 @@ def decode_attn(q, layer: PagedLayer, worklist: Optional[torch.Tensor], scale: f
         _ptr(layer.page_valid), _ptr(layer.n_pages), _ptr(worklist), ctypes.c_float(scale),
         _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream()), "decode_attn")
     return o, lse
+
+
+def decode_layer(q, layer: PagedLayer, budget: int, scale: float = 0.0, out=None, ws=None):
+    """Rows a5-a8 of one layer through dynsplit_decode_layer (score, select,
+    attention in one call).  out = (n_sel, marginal_block,
+    marginal_keep, worklist, o, lse) preallocated, or None.
+    -> (o, lse, Selection without scores / sel_blocks)."""
+    shape = _decode_shape(q, layer)
+    if out is None:
+        _, ns, mg, kp, wl = _sel_outputs(shape, layer.cfg, budget, q.device, want_blocks=False)
+        o = torch.empty(shape.B, shape.Hq, shape.d, dtype=torch.float32, device=q.device)
+        lse = torch.empty(shape.B, shape.Hq, dtype=torch.float32, device=q.device)
+    else:
+        ns, mg, kp, wl, o, lse = out
+    if ws is None:
+        ws = workspace(workspace_bytes(OP_DECODE_LAYER, shape, layer.cfg, budget), q.device, "layer")
+    _check(lib().dynsplit_decode_layer(
+        ctypes.byref(shape), ctypes.byref(layer.cfg), budget, _ptr(q), _ptr(layer.digests),
+        _ptr(layer.block_starts), _ptr(layer.n_blocks), _ptr(layer.page_first), _ptr(layer.Kp),
+        _ptr(layer.Vp), ctypes.c_float(scale), _ptr(ns), _ptr(mg), _ptr(kp), _ptr(wl), _ptr(o),
+        _ptr(lse), _ptr(ws), ws.numel(), _stream()), "decode_layer")
+    return o, lse, Selection(None, ns, mg, kp, wl, None)
 
 
 def merge_partials(o_parts, lse_parts):

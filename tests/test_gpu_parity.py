@@ -412,3 +412,27 @@ def test_select_kernels_agree(D, kind, S, Hq, Hkv, budget):
             m = int(np.searchsorted(st, budget - 1, side="right")) - 1
             assert reg.marginal_block[b].tolist() == [m] * Hq
             assert reg.marginal_keep[b].tolist() == [budget - int(st[m])] * Hq
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,budget", [(8192, 32, 8, 1024), (3000, 8, 2, 5000), (2000, 8, 8, 1)])
+def test_decode_layer_matches_separate_calls(D, S, Hq, Hkv, budget):
+    """dynsplit_decode_layer (a5-a8 in one call) == dynsplit_select +
+    dynsplit_decode_attn bit for bit, and == the oracle."""
+    B, d = 2, 128
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(950 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    qs, Ks, Vs = zip(*[G.decode_qkv(960 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    q = H.certify_queries(960, q, K, starts, budget, "bf16")
+    layer = _build(D, toks, K, V, cfg, "bf16", Hq)
+    qt = t(q, torch.bfloat16)
+    o1, lse1, sel1 = D.decode_layer(qt, layer, budget)
+    sel2 = D.select(qt, layer, budget)
+    o2, lse2 = D.decode_attn(qt, layer, sel2.worklist)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(lse1, lse2)
+    for name in ("n_sel", "marginal_block", "marginal_keep"):
+        assert torch.equal(getattr(sel1, name), getattr(sel2, name)), name
+    res = H.oracle_decode(q, K, V, starts, budget)
+    _check_attention(o1, lse1, res, B, Hq)

@@ -95,12 +95,21 @@ def main():
                 D.select(qs[l], layers[l], budget, out=(sb, ns, mg, kp, wl, None), ws=ws_sel)
                 D.decode_attn(qs[l], layers[l], sels[l][4], out=outs[l], ws=ws_dec)
 
-        t_s, t_f, t_a, t_all, t_fs, t_fu = (time_graph(f) / L for f in (score, selfs, attn, full, fsel, fused))
+        ws_lay = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer")
+
+        def layer_api():  # dynsplit_decode_layer per layer
+            for l in range(L):
+                _, ns, mg, kp, wl = sels[l]
+                D.decode_layer(qs[l], layers[l], budget, out=(ns, mg, kp, wl, outs[l][0], outs[l][1]),
+                               ws=ws_lay)
+
+        t_s, t_f, t_a, t_all, t_fs, t_fu, t_ly = (time_graph(f) / L for f in (score, selfs, attn, full, fsel,
+                                                                              fused, layer_api))
         rows = sum(int(D.worklist_rows(sels[l][4], shape, Hq // Hkv)[1].sum()) for l in range(L)) / L
         mbytes = rows * 2 * d * 2 / 2**20
         print(f"budget {budget:6d}: score {t_s:5.1f} | select {t_f:5.1f} | select() {t_fs:5.1f} | attn {t_a:5.1f} us "
               f"({mbytes:6.1f} MiB, {mbytes * 2**20 / (t_a * 1e-6) / 1e9:5.0f} GB/s) | layer: 3-kernel {t_all:5.1f} "
-              f"bench step {t_fu:5.1f} us")
+              f"select()+attn {t_fu:5.1f} | decode_layer {t_ly:5.1f} us")
 
 if __name__ == "__main__":
     main()
