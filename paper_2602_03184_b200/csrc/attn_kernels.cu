@@ -638,38 +638,39 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
   named_bar_sync(1, NW * 32);
   if (threadIdx.x == 0) astamp(4);
   if (!s_last) return;
-  // Last CTA of (b, KV head): LSE merge of the n_eff splits.  Lanes hold the
-  // split lse values (n_eff <= 64), weights by warp reductions (fixed
-  // butterfly order), then o = sum_s w_s o_s in split order, 16 loads in
-  // flight per lane (the first batch issued before the weights are known).
-  for (int h = warp; h < G; h += NW) {
+  // Last CTA of (b, KV head): LSE merge of the n_eff splits.  R = NW / G
+  // warps share a head: every warp reads all split lse values (lanes hold
+  // them, n_eff <= 64) and forms the weights by warp reductions (fixed
+  // butterfly order); warp part r sums w_s o_s over the splits s = r (mod R)
+  // with all its loads in flight at once (n_eff / R <= 16 per lane); the R
+  // parts are added in part order through shared memory.
+  constexpr int R = NW >= G ? NW / G : 1;
+  float* mrg = reinterpret_cast<float*>(smem);  // [G][R][kD]
+  const int hm = warp % G, part = warp / G;
+  if (warp < G * R) {
+    const int h = hm;
     const size_t row = (size_t)b * Hq + hk * G + h;
     const float* pl = part_lse + row * n_split;
     const float4* po_base = reinterpret_cast<const float4*>(part_o + row * n_split * kD) + lane;
     const float l0 = lane < n_eff ? __ldcg(pl + lane) : -CUDART_INF_F;
     const float l1 = lane + 32 < n_eff ? __ldcg(pl + lane + 32) : -CUDART_INF_F;
-    float4 po[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      po[k] = k < n_eff ? __ldcg(po_base + (size_t)k * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float M = warp_max(fmaxf(l0, l1));
     float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float M = warp_max(fmaxf(l0, l1));
     float L = -CUDART_INF_F;
     if (M != -CUDART_INF_F) {
       const float sum = warp_sum(expf(l0 - M) + expf(l1 - M));
       L = M + logf(sum);
       const float w0 = expf(l0 - L), w1 = expf(l1 - L);
-      for (int s0 = 0; s0 < n_eff; s0 += 16) {
-        if (s0) {
+      for (int s0 = part; s0 < n_eff; s0 += 16 * R) {
+        float4 po[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int s = s0 + k;
-            po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+        for (int k = 0; k < 16; ++k) {
+          const int s = s0 + k * R;
+          po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const int s = s0 + k;
+          const int s = s0 + k * R;
           const float w = __shfl_sync(0xffffffffu, s < 32 ? w0 : w1, s & 31);
           if (s < n_eff) {
             ov.x += w * po[k].x;
@@ -680,8 +681,28 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
         }
       }
     }
-    reinterpret_cast<float4*>(o + row * kD)[lane] = ov;
-    if (lane == 0) lse[row] = L;
+    if (R == 1) {
+      reinterpret_cast<float4*>(o + row * kD)[lane] = ov;
+      if (lane == 0) lse[row] = L;
+    } else {
+      reinterpret_cast<float4*>(mrg + (h * R + part) * kD)[lane] = ov;
+      if (part == 0 && lane == 0) lse[row] = L;
+    }
+  }
+  if (R > 1) {
+    named_bar_sync(1, NW * 32);
+    for (int j = threadIdx.x; j < G * (kD / 4); j += NW * 32) {
+      const int h = j / (kD / 4), c = j % (kD / 4);
+      float4 acc = reinterpret_cast<const float4*>(mrg + (h * R) * kD)[c];
+      for (int rr = 1; rr < R; ++rr) {
+        const float4 x = reinterpret_cast<const float4*>(mrg + (h * R + rr) * kD)[c];
+        acc.x += x.x;
+        acc.y += x.y;
+        acc.z += x.z;
+        acc.w += x.w;
+      }
+      reinterpret_cast<float4*>(o + ((size_t)b * Hq + hk * G + h) * kD)[c] = acc;
+    }
   }
   if (threadIdx.x == 0) {
     counters[bh] = 0;
