@@ -13,7 +13,7 @@
 namespace dsk {
 
 // ============================================================================
-// a5: block scores.  grid (chunks, Hkv, B), 256 threads.  A half-warp owns one
+// a5: block scores (k_score_blocks below: grid, staging).  A half-warp owns one
 // block digest (512 B bf16: kmax row + kmin row); lane hl owns dims
 // [8hl, 8hl+8).  max(q_j kmax_j, q_j kmin_j) = q_j * (q_j >= 0 ? kmax_j : kmin_j)
 // because kmax >= kmin element-wise; for bf16 the per-head choice is one
@@ -44,6 +44,10 @@ template <> struct DigestDot<bf16> {
     k.mx = __ldg(reinterpret_cast<const uint4*>(p));
     k.mn = __ldg(reinterpret_cast<const uint4*>(p + kD));
   }
+  static DSK_DEVICE void load_k_smem(const bf16* p, K& k) {
+    k.mx = *reinterpret_cast<const uint4*>(p);
+    k.mn = *reinterpret_cast<const uint4*>(p + kD);
+  }
   static DSK_DEVICE void zero_k(K& k) { k.mx = k.mn = make_uint4(0, 0, 0, 0); }
   static DSK_DEVICE float dot(const Q& q, const K& k) {
     const uint32_t mx[4] = {k.mx.x, k.mx.y, k.mx.z, k.mx.w};
@@ -73,6 +77,10 @@ template <> struct DigestDot<float> {
     Vec<float>::load8_nc(p, k.mx);
     Vec<float>::load8_nc(p + kD, k.mn);
   }
+  static DSK_DEVICE void load_k_smem(const float* p, K& k) {
+    Vec<float>::load8(p, k.mx);
+    Vec<float>::load8(p + kD, k.mn);
+  }
   static DSK_DEVICE void zero_k(K& k) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) k.mx[j] = k.mn[j] = 0.f;
@@ -100,77 +108,78 @@ DSK_DEVICE void sstamp(int k) {
 #endif
 }
 
+// grid (chunks, Hkv, B), 512 threads, one CTA per SM on chunks * B * Hkv SMs
+// (the launcher leaves enough SMs free for the select kernel's CTAs, which
+// can then become resident -- and load their plan -- while this one runs).
+// Before the PDL wait the CTA's whole digest range (resident data, <= `cap`
+// blocks) is copied into shared memory with TMA bulk copies, so its HBM read
+// overlaps the preceding kernel's tail; after the wait only q is loaded.
 template <typename T, int G>
-__global__ void __launch_bounds__(256) k_score_blocks(const T* __restrict__ q,
-                                                      const T* __restrict__ dig,
-                                                      const int32_t* __restrict__ n_blocks,
-                                                      float* __restrict__ scores, int Hq, int Hkv,
-                                                      int maxb) {
+__global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q,
+                                                         const T* __restrict__ dig,
+                                                         const int32_t* __restrict__ n_blocks,
+                                                         float* __restrict__ scores, int Hq, int Hkv,
+                                                         int maxb, int cap) {
   using DD = DigestDot<T>;
+  constexpr int RB = 2 * kD * (int)sizeof(T);  // digest bytes per block (kmax, kmin)
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
   const int hk = blockIdx.y, b = blockIdx.z;
   const int nb = n_blocks[b];
-  int per = (nb + gridDim.x - 1) / gridDim.x;
-  per = (per + 15) & ~15;
+  const int per = (nb + gridDim.x - 1) / gridDim.x;
   const int lo = blockIdx.x * per;
   const int hi = min(nb, lo + per);
-  if (lo >= hi) return;
+  const int n = max(hi - lo, 0);
+  const int pre = min(n, cap);  // blocks staged in shared memory
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int half = lane >> 4, hl = lane & 15;
   sstamp(0);
 
   const T* dbase = dig + ((size_t)b * Hkv + hk) * (size_t)maxb * 2 * kD;
   float* sbase = scores + ((size_t)b * Hq + hk * G) * maxb;
-  constexpr int U = 4;
-  // The digests are the resident cache: before waiting for the preceding
-  // kernel (PDL), pull this CTA's whole digest range towards L2 (bulk
-  // prefetch, 4 KiB per request) and issue the first batch of loads, so the
-  // HBM reads overlap the preceding kernel's tail.
-  {
-    const unsigned char* dp = reinterpret_cast<const unsigned char*>(dbase + (size_t)lo * 2 * kD);
-    const uint32_t bytes = (uint32_t)(hi - lo) * 2 * kD * (uint32_t)sizeof(T);
-    for (uint32_t off = threadIdx.x * 4096u; off < bytes; off += blockDim.x * 4096u)
-      prefetch_l2_bulk(dp + off, min(4096u, bytes - off));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    if (pre) {
+      const uint32_t bytes = (uint32_t)pre * RB;
+      mbar_arrive_expect_tx(&bar, bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(dbase + (size_t)lo * 2 * kD);
+      for (uint32_t off = 0; off < bytes; off += 32768u)
+        bulk_g2s(smem + off, src + off, min(32768u, bytes - off), &bar, policy_evict_first());
+    } else {
+      mbar_arrive(&bar);
+    }
   }
-  typename DD::K kb[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int blk = lo + warp * 2 + u * 16 + half;
-    if (blk < hi) DD::load_k(dbase + (size_t)blk * 2 * kD + hl * 8, kb[u]);
-    else DD::zero_k(kb[u]);
-  }
-  // the digests are the resident cache; q (and the scores buffer) belong to
-  // the step -> wait for the preceding kernel (PDL) before touching them
+  // q (and the scores buffer) belong to the step -> after the PDL wait
   pdl_trigger();
   pdl_wait();
   sstamp(1);
   typename DD::Q qv[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) DD::load_q(q + ((size_t)b * Hq + hk * G + g) * kD + hl * 8, qv[g]);
+  __syncthreads();  // the barrier's initialisation is visible
+  mbar_wait(&bar, 0);
+  __syncwarp();
 
-  for (int base = lo + warp * 2; base < hi; base += 16 * U) {
-    if (base != lo + warp * 2) {
+  // a half-warp per block; lane hl owns dims [8 hl, 8 hl + 8) of kmax / kmin
+  const T* sd = reinterpret_cast<const T*>(smem);
+  for (int base = warp * 2; base < n; base += 32) {  // warp-uniform trip count
+    const int i = base + half;
+    typename DD::K kb;
+    if (i < pre) DD::load_k_smem(sd + (size_t)i * 2 * kD + hl * 8, kb);
+    else if (i < n) DD::load_k(dbase + (size_t)(lo + i) * 2 * kD + hl * 8, kb);
+    else DD::zero_k(kb);
+    float acc[G];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int blk = base + u * 16 + half;
-        if (blk < hi) DD::load_k(dbase + (size_t)blk * 2 * kD + hl * 8, kb[u]);
-        else DD::zero_k(kb[u]);
-      }
+    for (int g = 0; g < G; ++g) acc[g] = DD::dot(qv[g], kb);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
     }
+    if (hl == 0 && i < n) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int blk = base + u * 16 + half;
-      float acc[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) acc[g] = DD::dot(qv[g], kb[u]);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-      }
-      if (hl == 0 && blk < hi) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) sbase[(size_t)g * maxb + blk] = acc[g];
-      }
+      for (int g = 0; g < G; ++g) sbase[(size_t)g * maxb + lo + i] = acc[g];
     }
   }
   sstamp(2);
@@ -211,22 +220,39 @@ __global__ void k_merge_partials(const float* __restrict__ o_parts, const float*
 // ============================================================================
 // host launchers
 // ============================================================================
+// Chunks per (b, KV head): the SMs left after reserving one per select CTA
+// (B * Hq of them, at most a quarter of the GPU); shared-memory staging of up
+// to 192 KiB of digests per CTA (blocks beyond it are read from HBM directly).
 template <typename T>
 static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const int32_t* nb,
                                   float* scores, int B, int Hq, int Hkv, int maxb, cudaStream_t st) {
   const int sms = num_sms();
-  int chunks = max(1, (sms * 4) / max(1, B * Hkv));
-  chunks = min(chunks, max(1, (maxb + 15) / 16));
+  const int reserve = min(B * Hq, sms / 4);
+  const int chunks = max(1, min((sms - reserve) / max(1, B * Hkv), (maxb + 31) / 32));
+  const int rb = 2 * kD * (int)sizeof(T);
+  const int cap = min((maxb + chunks - 1) / chunks, (192 * 1024) / rb);
+  const size_t smem = (size_t)cap * rb;
   dim3 grid(chunks, Hkv, B);
   const T* qq = static_cast<const T*>(q);
   const T* dd = static_cast<const T*>(dig);
+#define DSK_SC(GG)                                                                                   \
+  {                                                                                                  \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      allow_max_dyn_smem(k_score_blocks<T, GG>);                                                     \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    launch_ex(k_score_blocks<T, GG>, grid, 512, smem, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb, cap); \
+    break;                                                                                           \
+  }
   switch (G) {
-    case 1: launch_ex(k_score_blocks<T, 1>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
-    case 2: launch_ex(k_score_blocks<T, 2>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
-    case 4: launch_ex(k_score_blocks<T, 4>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
-    case 8: launch_ex(k_score_blocks<T, 8>, grid, 256, 0, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb); break;
+    case 1: DSK_SC(1)
+    case 2: DSK_SC(2)
+    case 4: DSK_SC(4)
+    case 8: DSK_SC(8)
     default: return cudaErrorInvalidValue;
   }
+#undef DSK_SC
   return post_launch(__func__, st);
 }
 
