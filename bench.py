@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -385,6 +386,36 @@ def main():
     h2d = L * B * Hq * d * e
     d2h = L * B * Hq * (d + 1) * 4
 
+    # ---- prefill row a1 (context, not the headline): Alg. 1 delimiter scoring
+    #      of one sequence-layer at S_pf (C5 shape: 32Q/8KV, bf16), one launch pair
+    prefill = None
+    if rank == 0 and not args.no_prefill:
+        S_pf = min(S, 32768)
+        gpf = torch.Generator(device=dev)
+        gpf.manual_seed(args.seed + 17)
+        toks_pf = toks[:1, :S_pf].contiguous()
+        Qs = torch.randn(1, 1, S_pf, Hq, d, generator=gpf, device=dev).to(torch.bfloat16)
+        Ks = torch.randn(1, 1, S_pf, Hkv, d, generator=gpf, device=dev).to(torch.bfloat16)
+        D.score_delimiters(toks_pf, ids, Qs, Ks, cfg)
+        torch.cuda.synchronize()
+        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pa.record(cur)
+        for _ in range(3):
+            D.score_delimiters(toks_pf, ids, Qs, Ks, cfg)
+        pb.record(cur)
+        torch.cuda.synchronize()
+        pf_ms = pa.elapsed_time(pb) / 3
+        # algorithmic work: causal Q.K^T and exps of every query row
+        # (all rows are computed; ~86 % are needed at this delimiter density)
+        rows = np.arange(S_pf, dtype=np.float64) + 1
+        flop = 2.0 * d * Hq * rows.sum()
+        exps = Hq * rows.sum()
+        prefill = {"row": "a1 k_lse_band + k_score_reduce", "seq_len": S_pf, "heads_q": Hq, "heads_kv": Hkv,
+                   "ms": pf_ms, "tflops": flop / (pf_ms * 1e-3) / 1e12,
+                   "tflops_peak": 1395.5, "exp_per_s": exps / (pf_ms * 1e-3),
+                   "note": "bf16 mma.sync tensor cores + MUFU ex2; peak = MEASURED_PEAKS bf16 sustained"}
+        del Qs, Ks
+
     # ---- dense baseline (row a9): every page, every head
     dense_ms = None
     if not args.no_dense:
@@ -472,6 +503,8 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        if prefill:
+            line["prefill"] = prefill
         if dense_ms:
             dense_bytes = L * B * Hkv * S * 2 * d * e
             line["dense"] = {"ms_per_step": dense_ms_v, "GB_s": dense_bytes / (dense_ms_v * 1e-3) / 1e9,
