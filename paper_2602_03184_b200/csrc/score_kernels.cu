@@ -22,6 +22,7 @@
 #include "kernels.h"
 
 #include <math_constants.h>
+#include <stdlib.h>
 
 namespace dsk {
 
@@ -278,9 +279,260 @@ __global__ void __launch_bounds__(128) k_lse_band(const int32_t* __restrict__ to
   }
 }
 
+
+// ============================================================================
+// tcgen05 version of k_lse_band (the default): one CTA per (128-row tile,
+// head, layer*batch), 6 warps.
+//   warp 4 (loader): the Q tile once and the K tiles of both passes with
+//     16-byte cp.async into 128-byte-swizzled K-major smem tiles (two 64-dim
+//     halves), 2 stages; after its copies land: fence.proxy.async + mbarrier.
+//   warp 5 lane 0 (MMA): S = Q K^T for a 128-key tile as 8 x
+//     tcgen05.mma.cta_group::1.kind::f16 (M = 128 rows, N = 128 keys, K = 16
+//     dims each, bf16 in, fp32 accumulate) into one of two 128-column TMEM
+//     accumulators; tcgen05.commit frees the K stage and publishes S.
+//   warps 0-3 (epilogue): thread t of warp w owns row 32 w + t: tcgen05.ld
+//     32x32b of its row (4 x 32 columns), then pass 1: online max / sum in the
+//     exp2 domain (no shuffles: a row is in one thread); pass 2 (the band
+//     tiles): p = exp2(z - lse2) accumulated into Ov[w], Fut[w] as in
+//     k_lse_band.  Per candidate, rows summed in row order into its slot.
+// TMEM: 256 columns (2 accumulators); smem 3 x 32 KiB + 1 KiB alignment.
+// ============================================================================
+constexpr int kTcRows = 128;   // rows per CTA (M) = keys per tile (N)
+constexpr int kTcStage = 2;
+constexpr int kTcTileBytes = kTcRows * kD * 2;  // 32 KiB
+
+DSK_DEVICE uint64_t umma_sdesc_sw128(uint32_t saddr) {
+  // K-major, SWIZZLE_128B: 128-byte rows, 8-row atoms of 1024 B (SBO), LBO
+  // unused, descriptor version 1, layout type 2
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+DSK_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+DSK_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+DSK_DEVICE void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+DSK_DEVICE void tc_ld32(uint32_t addr, float (&f)[32]) {
+  uint32_t v[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,"
+      "%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+}
+
+__global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restrict__ tokens,
+                                                       const int32_t* __restrict__ delim_ids, int n_ids,
+                                                       const bf16* __restrict__ Qs,
+                                                       const bf16* __restrict__ Ks, int B, int S, int Hq,
+                                                       int Hkv, int W, int R, float alpha,
+                                                       float scale_log2, float* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // 1024-byte aligned tiles (the swizzle atoms are address-based)
+  const uint32_t raw_s = smem_u32(smem_raw);
+  unsigned char* smem = smem_raw + (((raw_s + 1023u) & ~1023u) - raw_s);
+  unsigned char* sQ = smem;                       // [2 halves][128 rows][128 B]
+  unsigned char* sK = smem + kTcTileBytes;        // [kTcStage][2 halves][128 rows][128 B]
+  float* cbuf = reinterpret_cast<float*>(sK);     // [128][kMaxW], after the last MMA
+  __shared__ __align__(8) uint64_t kfull[kTcStage], kempty[kTcStage], sfull[2], sempty[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_ids[64];
+
+  const int tile = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, lb = blockIdx.z;  // heaviest tiles first
+  const int b = lb % B;
+  const int g = Hq / Hkv, hk = h / g;
+  const int r0 = tile * kTcRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int band = W + R - 1;
+  const int T = tile;                                   // diagonal key tile
+  const int kb0 = max(0, r0 - band) / kTcRows;          // first band tile
+  const int n1 = T + 1, n_all = n1 + (T - kb0 + 1);     // pass-1 tiles, all tiles
+  auto tile_of = [&](int i) { return i < n1 ? i : kb0 + (i - n1); };
+
+  if (threadIdx.x < n_ids) s_ids[threadIdx.x] = delim_ids[threadIdx.x];
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTcStage; ++st) {
+      mbar_init(&kfull[st], 32);
+      mbar_init(&kempty[st], 1);
+    }
+    for (int bb = 0; bb < 2; ++bb) {
+      mbar_init(&sfull[bb], 1);
+      mbar_init(&sempty[bb], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  const size_t ldq = (size_t)Hq * kD, ldk = (size_t)Hkv * kD;
+  const bf16* Qbase = Qs + (size_t)lb * S * ldq + (size_t)h * kD;
+  const bf16* Kbase = Ks + (size_t)lb * S * ldk + (size_t)hk * kD;
+
+  if (warp == 4) {  // ------------------------------------------------ loader
+    // 16-byte chunk c (of 16) of row r -> half c / 8, swizzled slot (c % 8) ^ (r % 8)
+    auto load_rows = [&](unsigned char* dst, const bf16* src, size_t ld, int row0) {
+      for (int e = lane; e < kTcRows * 16; e += 32) {
+        const int r = e >> 4, c = e & 15;
+        const bool ok = row0 + r < S;
+        const int half = c >> 3, slot = (c & 7) ^ (r & 7);
+        cp_async16(dst + half * (kTcRows * 128) + r * 128 + slot * 16,
+                   src + (size_t)(ok ? row0 + r : 0) * ld + c * 8, ok);
+      }
+    };
+    load_rows(sQ, Qbase, ldq, r0);  // lands with tile 0's group
+    for (int i = 0; i < n_all; ++i) {
+      const int st = i % kTcStage;
+      if (i >= kTcStage) mbar_wait(&kempty[st], ((i / kTcStage) - 1) & 1);
+      load_rows(sK + st * kTcTileBytes, Kbase, ldk, tile_of(i) * kTcRows);
+      cp_async_commit();
+      if (i >= 1) {
+        cp_async_wait<1>();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&kfull[(i - 1) % kTcStage]);
+      }
+    }
+    cp_async_wait<0>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(&kfull[(n_all - 1) % kTcStage]);
+  } else if (warp == 5) {  // ---------------------------------------- MMA issue
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcRows >> 3) << 17) |
+                           ((uint32_t)(kTcRows >> 4) << 24);
+    for (int i = 0; i < n_all; ++i) {
+      const int st = i % kTcStage, bb = i & 1;
+      mbar_wait(&kfull[st], (i / kTcStage) & 1);
+      if (i >= 2) mbar_wait(&sempty[bb], ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + st * kTcTileBytes);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint32_t off = (uint32_t)((k >> 2) * (kTcRows * 128) + (k & 3) * 32);
+          const uint64_t da = umma_sdesc_sw128(qa + off), db = umma_sdesc_sw128(ka + off);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + bb * kTcRows),
+              "l"(da), "l"(db), "r"(idesc), "r"((uint32_t)(k > 0)));
+        }
+        tc_commit(&sfull[bb]);
+        tc_commit(&kempty[st]);
+      }
+      __syncwarp();
+    }
+  } else {  // ---------------------------------------------------- epilogue
+    const int lr = warp * 32 + lane, row = r0 + lr;
+    float m = -CUDART_INF_F, l = 0.f, lse2 = 0.f;
+    float ov_all = 0.f, ov[kMaxW], fu[kMaxW];
+#pragma unroll
+    for (int w = 0; w < kMaxW; ++w) ov[w] = fu[w] = 0.f;
+    for (int i = 0; i < n_all; ++i) {
+      const int bb = i & 1, kt = tile_of(i);
+      mbar_wait(&sfull[bb], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(bb * kTcRows);
+      if (i == n1) lse2 = m + __log2f(l);  // pass 1 complete
+      for (int c0 = 0; c0 < kTcRows; c0 += 32) {
+        float z[32];
+        __syncwarp();  // .aligned TMEM loads need the converged warp
+        tc_ld32(base + (uint32_t)c0, z);
+        if (c0 + 32 >= kTcRows) {  // the accumulator may be overwritten now
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sempty[bb]);
+        }
+        const int key0 = kt * kTcRows + c0;
+        if (i < n1) {
+          float tmax = -CUDART_INF_F;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float v = z[j] * scale_log2;
+            if (key0 + j > row) v = -CUDART_INF_F;  // causal (only the diagonal tile has such keys)
+            z[j] = v;
+            tmax = fmaxf(tmax, v);
+          }
+          const float mn = fmaxf(m, tmax);
+          float ls = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) ls += ex2(z[j] - mn);
+          l = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mn)) + ls;
+          m = mn;
+        } else {
+          // band: dk = row - key in [0, band]
+          const int dk0 = row - key0;
+          if (dk0 < 0 || dk0 - 31 > band) continue;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int dk = dk0 - j;
+            if (dk < 0 || dk > band) continue;
+            const float p = ex2(z[j] * scale_log2 - lse2);
+            if (dk >= W && dk <= R) {
+              ov_all += p;
+            } else {
+#pragma unroll
+              for (int w = 1; w <= kMaxW; ++w) {
+                if (w > W) break;
+                if (dk < w) fu[w - 1] += p;
+                else if (dk <= w + R - 1) ov[w - 1] += p;
+              }
+            }
+          }
+        }
+      }
+    }
+    // every MMA has completed (the last sfull was waited): the K stages are free
+    named_bar_sync(1, 128);
+    const int32_t* tk = tokens + (size_t)b * S;
+    auto is_cand = [&](int i) -> bool {
+      if (i < 0 || i > S - 2) return false;
+      const int t = tk[i];
+      for (int j = 0; j < n_ids; ++j)
+        if (s_ids[j] == t) return true;
+      return false;
+    };
+#pragma unroll
+    for (int w = 1; w <= kMaxW; ++w) {
+      float c = 0.f;
+      const int i = row - w;
+      if (w <= W && row < S && is_cand(i)) {
+        const float o_ = ov_all + ov[w - 1];
+        const float dr = (i >= R) ? (1.f - o_ - fu[w - 1]) : 0.f;
+        c = o_ - alpha * dr;
+      }
+      cbuf[lr * kMaxW + (w - 1)] = c;
+    }
+    named_bar_sync(1, 128);
+    for (int ti = threadIdx.x; ti < kTcRows + W - 1; ti += 128) {
+      const int i = r0 - W + ti;
+      if (!is_cand(i)) continue;
+      const int q0 = max(i + 1, r0), q1 = min(min(i + W, S - 1), r0 + kTcRows - 1);
+      if (q0 > q1) continue;
+      float sacc = 0.f;
+      for (int q = q0; q <= q1; ++q) sacc += cbuf[(q - r0) * kMaxW + (q - i - 1)];
+      const int slot = (i + 1 >= r0) ? 0 : 1;
+      part[(((size_t)lb * Hq + h) * S + i) * 2 + slot] = sacc;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 __global__ void k_score_reduce(const int32_t* __restrict__ tokens, const int32_t* __restrict__ delim_ids,
                                int n_ids, const float* __restrict__ part, int Ls, int B, int S, int Hq,
-                               int W, float* __restrict__ out) {
+                               int W, int rows_per_tile, float* __restrict__ out) {
   __shared__ int s_ids[64];
   if (threadIdx.x < n_ids) s_ids[threadIdx.x] = delim_ids[threadIdx.x];
   __syncthreads();
@@ -295,7 +547,7 @@ __global__ void k_score_reduce(const int32_t* __restrict__ tokens, const int32_t
     return;
   }
   const int qlast = min(i + W, S - 1);
-  const bool two = ((i + 1) / kRowsPerCta) != (qlast / kRowsPerCta);
+  const bool two = ((i + 1) / rows_per_tile) != (qlast / rows_per_tile);
   double acc = 0.0;
   for (int l = 0; l < Ls; ++l)
     for (int h = 0; h < Hq; ++h) {
@@ -314,23 +566,41 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
                                     const void* Qs, const void* Ks, int Ls, int B, int S, int Hq,
                                     int Hkv, int W, int R, float alpha, float* out, void* ws,
                                     cudaStream_t st) {
-  const size_t smem = (size_t)(kRowsPerCta + 2 * kKeyTile) * kLds * sizeof(bf16) +
-                      kRowsPerCta * kMaxW * sizeof(float);
-  static bool attr_done = false;
-  if (!attr_done) {
-    allow_max_dyn_smem(k_lse_band);
-    attr_done = true;
-  }
+  // tcgen05 kernel by default; DYNSPLIT_A1_MMASYNC=1 selects the mma.sync kernel (A/B)
+  static const bool mmasync = getenv("DYNSPLIT_A1_MMASYNC") != nullptr;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
   float* part = static_cast<float*>(ws);
-  dim3 grid((S + kRowsPerCta - 1) / kRowsPerCta, Hq, Ls * B);
-  k_lse_band<<<grid, 128, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
-                                      static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,
-                                      scale_log2, part);
+  int rows_per_tile;
+  if (!mmasync) {
+    const size_t smem = (size_t)(1 + kTcStage) * kTcTileBytes + 1024;
+    static bool attr_tc = false;
+    if (!attr_tc) {
+      allow_max_dyn_smem(k_lse_band_tc);
+      attr_tc = true;
+    }
+    dim3 grid((S + kTcRows - 1) / kTcRows, Hq, Ls * B);
+    k_lse_band_tc<<<grid, 192, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
+                                           static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,
+                                           scale_log2, part);
+    rows_per_tile = kTcRows;
+  } else {
+    const size_t smem = (size_t)(kRowsPerCta + 2 * kKeyTile) * kLds * sizeof(bf16) +
+                        kRowsPerCta * kMaxW * sizeof(float);
+    static bool attr_done = false;
+    if (!attr_done) {
+      allow_max_dyn_smem(k_lse_band);
+      attr_done = true;
+    }
+    dim3 grid((S + kRowsPerCta - 1) / kRowsPerCta, Hq, Ls * B);
+    k_lse_band<<<grid, 128, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
+                                        static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,
+                                        scale_log2, part);
+    rows_per_tile = kRowsPerCta;
+  }
   cudaError_t e = post_launch(__func__, st);
   if (e != cudaSuccess) return e;
   k_score_reduce<<<dim3((S + 255) / 256, B), 256, 0, st>>>(tokens, delim_ids, n_ids, part, Ls, B, S,
-                                                           Hq, W, out);
+                                                           Hq, W, rows_per_tile, out);
   return post_launch(__func__, st);
 }
 
