@@ -413,7 +413,7 @@ def main():
         prefill = {"row": "a1 k_lse_band + k_score_reduce", "seq_len": S_pf, "heads_q": Hq, "heads_kv": Hkv,
                    "ms": pf_ms, "tflops": flop / (pf_ms * 1e-3) / 1e12,
                    "tflops_peak": 1395.5, "exp_per_s": exps / (pf_ms * 1e-3),
-                   "note": "bf16 mma.sync tensor cores + MUFU ex2; peak = MEASURED_PEAKS bf16 sustained"}
+                   "note": "tcgen05 (UMMA 128x128x16, TMEM) + MUFU ex2; peak = MEASURED_PEAKS bf16 sustained"}
         del Qs, Ks
 
     # ---- dense baseline (row a9): every page, every head

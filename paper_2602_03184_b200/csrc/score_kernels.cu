@@ -282,19 +282,20 @@ __global__ void __launch_bounds__(128) k_lse_band(const int32_t* __restrict__ to
 
 // ============================================================================
 // tcgen05 version of k_lse_band (the default): one CTA per (128-row tile,
-// head, layer*batch), 6 warps.
-//   warp 4 (loader): the Q tile once and the K tiles of both passes with
+// head, layer*batch), 10 warps.
+//   warp 8 (loader): the Q tile once and the K tiles of both passes with
 //     16-byte cp.async into 128-byte-swizzled K-major smem tiles (two 64-dim
 //     halves), 2 stages; after its copies land: fence.proxy.async + mbarrier.
-//   warp 5 lane 0 (MMA): S = Q K^T for a 128-key tile as 8 x
+//   warp 9 lane 0 (MMA): S = Q K^T for a 128-key tile as 8 x
 //     tcgen05.mma.cta_group::1.kind::f16 (M = 128 rows, N = 128 keys, K = 16
 //     dims each, bf16 in, fp32 accumulate) into one of two 128-column TMEM
 //     accumulators; tcgen05.commit frees the K stage and publishes S.
-//   warps 0-3 (epilogue): thread t of warp w owns row 32 w + t: tcgen05.ld
-//     32x32b of its row (4 x 32 columns), then pass 1: online max / sum in the
-//     exp2 domain (no shuffles: a row is in one thread); pass 2 (the band
-//     tiles): p = exp2(z - lse2) accumulated into Ov[w], Fut[w] as in
-//     k_lse_band.  Per candidate, rows summed in row order into its slot.
+//   warps 0-7 (epilogue): warp w reads TMEM lane quadrant w % 4 (rows
+//     32 (w % 4) + lane) and column half w / 4 of every tile with tcgen05.ld
+//     32x32b; a row's two halves keep separate online (max, sum) in the exp2
+//     domain (pass 1) and separate band sums Ov[w], Fut[w] (pass 2:
+//     p = exp2(z - lse2) over the band tiles), combined once through shared
+//     memory in fixed order.  Per candidate, rows summed in row order.
 // TMEM: 256 columns (2 accumulators); smem 3 x 32 KiB + 1 KiB alignment.
 // ============================================================================
 constexpr int kTcRows = 128;   // rows per CTA (M) = keys per tile (N)
@@ -328,12 +329,15 @@ DSK_DEVICE void tc_ld32(uint32_t addr, float (&f)[32]) {
   for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
 }
 
-__global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restrict__ tokens,
-                                                       const int32_t* __restrict__ delim_ids, int n_ids,
-                                                       const bf16* __restrict__ Qs,
-                                                       const bf16* __restrict__ Ks, int B, int S, int Hq,
-                                                       int Hkv, int W, int R, float alpha,
-                                                       float scale_log2, float* __restrict__ part) {
+constexpr int kTcEpiWarps = 8;  // two warps per TMEM lane quadrant: column halves
+constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const int32_t* __restrict__ tokens,
+                                                              const int32_t* __restrict__ delim_ids, int n_ids,
+                                                              const bf16* __restrict__ Qs,
+                                                              const bf16* __restrict__ Ks, int B, int S, int Hq,
+                                                              int Hkv, int W, int R, float alpha,
+                                                              float scale_log2, float* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 1024-byte aligned tiles (the swizzle atoms are address-based)
   const uint32_t raw_s = smem_u32(smem_raw);
@@ -341,6 +345,8 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
   unsigned char* sQ = smem;                       // [2 halves][128 rows][128 B]
   unsigned char* sK = smem + kTcTileBytes;        // [kTcStage][2 halves][128 rows][128 B]
   float* cbuf = reinterpret_cast<float*>(sK);     // [128][kMaxW], after the last MMA
+  constexpr int kX = 2 + 2 * kMaxW + 1;
+  __shared__ float xch[kTcRows * kX];             // half-row exchange (live while K stages are)
   __shared__ __align__(8) uint64_t kfull[kTcStage], kempty[kTcStage], sfull[2], sempty[2];
   __shared__ uint32_t s_tmem;
   __shared__ int s_ids[64];
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
     }
     for (int bb = 0; bb < 2; ++bb) {
       mbar_init(&sfull[bb], 1);
-      mbar_init(&sempty[bb], 4);
+      mbar_init(&sempty[bb], kTcEpiWarps);
     }
     fence_mbar_init();
   }
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
   const bf16* Qbase = Qs + (size_t)lb * S * ldq + (size_t)h * kD;
   const bf16* Kbase = Ks + (size_t)lb * S * ldk + (size_t)hk * kD;
 
-  if (warp == 4) {  // ------------------------------------------------ loader
+  if (warp == kTcEpiWarps) {  // ----------------------------------- loader
     // 16-byte chunk c (of 16) of row r -> half c / 8, swizzled slot (c % 8) ^ (r % 8)
     auto load_rows = [&](unsigned char* dst, const bf16* src, size_t ld, int row0) {
       for (int e = lane; e < kTcRows * 16; e += 32) {
@@ -408,7 +414,7 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
     cp_async_wait<0>();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive(&kfull[(n_all - 1) % kTcStage]);
-  } else if (warp == 5) {  // ---------------------------------------- MMA issue
+  } else if (warp == kTcEpiWarps + 1) {  // ------------------------ MMA issue
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcRows >> 3) << 17) |
                            ((uint32_t)(kTcRows >> 4) << 24);
     for (int i = 0; i < n_all; ++i) {
@@ -433,7 +439,9 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
       __syncwarp();
     }
   } else {  // ---------------------------------------------------- epilogue
-    const int lr = warp * 32 + lane, row = r0 + lr;
+    // warp w: TMEM lane quadrant q = w % 4 (rows 32 q + lane), column half hw = w / 4
+    const int q = warp & 3, hw = warp >> 2;
+    const int lr = q * 32 + lane, row = r0 + lr;
     float m = -CUDART_INF_F, l = 0.f, lse2 = 0.f;
     float ov_all = 0.f, ov[kMaxW], fu[kMaxW];
 #pragma unroll
@@ -442,32 +450,53 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
       const int bb = i & 1, kt = tile_of(i);
       mbar_wait(&sfull[bb], (i >> 1) & 1);
       tc_fence_after();
-      const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(bb * kTcRows);
-      if (i == n1) lse2 = m + __log2f(l);  // pass 1 complete
-      for (int c0 = 0; c0 < kTcRows; c0 += 32) {
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(bb * kTcRows + hw * 64);
+      if (i == n1) {  // pass 1 complete: combine the two column halves of the row
+        float* xr = xch + lr * kX;
+        if (hw) {
+          xr[0] = m;
+          xr[1] = l;
+        }
+        named_bar_sync(1, kTcEpiWarps * 32);
+        const float m2 = hw ? m : xr[0], l2 = hw ? l : xr[1];
+        const float mm = hw ? m : fmaxf(m, m2);
+        float ll = l;
+        if (!hw) {
+          ll = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mm)) + (m2 == -CUDART_INF_F ? 0.f : l2 * ex2(m2 - mm));
+          xr[0] = mm + __log2f(ll);
+        }
+        named_bar_sync(1, kTcEpiWarps * 32);
+        lse2 = xr[0];
+      }
+      for (int c0 = 0; c0 < 64; c0 += 32) {
         float z[32];
         __syncwarp();  // .aligned TMEM loads need the converged warp
         tc_ld32(base + (uint32_t)c0, z);
-        if (c0 + 32 >= kTcRows) {  // the accumulator may be overwritten now
+        if (c0 == 32) {  // the accumulator may be overwritten now
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sempty[bb]);
         }
-        const int key0 = kt * kTcRows + c0;
+        const int key0 = kt * kTcRows + hw * 64 + c0;
         if (i < n1) {
-          float tmax = -CUDART_INF_F;
+          if (kt == T) {  // diagonal tile: causal mask
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float v = z[j] * scale_log2;
-            if (key0 + j > row) v = -CUDART_INF_F;  // causal (only the diagonal tile has such keys)
-            z[j] = v;
-            tmax = fmaxf(tmax, v);
+            for (int j = 0; j < 32; ++j) z[j] = key0 + j > row ? -CUDART_INF_F : z[j] * scale_log2;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z[j] *= scale_log2;
           }
-          const float mn = fmaxf(m, tmax);
-          float ls = 0.f;
+          float t8[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) ls += ex2(z[j] - mn);
-          l = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mn)) + ls;
+          for (int j = 0; j < 8; ++j) t8[j] = fmaxf(fmaxf(z[j], z[j + 8]), fmaxf(z[j + 16], z[j + 24]));
+          const float tmax = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
+                                   fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
+          const float mn = fmaxf(m, tmax);
+          if (mn == -CUDART_INF_F) continue;  // nothing valid yet in this row
+          float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int j = 0; j < 32; ++j) ls[j & 3] += ex2(z[j] - mn);
+          l = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mn)) + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
           m = mn;
         } else {
           // band: dk = row - key in [0, band]
@@ -492,8 +521,27 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
         }
       }
     }
-    // every MMA has completed (the last sfull was waited): the K stages are free
-    named_bar_sync(1, 128);
+    // every MMA has completed (the last sfull was waited): the K stages are free.
+    // Combine the two column halves of each row (half 0 + half 1, fixed order).
+    named_bar_sync(1, kTcEpiWarps * 32);
+    float* xr = xch + lr * kX;
+    if (hw) {
+      xr[2] = ov_all;
+#pragma unroll
+      for (int w = 0; w < kMaxW; ++w) {
+        xr[3 + w] = ov[w];
+        xr[3 + kMaxW + w] = fu[w];
+      }
+    }
+    named_bar_sync(1, kTcEpiWarps * 32);
+    if (!hw) {
+      ov_all += xr[2];
+#pragma unroll
+      for (int w = 0; w < kMaxW; ++w) {
+        ov[w] += xr[3 + w];
+        fu[w] += xr[3 + kMaxW + w];
+      }
+    }
     const int32_t* tk = tokens + (size_t)b * S;
     auto is_cand = [&](int i) -> bool {
       if (i < 0 || i > S - 2) return false;
@@ -502,25 +550,27 @@ __global__ void __launch_bounds__(192, 1) k_lse_band_tc(const int32_t* __restric
         if (s_ids[j] == t) return true;
       return false;
     };
+    if (!hw) {
 #pragma unroll
-    for (int w = 1; w <= kMaxW; ++w) {
-      float c = 0.f;
-      const int i = row - w;
-      if (w <= W && row < S && is_cand(i)) {
-        const float o_ = ov_all + ov[w - 1];
-        const float dr = (i >= R) ? (1.f - o_ - fu[w - 1]) : 0.f;
-        c = o_ - alpha * dr;
+      for (int w = 1; w <= kMaxW; ++w) {
+        float c = 0.f;
+        const int i = row - w;
+        if (w <= W && row < S && is_cand(i)) {
+          const float o_ = ov_all + ov[w - 1];
+          const float dr = (i >= R) ? (1.f - o_ - fu[w - 1]) : 0.f;
+          c = o_ - alpha * dr;
+        }
+        cbuf[lr * kMaxW + (w - 1)] = c;
       }
-      cbuf[lr * kMaxW + (w - 1)] = c;
     }
-    named_bar_sync(1, 128);
-    for (int ti = threadIdx.x; ti < kTcRows + W - 1; ti += 128) {
+    named_bar_sync(1, kTcEpiWarps * 32);
+    for (int ti = threadIdx.x; ti < kTcRows + W - 1; ti += kTcEpiWarps * 32) {
       const int i = r0 - W + ti;
       if (!is_cand(i)) continue;
       const int q0 = max(i + 1, r0), q1 = min(min(i + W, S - 1), r0 + kTcRows - 1);
       if (q0 > q1) continue;
       float sacc = 0.f;
-      for (int q = q0; q <= q1; ++q) sacc += cbuf[(q - r0) * kMaxW + (q - i - 1)];
+      for (int qq = q0; qq <= q1; ++qq) sacc += cbuf[(qq - r0) * kMaxW + (qq - i - 1)];
       const int slot = (i + 1 >= r0) ? 0 : 1;
       part[(((size_t)lb * Hq + h) * S + i) * 2 + slot] = sacc;
     }
@@ -572,14 +622,14 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
   float* part = static_cast<float*>(ws);
   int rows_per_tile;
   if (!mmasync) {
-    const size_t smem = (size_t)(1 + kTcStage) * kTcTileBytes + 1024;
+    const size_t smem = (size_t)(1 + kTcStage) * kTcTileBytes + 1024;  // cbuf + exchange fit in sK
     static bool attr_tc = false;
     if (!attr_tc) {
       allow_max_dyn_smem(k_lse_band_tc);
       attr_tc = true;
     }
     dim3 grid((S + kTcRows - 1) / kTcRows, Hq, Ls * B);
-    k_lse_band_tc<<<grid, 192, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
+    k_lse_band_tc<<<grid, kTcThreads, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
                                            static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,
                                            scale_log2, part);
     rows_per_tile = kTcRows;
