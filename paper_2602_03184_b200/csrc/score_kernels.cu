@@ -21,6 +21,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <math_constants.h>
 #include <stdlib.h>
 
@@ -283,9 +286,9 @@ __global__ void __launch_bounds__(128) k_lse_band(const int32_t* __restrict__ to
 // ============================================================================
 // tcgen05 version of k_lse_band (the default): one CTA per (128-row tile,
 // head, layer*batch), 10 warps.
-//   warp 8 (loader): the Q tile once and the K tiles of both passes with
-//     16-byte cp.async into 128-byte-swizzled K-major smem tiles (two 64-dim
-//     halves), 2 stages; after its copies land: fence.proxy.async + mbarrier.
+//   warp 8 lane 0 (loader): the Q tile once and the K tiles of both passes
+//     with TMA tensor copies (cp.async.bulk.tensor, 128-byte swizzle) into
+//     K-major smem tiles (two 64-dim halves), 2 stages, mbarrier complete_tx.
 //   warp 9 lane 0 (MMA): S = Q K^T for a 128-key tile as 8 x
 //     tcgen05.mma.cta_group::1.kind::f16 (M = 128 rows, N = 128 keys, K = 16
 //     dims each, bf16 in, fp32 accumulate) into one of two 128-column TMEM
@@ -332,10 +335,20 @@ DSK_DEVICE void tc_ld32(uint32_t addr, float (&f)[32]) {
 constexpr int kTcEpiWarps = 8;  // two warps per TMEM lane quadrant: column halves
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const int32_t* __restrict__ tokens,
+// TMA: one 2-D box of 64 dims x 128 rows (128-byte swizzle, rows past S zero-filled)
+DSK_DEVICE void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_constant__ CUtensorMap tmQ,
+                                                              const __grid_constant__ CUtensorMap tmK,
+                                                              const int32_t* __restrict__ tokens,
                                                               const int32_t* __restrict__ delim_ids, int n_ids,
-                                                              const bf16* __restrict__ Qs,
-                                                              const bf16* __restrict__ Ks, int B, int S, int Hq,
+                                                              int B, int S, int Hq,
                                                               int Hkv, int W, int R, float alpha,
                                                               float scale_log2, float* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -365,7 +378,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const int32_t* __
   if (threadIdx.x < n_ids) s_ids[threadIdx.x] = delim_ids[threadIdx.x];
   if (threadIdx.x == 0) {
     for (int st = 0; st < kTcStage; ++st) {
-      mbar_init(&kfull[st], 32);
+      mbar_init(&kfull[st], 1);
       mbar_init(&kempty[st], 1);
     }
     for (int bb = 0; bb < 2; ++bb) {
@@ -384,36 +397,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const int32_t* __
   tc_fence_after();
   const uint32_t tmem = s_tmem;
 
-  const size_t ldq = (size_t)Hq * kD, ldk = (size_t)Hkv * kD;
-  const bf16* Qbase = Qs + (size_t)lb * S * ldq + (size_t)h * kD;
-  const bf16* Kbase = Ks + (size_t)lb * S * ldk + (size_t)hk * kD;
-
   if (warp == kTcEpiWarps) {  // ----------------------------------- loader
-    // 16-byte chunk c (of 16) of row r -> half c / 8, swizzled slot (c % 8) ^ (r % 8)
-    auto load_rows = [&](unsigned char* dst, const bf16* src, size_t ld, int row0) {
-      for (int e = lane; e < kTcRows * 16; e += 32) {
-        const int r = e >> 4, c = e & 15;
-        const bool ok = row0 + r < S;
-        const int half = c >> 3, slot = (c & 7) ^ (r & 7);
-        cp_async16(dst + half * (kTcRows * 128) + r * 128 + slot * 16,
-                   src + (size_t)(ok ? row0 + r : 0) * ld + c * 8, ok);
-      }
-    };
-    load_rows(sQ, Qbase, ldq, r0);  // lands with tile 0's group
-    for (int i = 0; i < n_all; ++i) {
-      const int st = i % kTcStage;
-      if (i >= kTcStage) mbar_wait(&kempty[st], ((i / kTcStage) - 1) & 1);
-      load_rows(sK + st * kTcTileBytes, Kbase, ldk, tile_of(i) * kTcRows);
-      cp_async_commit();
-      if (i >= 1) {
-        cp_async_wait<1>();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&kfull[(i - 1) % kTcStage]);
+    // TMA tensor copies (maps [lb][s][head][d]): per tile two boxes of 64 dims
+    // x 128 rows, hardware 128-byte swizzle = the UMMA K-major SW128 layout
+    if (lane == 0) {
+      for (int i = 0; i < n_all; ++i) {
+        const int st = i % kTcStage;
+        if (i >= kTcStage) mbar_wait(&kempty[st], ((i / kTcStage) - 1) & 1);
+        unsigned char* dst = sK + st * kTcTileBytes;
+        mbar_arrive_expect_tx(&kfull[st], (uint32_t)(kTcTileBytes + (i == 0 ? kTcTileBytes : 0)));
+        if (i == 0) {  // the Q tile rides on tile 0's barrier
+          tma_load_4d(sQ, &tmQ, 0, h, r0, lb, &kfull[0]);
+          tma_load_4d(sQ + kTcRows * 128, &tmQ, 64, h, r0, lb, &kfull[0]);
+        }
+        const int kr = tile_of(i) * kTcRows;
+        tma_load_4d(dst, &tmK, 0, hk, kr, lb, &kfull[st]);
+        tma_load_4d(dst + kTcRows * 128, &tmK, 64, hk, kr, lb, &kfull[st]);
       }
     }
-    cp_async_wait<0>();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive(&kfull[(n_all - 1) % kTcStage]);
+    __syncwarp();
   } else if (warp == kTcEpiWarps + 1) {  // ------------------------ MMA issue
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcRows >> 3) << 17) |
                            ((uint32_t)(kTcRows >> 4) << 24);
@@ -621,17 +623,37 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
   float* part = static_cast<float*>(ws);
   int rows_per_tile;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!mmasync && !encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
   if (!mmasync) {
-    const size_t smem = (size_t)(1 + kTcStage) * kTcTileBytes + 1024;  // cbuf + exchange fit in sK
+    // [Ls*B][S][H][d] bf16 -> dims (d, H, S, Ls*B); box (64, 1, 128, 1), 128-byte swizzle
+    auto make_map = [&](CUtensorMap* m, const void* base, int H) -> bool {
+      const cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)H, (cuuint64_t)S, (cuuint64_t)Ls * B};
+      const cuuint64_t strides[3] = {(cuuint64_t)kD * 2, (cuuint64_t)H * kD * 2, (cuuint64_t)S * H * kD * 2};
+      const cuuint32_t box[4] = {64, 1, (cuuint32_t)kTcRows, 1};
+      const cuuint32_t es[4] = {1, 1, 1, 1};
+      return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    CUtensorMap tmQ, tmK;
+    if (!make_map(&tmQ, Qs, Hq) || !make_map(&tmK, Ks, Hkv)) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)(1 + kTcStage) * kTcTileBytes + 1024;  // cbuf fits in sK
     static bool attr_tc = false;
     if (!attr_tc) {
       allow_max_dyn_smem(k_lse_band_tc);
       attr_tc = true;
     }
     dim3 grid((S + kTcRows - 1) / kTcRows, Hq, Ls * B);
-    k_lse_band_tc<<<grid, kTcThreads, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
-                                           static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,
-                                           scale_log2, part);
+    k_lse_band_tc<<<grid, kTcThreads, smem, st>>>(tmQ, tmK, tokens, delim_ids, n_ids, B, S, Hq, Hkv, W, R,
+                                                  alpha, scale_log2, part);
     rows_per_tile = kTcRows;
   } else {
     const size_t smem = (size_t)(kRowsPerCta + 2 * kKeyTile) * kLds * sizeof(bf16) +
