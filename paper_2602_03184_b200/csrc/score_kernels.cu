@@ -614,12 +614,15 @@ size_t score_ws_bytes(int Ls, int B, int S, int Hq) {
   return (size_t)Ls * B * Hq * S * 2 * sizeof(float);
 }
 
+static bool g_a1_mmasync = getenv("DYNSPLIT_A1_MMASYNC") != nullptr;
+
 cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
                                     const void* Qs, const void* Ks, int Ls, int B, int S, int Hq,
                                     int Hkv, int W, int R, float alpha, float* out, void* ws,
                                     cudaStream_t st) {
-  // tcgen05 kernel by default; DYNSPLIT_A1_MMASYNC=1 selects the mma.sync kernel (A/B)
-  static const bool mmasync = getenv("DYNSPLIT_A1_MMASYNC") != nullptr;
+  // tcgen05 kernel by default; DYNSPLIT_A1_MMASYNC=1 (or the test hook) selects the
+  // mma.sync kernel (A/B, parity of both)
+  const bool mmasync = g_a1_mmasync;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
   float* part = static_cast<float*>(ws);
   int rows_per_tile;
@@ -677,3 +680,7 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
 }
 
 }  // namespace dsk
+extern "C" int dynsplit_debug_a1_mmasync(int on) {
+  dsk::g_a1_mmasync = on != 0;
+  return 0;
+}

@@ -305,13 +305,24 @@ def _score_case(seed, Ls, B, S, Hq, Hkv):
     return toks, Qs, Ks
 
 
+@pytest.mark.parametrize("kernel", ["tcgen05", "mma.sync"])
 @pytest.mark.parametrize("Ls,B,S,Hq,Hkv,R", [(1, 1, 700, 4, 4, 128), (2, 2, 1500, 8, 2, 128),
-                                             (1, 1, 333, 2, 1, 16), (1, 2, 1100, 4, 2, 300)])
-def test_score_delimiters_parity(D, Ls, B, S, Hq, Hkv, R):
+                                             (1, 1, 333, 2, 1, 16), (1, 2, 1100, 4, 2, 300),
+                                             (1, 1, 129, 8, 8, 128)])
+def test_score_delimiters_parity(D, Ls, B, S, Hq, Hkv, R, kernel):
+    """a1 through both kernels: k_lse_band_tc (tcgen05, the default) and the
+    mma.sync k_lse_band (test hook), each within 2e-4 of the oracle."""
+    import ctypes
     cfg = D.default_config(R=R)
     toks, Qs, Ks = _score_case(1200, Ls, B, S, Hq, Hkv)
-    s = D.score_delimiters(t(toks), t(G.T7_IDS), t(Qs, torch.bfloat16), t(Ks, torch.bfloat16), cfg)
-    s = s.cpu().numpy()
+    lib = D.lib()
+    lib.dynsplit_debug_a1_mmasync.argtypes = [ctypes.c_int]
+    try:
+        lib.dynsplit_debug_a1_mmasync(1 if kernel == "mma.sync" else 0)
+        s = D.score_delimiters(t(toks), t(G.T7_IDS), t(Qs, torch.bfloat16), t(Ks, torch.bfloat16), cfg)
+        s = s.cpu().numpy()
+    finally:
+        lib.dynsplit_debug_a1_mmasync(0)
     worst = 0.0
     for b in range(B):
         ref = O.score_delimiters(toks[b], G.T7_IDS, Qs[:, b], Ks[:, b], cfg.W, R, cfg.alpha_pen)
