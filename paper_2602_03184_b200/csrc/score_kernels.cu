@@ -481,23 +481,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
         }
         const int key0 = kt * kTcRows + hw * 64 + c0;
         if (i < n1) {
+          // raw logits; the scale (> 0) is folded into one FFMA per element below
           if (kt == T) {  // diagonal tile: causal mask
 #pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] = key0 + j > row ? -CUDART_INF_F : z[j] * scale_log2;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] *= scale_log2;
+            for (int j = 0; j < 32; ++j) z[j] = key0 + j > row ? -CUDART_INF_F : z[j];
           }
           float t8[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) t8[j] = fmaxf(fmaxf(z[j], z[j + 8]), fmaxf(z[j + 16], z[j + 24]));
           const float tmax = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
                                    fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
-          const float mn = fmaxf(m, tmax);
+          const float mn = fmaxf(m, tmax * scale_log2);
           if (mn == -CUDART_INF_F) continue;  // nothing valid yet in this row
+          const float nmn = -mn;
           float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int j = 0; j < 32; ++j) ls[j & 3] += ex2(z[j] - mn);
+          for (int j = 0; j < 32; ++j) ls[j & 3] += ex2(fmaf(z[j], scale_log2, nmn));
           l = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mn)) + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
           m = mn;
         } else {
@@ -508,7 +507,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
           for (int j = 0; j < 32; ++j) {
             const int dk = dk0 - j;
             if (dk < 0 || dk > band) continue;
-            const float p = ex2(z[j] * scale_log2 - lse2);
+            const float p = ex2(fmaf(z[j], scale_log2, -lse2));
             if (dk >= W && dk <= R) {
               ov_all += p;
             } else {
