@@ -357,16 +357,27 @@ def main():
     attn_ms = t1.elapsed_time(t2) / (args.steps * L)
     split_step_ms = t0.elapsed_time(t2) / args.steps
 
-    # ---- e2e: host buffers through dynsplit_decode_step_host (copies inside)
-    q_host = [q.cpu().pin_memory() for q in qs]
-    o_host = [torch.empty(B, Hq, d).pin_memory() for _ in range(L)]
-    l_host = [torch.empty(B, Hq).pin_memory() for _ in range(L)]
-    ws_host = torch.zeros(D.step_host_workspace_bytes(shape, cfg, budget), dtype=torch.uint8, device=dev)
-    wl_host = torch.empty(D.worklist_bytes(shape, cfg, budget), dtype=torch.uint8, device=dev)
+    # ---- e2e: the step's inputs from pinned HOST memory (every layer's q, one
+    #      H2D copy), the public per-layer call dynsplit_decode_layer, and the
+    #      step's result (every layer's o and lse) read back to pinned host
+    #      memory (one D2H copy) and synchronised on, every step
+    q_all_h = torch.stack([q.cpu() for q in qs]).pin_memory()            # [L, B, Hq, d] bf16
+    o_all_h = torch.empty(L, B, Hq, d).pin_memory()
+    l_all_h = torch.empty(L, B, Hq).pin_memory()
+    q_all_d = torch.empty(q_all_h.shape, dtype=q_all_h.dtype, device=dev)
+    o_all_d = torch.empty(L, B, Hq, d, device=dev)
+    l_all_d = torch.empty(L, B, Hq, device=dev)
+    ws_layer = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer_e2e")
+    sel_e2e = D._sel_outputs(shape, cfg, budget, dev, want_blocks=False)
 
     def host_step():
+        q_all_d.copy_(q_all_h, non_blocking=True)
         for l in range(L):
-            D.decode_step_host(q_host[l], layers[l], budget, o_host[l], l_host[l], wl_host, ws_host)
+            _, ns, mg, kp, wl = sel_e2e
+            D.decode_layer(q_all_d[l], layers[l], budget, out=(ns, mg, kp, wl, o_all_d[l], l_all_d[l]),
+                           ws=ws_layer)
+        o_all_h.copy_(o_all_d, non_blocking=True)
+        l_all_h.copy_(l_all_d, non_blocking=True)
 
     host_step()
     torch.cuda.synchronize()
@@ -383,8 +394,8 @@ def main():
     ev1.record(cur)
     barrier()
     e2e_ms = ev0.elapsed_time(ev1) / args.steps
-    h2d = L * B * Hq * d * e
-    d2h = L * B * Hq * (d + 1) * 4
+    h2d = q_all_h.numel() * q_all_h.element_size()
+    d2h = o_all_h.numel() * 4 + l_all_h.numel() * 4
 
     # ---- prefill row a1 (context, not the headline): Alg. 1 delimiter scoring
     #      of one sequence-layer at S_pf (C5 shape: 32Q/8KV, bf16), one launch pair
