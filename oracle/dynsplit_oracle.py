@@ -215,7 +215,7 @@ def weight_table(tokens, s, delim_ids):
 # ---------------------------------------------------------------------------
 # O3  DD-Select dynamic segmentation, Delta = 14.
 # ---------------------------------------------------------------------------
-def _dd_select_loop(tokens, delim_ids, w10, C, delta, key_fn):
+def _dd_select_loop(tokens, delim_ids, w10, C, delta, key_fn, s_begin=0):
     S = len(tokens)
     if S < 1:
         raise ValueError("EmptySequence")
@@ -223,7 +223,7 @@ def _dd_select_loop(tokens, delim_ids, w10, C, delta, key_fn):
         raise ValueError("need 0 <= delta < C")     # S:192, Q11
     wmap = {int(t): int(w) for t, w in zip(delim_ids, w10)}
     starts = []
-    s_c = 0                                          # step 1: current pos
+    s_c = s_begin                                    # step 1: current pos
     while s_c < S:
         starts.append(s_c)
         s_e = s_c + C                                # step 1: initial end
@@ -259,6 +259,38 @@ def segment(tokens, delim_ids, w10, C=32, delta=14, lam_num=1, lam_den=2):
         return lam * Fraction(w, 10) + (1 - lam) * p
 
     return _dd_select_loop(tokens, delim_ids, w10, C, delta, key)
+
+
+def segment_incremental(prev_starts, tokens, delim_ids, w10, C=32, delta=14, lam_num=1, lam_den=2):
+    """Incremental update during decoding ("only the most recent
+    segmentation ranges are recomputed"; SPEC S:206-209 with the strict
+    frozen rule of reading Q23).
+
+    prev_starts: the plan of the prefix of length L' = prev_starts[-1];
+    tokens: the extended sequence (length L >= L').  Every block whose start
+    s_c satisfies s_c + C + delta < L' is kept verbatim (its window and its
+    end test only see tokens < L'); segmentation resumes from the first other
+    block start.  Returns (block_starts of the extended sequence, index of the
+    first recomputed block).
+    """
+    prev = [int(x) for x in prev_starts]
+    Lp, L = prev[-1], len(tokens)
+    if L < Lp:
+        raise ValueError("PlanMismatch: the sequence is shorter than the plan")  # S:210
+    if L == Lp:
+        return prev, len(prev) - 1
+    nprev = len(prev) - 1
+    f = 0
+    while f < nprev and prev[f] + C + delta < Lp:    # frozen prefix (strict <, Q23)
+        f += 1
+    lam = Fraction(lam_num, lam_den)
+
+    def key(w, dist):
+        p = 1 - Fraction(dist, delta + 1)
+        return lam * Fraction(w, 10) + (1 - lam) * p
+
+    s0 = prev[f] if f < nprev else Lp
+    return prev[:f] + _dd_select_loop(tokens, delim_ids, w10, C, delta, key, s_begin=s0), f
 
 
 def segment_float_key(tokens, delim_ids, w10, C=32, delta=14, lam=0.5):

@@ -186,3 +186,53 @@ def test_page_map_bijection(seed):
     for pg, sl in slots:
         used[pg, sl] = True
     assert np.all(Xp[:, ~used, :] == 0)           # padding slots are zero
+
+
+# ---------------------------------------------------------------- NEXT-1: incremental update
+def test_incremental_extend_by_zero_is_identity():
+    # S:212
+    toks = G.tokens(41, 300)
+    prev = O.segment(toks, G.T7_IDS, G.T7_W10, 64, 14)
+    new, f = O.segment_incremental(prev, toks, G.T7_IDS, G.T7_W10, 64, 14)
+    assert new == prev and f == len(prev) - 1
+
+
+def test_incremental_frozen_prefix_numbers():
+    # S:213 with the strict frozen rule (Q23): L' = 300, C = 64, Delta = 14 ->
+    # every block starting at s_c < 222 is kept verbatim
+    toks = G.tokens(42, 301)
+    prev = O.segment(toks[:300], G.T7_IDS, G.T7_W10, 64, 14)
+    new, f = O.segment_incremental(prev, toks, G.T7_IDS, G.T7_W10, 64, 14)
+    kept = [s for s in prev[:-1] if s + 64 + 14 < 300]
+    assert new[:len(kept)] == kept and f == len(kept)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_incremental_equals_from_scratch(seed):
+    # random prefixes L' in [100, 500] extended by 1..64 tokens (plus
+    # chained one-token steps): identical to segmenting the whole sequence
+    r = G.rng(7, seed)
+    for trial in range(40):
+        C = int(r.choice([16, 32, 64]))
+        delta = int(r.integers(0, C))
+        Lp = int(r.integers(100, 501))
+        L = Lp + int(r.integers(1, 65))
+        toks = G.tokens(1000 * seed + trial, L)
+        w10 = r.integers(0, 11, size=len(G.T7_IDS)).astype(np.uint8)
+        prev = O.segment(toks[:Lp], G.T7_IDS, w10, C, delta)
+        new, f = O.segment_incremental(prev, toks, G.T7_IDS, w10, C, delta)
+        assert new == O.segment(toks, G.T7_IDS, w10, C, delta), (seed, trial, C, delta, Lp, L)
+        assert new[:f] == prev[:f]
+    # token-by-token decoding
+    toks = G.tokens(77 + seed, 400)
+    plan = O.segment(toks[:200], G.T7_IDS, G.T7_W10, 32, 14)
+    for L in range(201, 401):
+        plan, _ = O.segment_incremental(plan, toks[:L], G.T7_IDS, G.T7_W10, 32, 14)
+    assert plan == O.segment(toks, G.T7_IDS, G.T7_W10, 32, 14)
+
+
+def test_incremental_rejects_shorter_sequence():
+    toks = G.tokens(43, 200)
+    prev = O.segment(toks, G.T7_IDS, G.T7_W10, 32, 14)
+    with pytest.raises(ValueError):
+        O.segment_incremental(prev, toks[:150], G.T7_IDS, G.T7_W10, 32, 14)
