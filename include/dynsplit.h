@@ -57,7 +57,8 @@ typedef enum {
   DYNSPLIT_OP_BUILD_BLOCKS = 2,
   DYNSPLIT_OP_SELECT = 3,
   DYNSPLIT_OP_DECODE_ATTN = 4,
-  DYNSPLIT_OP_DECODE_LAYER = 5
+  DYNSPLIT_OP_DECODE_LAYER = 5,
+  DYNSPLIT_OP_APPEND = 6
 } dynsplit_op;
 
 typedef struct {
@@ -263,6 +264,44 @@ dynsplit_status dynsplit_decode_layer(const dynsplit_shape* shape, const dynspli
                                       float scale, int32_t* n_sel, int32_t* marginal_block,
                                       int32_t* marginal_keep, void* worklist, float* o, float* lse,
                                       void* ws, size_t ws_bytes, void* stream);
+
+/* NEXT-1: decode-time append with incremental DD-Select ("Incremental Update
+ * during Decoding ... only the most recent segmentation ranges are
+ * recomputed"; frozen rule strict, reading Q23).
+ * shape.S is the CAPACITY every per-sequence buffer was allocated for; the
+ * first L_prev tokens of each sequence are already planned and paged, L is
+ * the new length (the same for every sequence of the batch;
+ * 0 <= L_prev <= L <= S, L >= 1; L_prev = 0 plans and pages a whole prefix).
+ *
+ * dynsplit_append_plan (once per step, the plan is shared by the layers):
+ * blocks whose start s_c has s_c + C + Delta < L_prev are kept verbatim, DD
+ * Select resumes at the first other block start over the tokens up to L
+ * (exact integer keys as in dynsplit_segment), block_starts / n_blocks are
+ * rewritten from there (padding entries = L) and the page tables rebuilt as
+ * in dynsplit_map_pages.  The page locations of the re-planned old tokens
+ * (at most C + Delta per sequence) are left in `ws` for dynsplit_append_kv.
+ *   tokens int32 [B, S] (the first L valid); w10 uint8 [B, n_ids] (device);
+ *   plan arrays as in dynsplit_build_blocks (in/out).
+ * Workspace: DYNSPLIT_OP_APPEND.  Errors: ERR_DIMENSION_MISMATCH for
+ * L_prev > L or L > S; ERR_UNSUPPORTED if C + Delta exceeds the staging
+ * bound (256 bf16, 200 fp32).
+ *
+ * dynsplit_append_kv (per layer, after dynsplit_append_plan): moves the
+ * re-planned old rows of K and V into their new page slots, writes the new
+ * rows K_new / V_new [B, L - L_prev, Hkv, d] (kv dtype), zeroes the padding
+ * rows of the rewritten pages and recomputes their blocks' min/max digests.
+ * Pages and digests of the kept blocks are not touched. */
+dynsplit_status dynsplit_append_plan(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                     int32_t L_prev, int32_t L, const int32_t* tokens,
+                                     const int32_t* delim_ids, int32_t n_ids, const uint8_t* w10,
+                                     int32_t* block_starts, int32_t* n_blocks, int32_t* page_first,
+                                     int32_t* page_block, int16_t* page_valid, int32_t* n_pages,
+                                     void* ws, size_t ws_bytes, void* stream);
+dynsplit_status dynsplit_append_kv(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                   int32_t L_prev, int32_t L, const void* K_new, const void* V_new,
+                                   const int32_t* block_starts, const int32_t* n_blocks,
+                                   const int32_t* page_first, const void* ws, void* Kp, void* Vp,
+                                   void* digests, void* stream);
 
 /* Row a8 standalone (cross-GPU merge of sequence-split shards):
  *   o_parts fp32 [n_parts, rows, d], lse_parts fp32 [n_parts, rows] ->

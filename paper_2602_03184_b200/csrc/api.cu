@@ -223,6 +223,7 @@ size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* s, const dynsp
     case DYNSPLIT_OP_SELECT: return select_ws(s, c);
     case DYNSPLIT_OP_DECODE_ATTN: return decode_ws(s);
     case DYNSPLIT_OP_DECODE_LAYER: return layer_ws(s, c);
+    case DYNSPLIT_OP_APPEND: return append_ws_bytes(s->B);
     default: return 0;
   }
 }
@@ -485,6 +486,53 @@ dynsplit_status dynsplit_decode_layer(const dynsplit_shape* s, const dynsplit_co
                       n_sel, marginal_block, marginal_keep, worklist, ws_sel, select_ws(s, c), stream));
   return dynsplit_decode_attn(s, c, q, Kp, Vp, nullptr, nullptr, worklist, scale, o, lse, ws_dec,
                               decode_ws(s), stream);
+}
+
+// ------------------------------------------------------------------ NEXT-1: append
+dynsplit_status dynsplit_append_plan(const dynsplit_shape* s, const dynsplit_config* c, int32_t L_prev,
+                                     int32_t L, const int32_t* tokens, const int32_t* delim_ids,
+                                     int32_t n_ids, const uint8_t* w10, int32_t* block_starts,
+                                     int32_t* n_blocks, int32_t* page_first, int32_t* page_block,
+                                     int16_t* page_valid, int32_t* n_pages, void* ws, size_t ws_bytes,
+                                     void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!tokens || !delim_ids || !w10 || !block_starts || !n_blocks || !page_first || !page_block ||
+      !page_valid || !n_pages || !ws)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_ids < 1 || n_ids > 64) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (L < 1) return DYNSPLIT_ERR_EMPTY_SEQUENCE;
+  if (L_prev < 0 || L_prev > L || L > s->S) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
+  if (ws_bytes < append_ws_bytes(s->B)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int maxb = dynsplit_max_blocks(s->S, c);
+  if (launch_plan_append(tokens, delim_ids, n_ids, w10, s->B, s->S, maxb, c->C, c->delta, c->lambda_num,
+                         c->lambda_den, c->page_size, L_prev, L, block_starts, n_blocks, page_first,
+                         static_cast<int32_t*>(ws), st) != cudaSuccess)
+    return DYNSPLIT_ERR_CUDA;
+  return dynsplit_map_pages(s, c, block_starts, n_blocks, page_first, page_block, page_valid, n_pages,
+                            stream);
+}
+
+dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_config* c, int32_t L_prev,
+                                   int32_t L, const void* K_new, const void* V_new,
+                                   const int32_t* block_starts, const int32_t* n_blocks,
+                                   const int32_t* page_first, const void* ws, void* Kp, void* Vp,
+                                   void* digests, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!block_starts || !n_blocks || !page_first || !ws || !Kp || !Vp || !digests)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (L < 1) return DYNSPLIT_ERR_EMPTY_SEQUENCE;
+  if (L_prev < 0 || L_prev > L || L > s->S) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  if (L > L_prev && (!K_new || !V_new)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
+  return cuda_status(launch_kv_append(s->kv_dtype, K_new, V_new, L - L_prev, s->B, s->Hkv,
+                                      dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
+                                      c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks,
+                                      page_first, static_cast<const int32_t*>(ws), Kp, Vp, digests,
+                                      static_cast<cudaStream_t>(stream)));
 }
 
 dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_parts,

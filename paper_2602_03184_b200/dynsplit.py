@@ -21,7 +21,8 @@ LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit_debug.so" if os.environ.get("D
 
 OK = 0
 BF16, FP32 = 0, 1
-OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN, OP_DECODE_LAYER = range(6)
+(OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN, OP_DECODE_LAYER,
+ OP_APPEND) = range(7)
 INT32_MAX = 0x7FFFFFFF
 
 
@@ -76,6 +77,8 @@ SIGNATURES = {
                                   _SZ, _P]),
     "dynsplit_decode_layer": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, ctypes.c_float, _P, _P,
                                    _P, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_append_plan": (_I, [_PS, _PC, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_append_kv": (_I, [_PS, _PC, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dynsplit_merge_partials": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
     "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
@@ -321,6 +324,57 @@ def build_blocks(tokens, delim_ids, K, V, cfg: Config, static_w10=None, Qs=None,
 # ---------------------------------------------------------------------------
 # decode
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+# NEXT-1: growing sequences (decode-time append, incremental DD-Select)
+# ---------------------------------------------------------------------------
+def alloc_paged(B: int, S_cap: int, Hq: int, Hkv: int, cfg: Config, w10, dtype=torch.bfloat16,
+                device="cuda", plan_from: Optional[PagedLayer] = None) -> PagedLayer:
+    """Empty paged layer with room for S_cap tokens per sequence (its shape.S
+    is the capacity).  w10: uint8 [B, n_ids] device weights.  plan_from: share
+    the plan tensors of another layer (the plan is per sequence, not per layer)."""
+    d = 128
+    shape = make_shape(B, S_cap, Hq, Hkv, d, 1, BF16 if dtype == torch.bfloat16 else FP32)
+    mb, mp, P = max_blocks(S_cap, cfg), max_pages(S_cap, cfg), cfg.page_size
+    dev = torch.device(device)
+    if plan_from is None:
+        bs = torch.zeros(B, mb + 1, dtype=torch.int32, device=dev)
+        nb = torch.zeros(B, dtype=torch.int32, device=dev)
+        pf = torch.zeros(B, mb + 1, dtype=torch.int32, device=dev)
+        pb = torch.full((B, mp), -1, dtype=torch.int32, device=dev)
+        pv = torch.zeros(B, mp, dtype=torch.int16, device=dev)
+        npg = torch.zeros(B, dtype=torch.int32, device=dev)
+    else:
+        p = plan_from
+        bs, nb, pf, pb, pv, npg = p.block_starts, p.n_blocks, p.page_first, p.page_block, p.page_valid, p.n_pages
+    Kp = torch.zeros(B, Hkv, mp, P, d, dtype=dtype, device=dev)
+    Vp = torch.zeros_like(Kp)
+    dig = torch.zeros(B, Hkv, mb, 2, d, dtype=dtype, device=dev)
+    return PagedLayer(shape, cfg, w10, bs, nb, pf, pb, pv, npg, Kp, Vp, dig)
+
+
+def append_workspace(layer: PagedLayer) -> torch.Tensor:
+    return torch.zeros(max(workspace_bytes(OP_APPEND, layer.shape, layer.cfg), 256), dtype=torch.uint8,
+                       device=layer.block_starts.device)
+
+
+def append_plan(tokens, delim_ids, layer: PagedLayer, L_prev: int, L: int, ws) -> None:
+    """dynsplit_append_plan: re-plan the tail for L_prev -> L tokens (in place)."""
+    _check(lib().dynsplit_append_plan(
+        ctypes.byref(layer.shape), ctypes.byref(layer.cfg), L_prev, L, _ptr(tokens), _ptr(delim_ids),
+        delim_ids.numel(), _ptr(layer.w10), _ptr(layer.block_starts), _ptr(layer.n_blocks),
+        _ptr(layer.page_first), _ptr(layer.page_block), _ptr(layer.page_valid), _ptr(layer.n_pages),
+        _ptr(ws), ws.numel(), _stream()), "append_plan")
+
+
+def append_kv(layer: PagedLayer, K_new, V_new, L_prev: int, L: int, ws) -> None:
+    """dynsplit_append_kv: move the re-planned rows and write K_new / V_new
+    [B, L - L_prev, Hkv, d] into the layer's pages and digests."""
+    _check(lib().dynsplit_append_kv(
+        ctypes.byref(layer.shape), ctypes.byref(layer.cfg), L_prev, L, _ptr(K_new), _ptr(V_new),
+        _ptr(layer.block_starts), _ptr(layer.n_blocks), _ptr(layer.page_first), _ptr(ws),
+        _ptr(layer.Kp), _ptr(layer.Vp), _ptr(layer.digests), _stream()), "append_kv")
+
+
 @dataclass
 class Selection:
     sel_blocks: torch.Tensor    # int32 [B, Hq, max_sel] (ascending; first n_sel valid)

@@ -81,3 +81,24 @@ def test_product_path_has_no_oracle_dependency():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not pat.search(src), f
+
+
+def test_append_argument_validation(D):
+    """NEXT-1 entry points reject bad lengths / configs before any launch."""
+    import ctypes as C
+    sh = D.make_shape(1, 1000, 8, 8, 128)
+    cfg = D.default_config()
+    lib = D.lib()
+    p = C.c_void_p(16)  # never dereferenced: validation fails first
+    bad = [(5, 3), (-1, 3), (0, 0), (10, 1001)]
+    for lp, l in bad:
+        st = lib.dynsplit_append_plan(C.byref(sh), C.byref(cfg), lp, l, p, p, 13, p, p, p, p, p, p, p, p,
+                                      1 << 20, None)
+        assert st != 0, (lp, l)
+        st = lib.dynsplit_append_kv(C.byref(sh), C.byref(cfg), lp, l, p, p, p, p, p, p, p, p, p, None)
+        assert st != 0, (lp, l)
+    wide = D.default_config(C=200, delta=100)
+    st = lib.dynsplit_append_plan(C.byref(sh), C.byref(wide), 0, 10, p, p, 13, p, p, p, p, p, p, p, p,
+                                  1 << 20, None)
+    assert st == 5  # DYNSPLIT_ERR_UNSUPPORTED (C + Delta above the staging bound)
+    assert D.workspace_bytes(D.OP_APPEND, sh, cfg) > 0
