@@ -278,7 +278,8 @@ dynsplit_status dynsplit_decode_layer(const dynsplit_shape* shape, const dynspli
  * Select resumes at the first other block start over the tokens up to L
  * (exact integer keys as in dynsplit_segment), block_starts / n_blocks are
  * rewritten from there (padding entries = L) and the page tables rebuilt as
- * in dynsplit_map_pages.  The page locations of the re-planned old tokens
+ * in dynsplit_map_pages (only from the first re-planned block on).  The page
+ * locations of the re-planned old tokens
  * (at most C + Delta per sequence) are left in `ws` for dynsplit_append_kv.
  *   tokens int32 [B, S] (the first L valid); w10 uint8 [B, n_ids] (device);
  *   plan arrays as in dynsplit_build_blocks (in/out).
@@ -302,6 +303,15 @@ dynsplit_status dynsplit_append_kv(const dynsplit_shape* shape, const dynsplit_c
                                    const int32_t* block_starts, const int32_t* n_blocks,
                                    const int32_t* page_first, const void* ws, void* Kp, void* Vp,
                                    void* digests, void* stream);
+/* The same for n_layers (<= 64) layers sharing the plan in one launch: HOST
+ * arrays of n_layers device pointers (K_new[l], V_new[l] [B, L - L_prev, Hkv,
+ * d]; Kp[l], Vp[l], digests[l] as in dynsplit_build_blocks). */
+dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                          int32_t L_prev, int32_t L, int32_t n_layers,
+                                          const void* const* K_new, const void* const* V_new,
+                                          const int32_t* block_starts, const int32_t* n_blocks,
+                                          const int32_t* page_first, const void* ws, void* const* Kp,
+                                          void* const* Vp, void* const* digests, void* stream);
 
 /* Row a8 standalone (cross-GPU merge of sequence-split shards):
  *   o_parts fp32 [n_parts, rows, d], lse_parts fp32 [n_parts, rows] ->

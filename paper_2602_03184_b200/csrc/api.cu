@@ -505,14 +505,36 @@ dynsplit_status dynsplit_append_plan(const dynsplit_shape* s, const dynsplit_con
   if (L_prev < 0 || L_prev > L || L > s->S) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
   if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
   if (ws_bytes < append_ws_bytes(s->B)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int maxb = dynsplit_max_blocks(s->S, c);
-  if (launch_plan_append(tokens, delim_ids, n_ids, w10, s->B, s->S, maxb, c->C, c->delta, c->lambda_num,
-                         c->lambda_den, c->page_size, L_prev, L, block_starts, n_blocks, page_first,
-                         static_cast<int32_t*>(ws), st) != cudaSuccess)
-    return DYNSPLIT_ERR_CUDA;
-  return dynsplit_map_pages(s, c, block_starts, n_blocks, page_first, page_block, page_valid, n_pages,
-                            stream);
+  return cuda_status(launch_plan_append(
+      tokens, delim_ids, n_ids, w10, s->B, s->S, dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
+      c->C, c->delta, c->lambda_num, c->lambda_den, c->page_size, L_prev, L, block_starts, n_blocks,
+      page_first, page_block, page_valid, n_pages, static_cast<int32_t*>(ws),
+      static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynsplit_config* c,
+                                          int32_t L_prev, int32_t L, int32_t n_layers,
+                                          const void* const* K_new, const void* const* V_new,
+                                          const int32_t* block_starts, const int32_t* n_blocks,
+                                          const int32_t* page_first, const void* ws, void* const* Kp,
+                                          void* const* Vp, void* const* digests, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!block_starts || !n_blocks || !page_first || !ws || !Kp || !Vp || !digests)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_layers < 1 || n_layers > kAppendMaxLayers) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (L < 1) return DYNSPLIT_ERR_EMPTY_SEQUENCE;
+  if (L_prev < 0 || L_prev > L || L > s->S) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  for (int l = 0; l < n_layers; ++l) {
+    if (!Kp[l] || !Vp[l] || !digests[l]) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+    if (L > L_prev && (!K_new || !V_new || !K_new[l] || !V_new[l])) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  }
+  if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
+  return cuda_status(launch_kv_append(s->kv_dtype, n_layers, K_new, V_new, L - L_prev, s->B, s->Hkv,
+                                      dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
+                                      c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks,
+                                      page_first, static_cast<const int32_t*>(ws), Kp, Vp, digests,
+                                      static_cast<cudaStream_t>(stream)));
 }
 
 dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_config* c, int32_t L_prev,
@@ -520,19 +542,13 @@ dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_confi
                                    const int32_t* block_starts, const int32_t* n_blocks,
                                    const int32_t* page_first, const void* ws, void* Kp, void* Vp,
                                    void* digests, void* stream) {
-  DSK_TRY(check_shape(s));
-  DSK_TRY(check_cfg(c));
-  if (!block_starts || !n_blocks || !page_first || !ws || !Kp || !Vp || !digests)
-    return DYNSPLIT_ERR_INVALID_ARGUMENT;
-  if (L < 1) return DYNSPLIT_ERR_EMPTY_SEQUENCE;
-  if (L_prev < 0 || L_prev > L || L > s->S) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
-  if (L > L_prev && (!K_new || !V_new)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
-  if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
-  return cuda_status(launch_kv_append(s->kv_dtype, K_new, V_new, L - L_prev, s->B, s->Hkv,
-                                      dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
-                                      c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks,
-                                      page_first, static_cast<const int32_t*>(ws), Kp, Vp, digests,
-                                      static_cast<cudaStream_t>(stream)));
+  const void* kn[1] = {K_new};
+  const void* vn[1] = {V_new};
+  void* kp[1] = {Kp};
+  void* vp[1] = {Vp};
+  void* dg[1] = {digests};
+  return dynsplit_append_kv_layers(s, c, L_prev, L, 1, kn, vn, block_starts, n_blocks, page_first, ws, kp,
+                                   vp, dg, stream);
 }
 
 dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_parts,

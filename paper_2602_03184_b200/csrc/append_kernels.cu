@@ -25,15 +25,27 @@
 namespace dsk {
 
 constexpr int kAppendMaxTail = 256;  // C + Delta bound for the staged old tail
+
+// per-layer pointers of one dynsplit_append_kv_layers call (kernel argument)
+struct AppendLayers {
+  const void* kn[kAppendMaxLayers];
+  const void* vn[kAppendMaxLayers];
+  void* kp[kAppendMaxLayers];
+  void* vp[kAppendMaxLayers];
+  void* dg[kAppendMaxLayers];
+};
 constexpr int kAppendWs = 4 + kAppendMaxTail;  // int32 per sequence: f, start_f, n_old, pad, loc[]
 
 __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ tokens,
                                                     const int32_t* __restrict__ delim_ids, int n_ids,
-                                                    const uint8_t* __restrict__ w10, int S, int maxb, int C,
-                                                    int delta, int lam_num, int lam_den, int P, int L_prev,
-                                                    int L, int32_t* __restrict__ block_starts,
+                                                    const uint8_t* __restrict__ w10, int S, int maxb, int maxp,
+                                                    int C, int delta, int lam_num, int lam_den, int P,
+                                                    int L_prev, int L, int32_t* __restrict__ block_starts,
                                                     int32_t* __restrict__ n_blocks,
-                                                    const int32_t* __restrict__ page_first,
+                                                    int32_t* __restrict__ page_first,
+                                                    int32_t* __restrict__ page_block,
+                                                    int16_t* __restrict__ page_valid,
+                                                    int32_t* __restrict__ n_pages,
                                                     int32_t* __restrict__ ws) {
   __shared__ int s_ids[64], s_w[64];
   const int b = blockIdx.x, lane = threadIdx.x;
@@ -43,7 +55,7 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
   }
   __syncwarp();
   int32_t* bs = block_starts + (size_t)b * (maxb + 1);
-  const int32_t* pf = page_first + (size_t)b * (maxb + 1);
+  int32_t* pf = page_first + (size_t)b * (maxb + 1);
   int32_t* w = ws + (size_t)b * kAppendWs;
   const int32_t* tk = tokens + (size_t)b * S;
 
@@ -116,22 +128,54 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
   }
   for (int j = nb + lane; j <= maxb; j += 32) bs[j] = L;
   if (lane == 0) n_blocks[b] = nb;
+  if (L_prev == 0) return;  // a whole prefix: the launcher rebuilds every page table
+
+  // ---- 3. page tables of blocks f .. nb-1 (pages before page_first[f] do not move)
+  __syncwarp();
+  int32_t* pb = page_block + (size_t)b * maxp;
+  int16_t* pv = page_valid + (size_t)b * maxp;
+  const int np_old = n_pages[b];
+  int carry = pf[f];
+  for (int j0 = f; j0 < nb; j0 += 32) {
+    const int j = j0 + lane;
+    const int len = j < nb ? bs[j + 1] - bs[j] : 0;
+    const int np = (len + P - 1) / P;
+    const int inc = warp_incl_scan(np);
+    const int first = carry + inc - np;
+    if (j < nb) {
+      pf[j] = first;
+      for (int jj = 0; jj < np; ++jj) {
+        pb[first + jj] = j;
+        pv[first + jj] = (int16_t)min(P, len - P * jj);
+      }
+    }
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  for (int j = nb + lane; j <= maxb; j += 32) pf[j] = carry;
+  for (int p2 = carry + lane; p2 < np_old; p2 += 32) {  // pages the tail no longer uses
+    pb[p2] = -1;
+    pv[p2] = 0;
+  }
+  if (lane == 0) n_pages[b] = carry;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_kv_append(const T* __restrict__ K_new, const T* __restrict__ V_new,
-                                                   int n_new, int Hkv, int maxb, int maxp, int P, int L_prev,
-                                                   int max_tail,
+__global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new, int Hkv, int maxb, int maxp,
+                                                   int P, int L_prev, int max_tail,
                                                    const int32_t* __restrict__ block_starts,
                                                    const int32_t* __restrict__ n_blocks,
                                                    const int32_t* __restrict__ page_first,
-                                                   const int32_t* __restrict__ ws, T* __restrict__ Kp,
-                                                   T* __restrict__ Vp, T* __restrict__ dig) {
+                                                   const int32_t* __restrict__ ws) {
   constexpr int LE = kD / 32;  // elements per lane
   extern __shared__ __align__(16) unsigned char smem[];
   T* sK = reinterpret_cast<T*>(smem);  // [max_tail][kD]
   T* sV = sK + (size_t)max_tail * kD;
-  const int hk = blockIdx.x, b = blockIdx.y;
+  const int hk = blockIdx.x, b = blockIdx.y, layer = blockIdx.z;
+  const T* K_new = static_cast<const T*>(lays.kn[layer]);
+  const T* V_new = static_cast<const T*>(lays.vn[layer]);
+  T* Kp = static_cast<T*>(lays.kp[layer]);
+  T* Vp = static_cast<T*>(lays.vp[layer]);
+  T* dig = static_cast<T*>(lays.dg[layer]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int32_t* w = ws + (size_t)b * kAppendWs;
   const int f = w[0], s0 = w[1], n_old = w[2];
@@ -166,29 +210,43 @@ __global__ void __launch_bounds__(256) k_kv_append(const T* __restrict__ K_new, 
       mn[e] = CUDART_INF_F;
     }
     const int np = (t1 - t0 + P - 1) / P;
-    for (int t = t0; t < t0 + np * P; ++t) {
-      T* kd = kpb + ((size_t)(pf[j] + (t - t0) / P) * P + (t - t0) % P) * kD + lane * LE;
-      T* vd = vpb + ((size_t)(pf[j] + (t - t0) / P) * P + (t - t0) % P) * kD + lane * LE;
-      T kv[LE], vv[LE];
-      if (t < t1) {
-        const T* ksrc = t < L_prev ? sK + (size_t)(t - s0) * kD : kn + (size_t)(t - L_prev) * new_row;
-        const T* vsrc = t < L_prev ? sV + (size_t)(t - s0) * kD : vn + (size_t)(t - L_prev) * new_row;
+    const T* kb = kpb;  // silence unused warnings in some instantiations
+    (void)kb;
+    // 4 rows per iteration, all loads first (independent), then the stores
+    for (int tb = t0; tb < t0 + np * P; tb += 4) {
+      T kv[4][LE], vv[4][LE];
 #pragma unroll
-        for (int e = 0; e < LE; ++e) {
-          kv[e] = ksrc[lane * LE + e];
-          vv[e] = vsrc[lane * LE + e];
-          const float x = (float)kv[e];
-          mx[e] = fmaxf(mx[e], x);
-          mn[e] = fminf(mn[e], x);
+      for (int u = 0; u < 4; ++u) {
+        const int t = tb + u;
+        if (t < t1) {
+          const T* ksrc = t < L_prev ? sK + (size_t)(t - s0) * kD : kn + (size_t)(t - L_prev) * new_row;
+          const T* vsrc = t < L_prev ? sV + (size_t)(t - s0) * kD : vn + (size_t)(t - L_prev) * new_row;
+#pragma unroll
+          for (int e = 0; e < LE; ++e) {
+            kv[u][e] = ksrc[lane * LE + e];
+            vv[u][e] = vsrc[lane * LE + e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < LE; ++e) kv[u][e] = vv[u][e] = (T)0.f;
         }
-      } else {
-#pragma unroll
-        for (int e = 0; e < LE; ++e) kv[e] = vv[e] = (T)0.f;
       }
 #pragma unroll
-      for (int e = 0; e < LE; ++e) {
-        kd[e] = kv[e];
-        vd[e] = vv[e];
+      for (int u = 0; u < 4; ++u) {
+        const int t = tb + u;
+        if (t >= t0 + np * P) break;
+        T* kd = kpb + ((size_t)(pf[j] + (t - t0) / P) * P + (t - t0) % P) * kD + lane * LE;
+        T* vd = vpb + ((size_t)(pf[j] + (t - t0) / P) * P + (t - t0) % P) * kD + lane * LE;
+#pragma unroll
+        for (int e = 0; e < LE; ++e) {
+          kd[e] = kv[u][e];
+          vd[e] = vv[u][e];
+          if (t < t1) {
+            const float x = (float)kv[u][e];
+            mx[e] = fmaxf(mx[e], x);
+            mn[e] = fminf(mn[e], x);
+          }
+        }
       }
     }
     T* dd = dig + (((size_t)b * Hkv + hk) * maxb + j) * 2 * kD + lane * LE;
@@ -208,41 +266,52 @@ int append_max_tail(int dtype) {
 }
 
 cudaError_t launch_plan_append(const int32_t* tokens, const int32_t* delim_ids, int n_ids, const uint8_t* w10,
-                               int B, int S, int maxb, int C, int delta, int lam_num, int lam_den, int P,
-                               int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
-                               const int32_t* page_first, int32_t* ws, cudaStream_t st) {
-  k_plan_append<<<B, 32, 0, st>>>(tokens, delim_ids, n_ids, w10, S, maxb, C, delta, lam_num, lam_den, P,
-                                   L_prev, L, block_starts, n_blocks, page_first, ws);
-  return post_launch(__func__, st);
+                               int B, int S, int maxb, int maxp, int C, int delta, int lam_num, int lam_den,
+                               int P, int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
+                               int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                               int32_t* n_pages, int32_t* ws, cudaStream_t st) {
+  k_plan_append<<<B, 32, 0, st>>>(tokens, delim_ids, n_ids, w10, S, maxb, maxp, C, delta, lam_num, lam_den, P,
+                                   L_prev, L, block_starts, n_blocks, page_first, page_block, page_valid,
+                                   n_pages, ws);
+  cudaError_t e = post_launch(__func__, st);
+  if (e != cudaSuccess || L_prev > 0) return e;
+  return launch_map_pages(block_starts, n_blocks, B, maxb, maxp, P, page_first, page_block, page_valid,
+                          n_pages, st);
 }
 
-cudaError_t launch_kv_append(int dtype, const void* K_new, const void* V_new, int n_new, int B, int Hkv,
-                             int maxb, int maxp, int P, int L_prev, int max_tail, const int32_t* block_starts,
-                             const int32_t* n_blocks, const int32_t* page_first, const int32_t* ws,
-                             void* Kp, void* Vp, void* dig, cudaStream_t st) {
+cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, const void* const* V_new,
+                             int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
+                             const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
+                             const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
+                             cudaStream_t st) {
+  if (n_layers < 1 || n_layers > kAppendMaxLayers) return cudaErrorInvalidValue;
+  AppendLayers lays = {};
+  for (int l = 0; l < n_layers; ++l) {
+    lays.kn[l] = K_new ? K_new[l] : nullptr;
+    lays.vn[l] = V_new ? V_new[l] : nullptr;
+    lays.kp[l] = Kp[l];
+    lays.vp[l] = Vp[l];
+    lays.dg[l] = dig[l];
+  }
   const size_t esz = dtype == 0 ? 2 : 4;
   const size_t smem = 2 * (size_t)max(max_tail, 1) * kD * esz;
-  dim3 grid(Hkv, B);
+  dim3 grid(Hkv, B, n_layers);
   if (dtype == 0) {
     static bool attr = false;
     if (!attr) {
       allow_max_dyn_smem(k_kv_append<bf16>);
       attr = true;
     }
-    k_kv_append<bf16><<<grid, 256, smem, st>>>(static_cast<const bf16*>(K_new), static_cast<const bf16*>(V_new),
-                                               n_new, Hkv, maxb, maxp, P, L_prev, max_tail, block_starts, n_blocks,
-                                               page_first, ws, static_cast<bf16*>(Kp), static_cast<bf16*>(Vp),
-                                               static_cast<bf16*>(dig));
+    k_kv_append<bf16><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
+                                               block_starts, n_blocks, page_first, ws);
   } else {
     static bool attr = false;
     if (!attr) {
       allow_max_dyn_smem(k_kv_append<float>);
       attr = true;
     }
-    k_kv_append<float><<<grid, 256, smem, st>>>(static_cast<const float*>(K_new), static_cast<const float*>(V_new),
-                                                n_new, Hkv, maxb, maxp, P, L_prev, max_tail, block_starts, n_blocks,
-                                                page_first, ws, static_cast<float*>(Kp), static_cast<float*>(Vp),
-                                                static_cast<float*>(dig));
+    k_kv_append<float><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
+                                                block_starts, n_blocks, page_first, ws);
   }
   return post_launch(__func__, st);
 }

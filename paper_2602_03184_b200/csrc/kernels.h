@@ -89,16 +89,19 @@ cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const 
                                  cudaStream_t st);
 
 // NEXT-1 decode-time append (append_kernels.cu)
+constexpr int kAppendMaxLayers = 64;
 size_t append_ws_bytes(int B);
 int append_max_tail(int dtype);
 cudaError_t launch_plan_append(const int32_t* tokens, const int32_t* delim_ids, int n_ids, const uint8_t* w10,
-                               int B, int S, int maxb, int C, int delta, int lam_num, int lam_den, int P,
-                               int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
-                               const int32_t* page_first, int32_t* ws, cudaStream_t st);
-cudaError_t launch_kv_append(int dtype, const void* K_new, const void* V_new, int n_new, int B, int Hkv,
-                             int maxb, int maxp, int P, int L_prev, int max_tail, const int32_t* block_starts,
-                             const int32_t* n_blocks, const int32_t* page_first, const int32_t* ws,
-                             void* Kp, void* Vp, void* dig, cudaStream_t st);
+                               int B, int S, int maxb, int maxp, int C, int delta, int lam_num, int lam_den,
+                               int P, int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
+                               int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                               int32_t* n_pages, int32_t* ws, cudaStream_t st);
+cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, const void* const* V_new,
+                             int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
+                             const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
+                             const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
+                             cudaStream_t st);
 
 // prefill scoring (score_kernels.cu)
 size_t score_ws_bytes(int Ls, int B, int S, int Hq);

@@ -79,6 +79,7 @@ SIGNATURES = {
                                    _P, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_append_plan": (_I, [_PS, _PC, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_append_kv": (_I, [_PS, _PC, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "dynsplit_append_kv_layers": (_I, [_PS, _PC, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dynsplit_merge_partials": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
     "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
@@ -373,6 +374,19 @@ def append_kv(layer: PagedLayer, K_new, V_new, L_prev: int, L: int, ws) -> None:
         ctypes.byref(layer.shape), ctypes.byref(layer.cfg), L_prev, L, _ptr(K_new), _ptr(V_new),
         _ptr(layer.block_starts), _ptr(layer.n_blocks), _ptr(layer.page_first), _ptr(ws),
         _ptr(layer.Kp), _ptr(layer.Vp), _ptr(layer.digests), _stream()), "append_kv")
+
+
+def append_kv_layers(layers, K_new, V_new, L_prev: int, L: int, ws) -> None:
+    """dynsplit_append_kv_layers: append to several layers sharing one plan in one launch."""
+    n = len(layers)
+    arr = lambda xs: (ctypes.c_void_p * n)(*[ctypes.c_void_p(x.data_ptr()) if x is not None else None
+                                             for x in xs])
+    lay = layers[0]
+    _check(lib().dynsplit_append_kv_layers(
+        ctypes.byref(lay.shape), ctypes.byref(lay.cfg), L_prev, L, n, arr(K_new), arr(V_new),
+        _ptr(lay.block_starts), _ptr(lay.n_blocks), _ptr(lay.page_first), _ptr(ws),
+        arr([x.Kp for x in layers]), arr([x.Vp for x in layers]), arr([x.digests for x in layers]),
+        _stream()), "append_kv_layers")
 
 
 @dataclass

@@ -69,9 +69,13 @@ def test_append_matches_oracle(dtype, C, delta, P, S0, steps, multi):
 
     def step(Lp, L):
         D.append_plan(toks_d, ids, lay0, Lp, L, ws)
-        D.append_kv(lay0, Kd[:, Lp:L].contiguous(), Vd[:, Lp:L].contiguous(), Lp, L, ws)
-        # a second layer sharing the plan: V and K swapped (independent data)
-        D.append_kv(lay1, Vd[:, Lp:L].contiguous(), Kd[:, Lp:L].contiguous(), Lp, L, ws)
+        kn, vn = Kd[:, Lp:L].contiguous(), Vd[:, Lp:L].contiguous()
+        if (L - Lp) % 2:   # one call per layer ...
+            D.append_kv(lay0, kn, vn, Lp, L, ws)
+            # a second layer sharing the plan: V and K swapped (independent data)
+            D.append_kv(lay1, vn, kn, Lp, L, ws)
+        else:              # ... or both layers in one launch
+            D.append_kv_layers([lay0, lay1], [kn, vn], [vn, kn], Lp, L, ws)
 
     step(0, S0)
     torch.cuda.synchronize()
