@@ -379,6 +379,25 @@ def digests(K, block_starts):
     return kmax, kmin
 
 
+def digests_mean(K, block_starts):
+    """NEXT-2 variant: mean-pooling compression ("we further evaluate our
+    approach with mean pooling-based compression"; Appendix A.2,
+    P:646): kmean[h, b, :] = mean over the block's tokens of K[t, h, :].
+    Returns float64 [Hkv, n_b, d]."""
+    K = _f64(K)
+    S, H, d = K.shape
+    nb = len(block_starts) - 1
+    kmean = np.zeros((H, nb, d))
+    for b in range(nb):
+        kmean[:, b, :] = K[int(block_starts[b]):int(block_starts[b + 1])].mean(axis=0)
+    return kmean
+
+
+def block_scores_mean(qh, kmean_h):
+    """Query-compressed vector product with the mean vector: q . kmean."""
+    return (_f64(kmean_h) * _f64(qh)).sum(axis=1)
+
+
 # ---------------------------------------------------------------------------
 # O6  Block score = "query-compressed vector product" (P:255), Q14:
 #     s_b = sum_j max(q_j kmax_j, q_j kmin_j).
@@ -504,23 +523,27 @@ def merge_partials(o_parts, lse_parts):
 # ---------------------------------------------------------------------------
 # One decode step for one sequence and one layer (Steps 1-3).
 # ---------------------------------------------------------------------------
-def decode_step(q, K, V, block_starts, budget, scale=None):
+def decode_step(q, K, V, block_starts, budget, scale=None, digest_mode="minmax"):
     """q [Hq, d]; K, V [S, Hkv, d].  Per query head (Q18): O5 digests, O6
-    scores, O7 selection, O8 attention.  Returns a dict of per-head results."""
+    scores, O7 selection, O8 attention.  digest_mode "mean" uses the
+    mean-pooling variant.  Returns a dict of per-head results."""
     q = _f64(q)
     Hq, d = q.shape
     Hkv = np.asarray(K).shape[1]
     g = Hq // Hkv
     if scale is None:
         scale = 1.0 / math.sqrt(d)
-    kmax, kmin = digests(K, block_starts)
+    if digest_mode == "mean":
+        kmean = digests_mean(K, block_starts)
+    else:
+        kmax, kmin = digests(K, block_starts)
     res = {"scores": [], "tokens": [], "sel_blocks": [], "marginal": [],
            "keep": [], "o": np.zeros((Hq, d)), "lse": np.zeros(Hq)}
     Kf = _f64(K)
     Vf = _f64(V)
     for h in range(Hq):
         hk = h // g
-        sc = block_scores(q[h], kmax[hk], kmin[hk])
+        sc = block_scores_mean(q[h], kmean[hk]) if digest_mode == "mean" else block_scores(q[h], kmax[hk], kmin[hk])
         toks = select_tokens(sc, block_starts, budget)
         sb, m, keep = selection_from_tokens(toks, sc, block_starts, budget)
         o, lse = sparse_attention(q[h], Kf[:, hk, :], Vf[:, hk, :], toks, scale)

@@ -148,3 +148,40 @@ def test_merge_of_splits_equals_one_pass():
         assert np.allclose(o, full_o, atol=1e-12) and L == pytest.approx(full_lse, abs=1e-12)
     o, L = O.merge_partials(np.zeros((2, 32)), np.array([-np.inf, -np.inf]))
     assert L == -np.inf and np.all(o == 0)
+
+
+# ---------------------------------------------------------------- NEXT-2: mean-pooling digests
+def test_mean_digest_special_cases():
+    r = G.rng(31, 1)
+    K = r.standard_normal((10, 2, 8))
+    starts = [0, 1, 4, 10]
+    km = O.digests_mean(K, starts)
+    assert np.array_equal(km[:, 0, :], K[0])                       # singleton block -> k
+    assert np.allclose(km[:, 1, :], (K[1] + K[2] + K[3]) / 3, rtol=0, atol=1e-15)
+    Kc = np.ones((6, 1, 4)) * 2.5                                  # constant block -> the constant
+    assert np.array_equal(O.digests_mean(Kc, [0, 6])[0, 0], np.full(4, 2.5))
+    kmax, kmin = O.digests(K, starts)
+    assert np.all(km <= kmax) and np.all(km >= kmin)               # containment
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_mean_score_is_mean_of_token_scores(seed):
+    # linearity: q . mean_t(k_t) = mean_t (q . k_t), checked token by token
+    r = G.rng(32, seed)
+    S, d = 200, 16
+    K = r.standard_normal((S, 1, d))
+    q = r.standard_normal(d)
+    starts = [0, 7, 40, 41, 90, 200]
+    sc = O.block_scores_mean(q, O.digests_mean(K, starts)[0])
+    for b in range(len(starts) - 1):
+        toks = [float(np.dot(q, K[t, 0])) for t in range(starts[b], starts[b + 1])]
+        assert abs(sc[b] - sum(toks) / len(toks)) <= 1e-12 * (1 + abs(sc[b]))
+
+
+def test_mean_mode_full_budget_equals_dense():
+    q, K, V = G.decode_qkv(33, 300, 4, 2, 16)
+    starts = O.segment(G.tokens(33, 300), G.T7_IDS, G.T7_W10, 32, 14)
+    res = O.decode_step(q, K, V, starts, 10_000, digest_mode="mean")
+    for h in range(4):
+        o, lse = O.dense_attention(q[h], K[:, h // 2], V[:, h // 2], 1 / math.sqrt(16))
+        assert np.allclose(res["o"][h], o, rtol=0, atol=1e-12) and abs(res["lse"][h] - lse) < 1e-12
