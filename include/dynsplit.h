@@ -79,6 +79,9 @@ typedef struct {
   int32_t lambda_num;      /* DD-Select mix lambda = num/den ("alpha"); 1/2 */
   int32_t lambda_den;
   int32_t page_size;       /* P: fixed page length of the uniform mapping; 16 (power of 2, <= 64) */
+  int32_t digest_mode;     /* block compression: 0 = element-wise max/min rows (V2F, the
+                              default); 1 = mean pooling (Appendix A.2): the fp32 mean
+                              of the block's keys in the same digest slot, scored as q . mean */
 } dynsplit_config;
 
 /* Fills the defaults above. */

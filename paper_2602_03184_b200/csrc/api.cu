@@ -102,6 +102,7 @@ dynsplit_status check_cfg(const dynsplit_config* c) {
   if (c->page_size < 1 || c->page_size > 64 || (c->page_size & (c->page_size - 1)))
     return DYNSPLIT_ERR_UNSUPPORTED;  // P: power of two in [1, 64]
   if (c->W < 1 || c->R < 1 || !(c->alpha_pen >= 0.f)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->digest_mode != 0 && c->digest_mode != 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return DYNSPLIT_OK;
 }
 
@@ -187,6 +188,7 @@ void dynsplit_default_config(dynsplit_config* c) {
   c->lambda_num = 1;
   c->lambda_den = 2;
   c->page_size = 16;
+  c->digest_mode = 0;
 }
 
 int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* c) {
@@ -317,7 +319,7 @@ dynsplit_status dynsplit_repack_digest(const dynsplit_shape* s, const dynsplit_c
     return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return cuda_status(launch_repack_digest(s->kv_dtype, K, V, block_starts, n_blocks, page_first,
                                           s->B, s->S, s->Hkv, dynsplit_max_blocks(s->S, c),
-                                          dynsplit_max_pages(s->S, c), c->page_size, Kp, Vp,
+                                          dynsplit_max_pages(s->S, c), c->page_size, c->digest_mode, Kp, Vp,
                                           digests, static_cast<cudaStream_t>(stream)));
 }
 
@@ -371,7 +373,7 @@ dynsplit_status dynsplit_score_blocks(const dynsplit_shape* s, const dynsplit_co
   if (!q || !digests || !n_blocks || !scores) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return cuda_status(launch_score_blocks(s->kv_dtype, s->Hq / s->Hkv, q, digests, n_blocks, scores,
                                          s->B, s->Hq, s->Hkv, dynsplit_max_blocks(s->S, c),
-                                         static_cast<cudaStream_t>(stream)));
+                                         c->digest_mode, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"
@@ -534,7 +536,7 @@ dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynspli
                                       dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
                                       c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks,
                                       page_first, static_cast<const int32_t*>(ws), Kp, Vp, digests,
-                                      static_cast<cudaStream_t>(stream)));
+                                      c->digest_mode, static_cast<cudaStream_t>(stream)));
 }
 
 dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_config* c, int32_t L_prev,

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
                                                    const int32_t* __restrict__ block_starts,
                                                    const int32_t* __restrict__ n_blocks,
                                                    const int32_t* __restrict__ page_first,
-                                                   const int32_t* __restrict__ ws) {
+                                                   const int32_t* __restrict__ ws, int mean_mode) {
   constexpr int LE = kD / 32;  // elements per lane
   extern __shared__ __align__(16) unsigned char smem[];
   T* sK = reinterpret_cast<T*>(smem);  // [max_tail][kD]
@@ -203,11 +203,12 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
   const T* vn = V_new + ((size_t)b * n_new * Hkv + hk) * kD;
   for (int j = f + warp; j < nb; j += nw) {
     const int t0 = bs[j], t1 = bs[j + 1];
-    float mx[LE], mn[LE];
+    float mx[LE], mn[LE], sm[LE];
 #pragma unroll
     for (int e = 0; e < LE; ++e) {
       mx[e] = -CUDART_INF_F;
       mn[e] = CUDART_INF_F;
+      sm[e] = 0.f;
     }
     const int np = (t1 - t0 + P - 1) / P;
     const T* kb = kpb;  // silence unused warnings in some instantiations
@@ -245,15 +246,22 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
             const float x = (float)kv[u][e];
             mx[e] = fmaxf(mx[e], x);
             mn[e] = fminf(mn[e], x);
+            sm[e] += x;  // token order
           }
         }
       }
     }
     T* dd = dig + (((size_t)b * Hkv + hk) * maxb + j) * 2 * kD + lane * LE;
+    if (mean_mode) {  // NEXT-2 mean pooling: fp32 mean row (as k_repack_digest)
+      float* fp = reinterpret_cast<float*>(dig + (((size_t)b * Hkv + hk) * maxb + j) * 2 * kD) + lane * LE;
 #pragma unroll
-    for (int e = 0; e < LE; ++e) {
-      dd[e] = (T)mx[e];       // max / min of stored values: exact
-      dd[kD + e] = (T)mn[e];
+      for (int e = 0; e < LE; ++e) fp[e] = sm[e] / (float)(t1 - t0);
+    } else {
+#pragma unroll
+      for (int e = 0; e < LE; ++e) {
+        dd[e] = (T)mx[e];       // max / min of stored values: exact
+        dd[kD + e] = (T)mn[e];
+      }
     }
   }
 }
@@ -283,7 +291,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
-                             cudaStream_t st) {
+                             int mean_mode, cudaStream_t st) {
   if (n_layers < 1 || n_layers > kAppendMaxLayers) return cudaErrorInvalidValue;
   AppendLayers lays = {};
   for (int l = 0; l < n_layers; ++l) {
@@ -303,7 +311,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
       attr = true;
     }
     k_kv_append<bf16><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
-                                               block_starts, n_blocks, page_first, ws);
+                                               block_starts, n_blocks, page_first, ws, mean_mode);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -311,7 +319,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
       attr = true;
     }
     k_kv_append<float><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
-                                                block_starts, n_blocks, page_first, ws);
+                                                block_starts, n_blocks, page_first, ws, mean_mode);
   }
   return post_launch(__func__, st);
 }

@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
                                                        const int32_t* __restrict__ n_blocks,
                                                        const int32_t* __restrict__ page_first, int S,
                                                        int Hkv, int maxb, int maxp, int P,
-                                                       T* __restrict__ Kp, T* __restrict__ Vp,
-                                                       T* __restrict__ dig) {
+                                                       int mean_mode, T* __restrict__ Kp,
+                                                       T* __restrict__ Vp, T* __restrict__ dig) {
   constexpr int EPC = 16 / sizeof(T);     // elements per 16-byte chunk
   constexpr int CPR = kD / EPC;           // chunks per head row
   const int b = blockIdx.y;
@@ -263,11 +263,12 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
     const int npg = (len + P - 1) / P;
     for (int hc = threadIdx.x; hc < HC; hc += blockDim.x) {
       const int h = hc / CPR, c = hc % CPR;
-      float mx[EPC], mn[EPC];
+      float mx[EPC], mn[EPC], sm[EPC];
 #pragma unroll
       for (int e = 0; e < EPC; ++e) {
         mx[e] = -CUDART_INF_F;
         mn[e] = CUDART_INF_F;
+        sm[e] = 0.f;
       }
       const size_t page_base = ((size_t)b * Hkv + h) * maxp;
       int t = 0;
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
           for (int e = 0; e < EPC; ++e) {
             mx[e] = fmaxf(mx[e], x[e]);
             mn[e] = fminf(mn[e], x[e]);
+            sm[e] += x[e];  // token order
           }
         }
       }
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
         for (int e = 0; e < EPC; ++e) {
           mx[e] = fmaxf(mx[e], x[e]);
           mn[e] = fminf(mn[e], x[e]);
+          sm[e] += x[e];
         }
       }
       const uint4 z = make_uint4(0, 0, 0, 0);
@@ -314,6 +317,12 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
         const size_t dst = ((page_base + p0 + tt / P) * P + tt % P) * kD + c * EPC;
         *reinterpret_cast<uint4*>(Kp + dst) = z;
         *reinterpret_cast<uint4*>(Vp + dst) = z;
+      }
+      if (mean_mode) {  // NEXT-2 mean pooling: fp32 mean row in the digest slot (sum in token order / len)
+        float* fp = reinterpret_cast<float*>(dig + (((size_t)b * Hkv + h) * maxb + blk) * 2 * kD) + c * EPC;
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) fp[e] = sm[e] / (float)len;
+        continue;
       }
       // digest row: [.., 0, :] = kmax, [.., 1, :] = kmin (values are exact copies)
       T* dp = dig + (((size_t)b * Hkv + h) * maxb + blk) * 2 * kD + c * EPC;
@@ -364,18 +373,18 @@ cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int ma
 
 cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
                                  const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
-                                 int maxb, int maxp, int P, void* Kp, void* Vp, void* dig,
+                                 int maxb, int maxp, int P, int mean_mode, void* Kp, void* Vp, void* dig,
                                  cudaStream_t st) {
   const int ctas = max(1, min(maxb, num_sms() * 8 / max(1, B)));
   dim3 grid(ctas, B);
   if (dtype == 0)
     k_repack_digest<bf16><<<grid, 128, 0, st>>>(
         static_cast<const bf16*>(K), static_cast<const bf16*>(V), bs, nb, pf, S, Hkv, maxb, maxp, P,
-        static_cast<bf16*>(Kp), static_cast<bf16*>(Vp), static_cast<bf16*>(dig));
+        mean_mode, static_cast<bf16*>(Kp), static_cast<bf16*>(Vp), static_cast<bf16*>(dig));
   else
     k_repack_digest<float><<<grid, 128, 0, st>>>(
         static_cast<const float*>(K), static_cast<const float*>(V), bs, nb, pf, S, Hkv, maxb, maxp,
-        P, static_cast<float*>(Kp), static_cast<float*>(Vp), static_cast<float*>(dig));
+        P, mean_mode, static_cast<float*>(Kp), static_cast<float*>(Vp), static_cast<float*>(dig));
   return post_launch(__func__, st);
 }
 

@@ -49,6 +49,15 @@ template <> struct DigestDot<bf16> {
     k.mn = *reinterpret_cast<const uint4*>(p + kD);
   }
   static DSK_DEVICE void zero_k(K& k) { k.mx = k.mn = make_uint4(0, 0, 0, 0); }
+  static DSK_DEVICE float dot_mean(const Q& q, const float (&m)[8]) {  // 8 sequential FFMA
+    float a = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a = fmaf(bf_lo(q.w[i]), m[2 * i], a);
+      a = fmaf(bf_hi(q.w[i]), m[2 * i + 1], a);
+    }
+    return a;
+  }
   static DSK_DEVICE float dot(const Q& q, const K& k) {
     const uint32_t mx[4] = {k.mx.x, k.mx.y, k.mx.z, k.mx.w};
     const uint32_t mn[4] = {k.mn.x, k.mn.y, k.mn.z, k.mn.w};
@@ -85,6 +94,12 @@ template <> struct DigestDot<float> {
 #pragma unroll
     for (int j = 0; j < 8; ++j) k.mx[j] = k.mn[j] = 0.f;
   }
+  static DSK_DEVICE float dot_mean(const Q& q, const float (&m)[8]) {
+    float a = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = fmaf(q.v[j], m[j], a);
+    return a;
+  }
   static DSK_DEVICE float dot(const Q& q, const K& k) {
     float a = 0.f;
 #pragma unroll
@@ -119,7 +134,7 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
                                                          const T* __restrict__ dig,
                                                          const int32_t* __restrict__ n_blocks,
                                                          float* __restrict__ scores, int Hq, int Hkv,
-                                                         int maxb, int cap) {
+                                                         int maxb, int cap, int mean_mode) {
   using DD = DigestDot<T>;
   constexpr int RB = 2 * kD * (int)sizeof(T);  // digest bytes per block (kmax, kmin)
   extern __shared__ __align__(128) unsigned char smem[];
@@ -165,13 +180,27 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
   const T* sd = reinterpret_cast<const T*>(smem);
   for (int base = warp * 2; base < n; base += 32) {  // warp-uniform trip count
     const int i = base + half;
-    typename DD::K kb;
-    if (i < pre) DD::load_k_smem(sd + (size_t)i * 2 * kD + hl * 8, kb);
-    else if (i < n) DD::load_k(dbase + (size_t)(lo + i) * 2 * kD + hl * 8, kb);
-    else DD::zero_k(kb);
     float acc[G];
+    if (mean_mode) {
+      // NEXT-2 mean pooling: q . mean, the fp32 mean row in the block's digest slot
+      float mrow[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (i < n) {
+        const float* mp = i < pre ? reinterpret_cast<const float*>(sd + (size_t)i * 2 * kD) + hl * 8
+                                  : reinterpret_cast<const float*>(dbase + (size_t)(lo + i) * 2 * kD) + hl * 8;
+        const float4 a = reinterpret_cast<const float4*>(mp)[0], c = reinterpret_cast<const float4*>(mp)[1];
+        mrow[0] = a.x; mrow[1] = a.y; mrow[2] = a.z; mrow[3] = a.w;
+        mrow[4] = c.x; mrow[5] = c.y; mrow[6] = c.z; mrow[7] = c.w;
+      }
 #pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = DD::dot(qv[g], kb);
+      for (int g = 0; g < G; ++g) acc[g] = DD::dot_mean(qv[g], mrow);
+    } else {
+      typename DD::K kb;
+      if (i < pre) DD::load_k_smem(sd + (size_t)i * 2 * kD + hl * 8, kb);
+      else if (i < n) DD::load_k(dbase + (size_t)(lo + i) * 2 * kD + hl * 8, kb);
+      else DD::zero_k(kb);
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g] = DD::dot(qv[g], kb);
+    }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -225,7 +254,8 @@ __global__ void k_merge_partials(const float* __restrict__ o_parts, const float*
 // to 192 KiB of digests per CTA (blocks beyond it are read from HBM directly).
 template <typename T>
 static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const int32_t* nb,
-                                  float* scores, int B, int Hq, int Hkv, int maxb, cudaStream_t st) {
+                                  float* scores, int B, int Hq, int Hkv, int maxb, int mean_mode,
+                                  cudaStream_t st) {
   const int sms = num_sms();
   const int reserve = min(B * Hq, sms / 4);
   const int chunks = max(1, min((sms - reserve) / max(1, B * Hkv), (maxb + 31) / 32));
@@ -242,7 +272,8 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
       allow_max_dyn_smem(k_score_blocks<T, GG>);                                                     \
       attr = true;                                                                                   \
     }                                                                                                \
-    launch_ex(k_score_blocks<T, GG>, grid, 512, smem, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb, cap); \
+    launch_ex(k_score_blocks<T, GG>, grid, 512, smem, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb, cap,   \
+              mean_mode);                                                                            \
     break;                                                                                           \
   }
   switch (G) {
@@ -257,9 +288,10 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
 }
 
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
-                                float* scores, int B, int Hq, int Hkv, int maxb, cudaStream_t st) {
-  if (dtype == 0) return score_blocks_t<bf16>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, st);
-  return score_blocks_t<float>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, st);
+                                float* scores, int B, int Hq, int Hkv, int maxb, int mean_mode,
+                                cudaStream_t st) {
+  if (dtype == 0) return score_blocks_t<bf16>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, mean_mode, st);
+  return score_blocks_t<float>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, mean_mode, st);
 }
 
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,

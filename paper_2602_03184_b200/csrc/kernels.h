@@ -58,7 +58,8 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 cudaError_t post_launch(const char* where, cudaStream_t st);
 // decode (decode_kernels.cu, select_kernels.cu, attn_kernels.cu)
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
-                                float* scores, int B, int Hq, int Hkv, int maxb, cudaStream_t st);
+                                float* scores, int B, int Hq, int Hkv, int maxb, int mean_mode,
+                                cudaStream_t st);
 size_t select_smem_needed(int maxb, int G);  // (size_t)-1 if it cannot fit
 cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const int32_t* nb,
                           const int32_t* pf, int B, int Hq, int Hkv, int maxb, int max_sel,
@@ -85,7 +86,7 @@ cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int ma
                              int32_t* n_pages, cudaStream_t st);
 cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
                                  const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
-                                 int maxb, int maxp, int P, void* Kp, void* Vp, void* dig,
+                                 int maxb, int maxp, int P, int mean_mode, void* Kp, void* Vp, void* dig,
                                  cudaStream_t st);
 
 // NEXT-1 decode-time append (append_kernels.cu)
@@ -101,7 +102,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
-                             cudaStream_t st);
+                             int mean_mode, cudaStream_t st);
 
 // prefill scoring (score_kernels.cu)
 size_t score_ws_bytes(int Ls, int B, int S, int Hq);

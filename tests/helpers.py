@@ -95,3 +95,55 @@ def row_rel_err(o, o_ref):
 
 def starts_from_gpu(bs_row, nb):
     return [int(x) for x in bs_row[: int(nb) + 1]]
+
+
+# ---------------------------------------------------------------- NEXT-2 mean-pooling mode
+def mean_digest_error_bound(K, starts):
+    """|fp32 mean (token-order fp32 sum, then / len) - exact mean| <=
+    (gamma_len + u) * sum_t |k_t| / len, per (head, block, dim)."""
+    Kf = np.abs(np.asarray(K, np.float64))
+    H = Kf.shape[1]
+    nb = len(starts) - 1
+    out = np.zeros((H, nb, Kf.shape[2]))
+    for b in range(nb):
+        ln = starts[b + 1] - starts[b]
+        out[:, b, :] = (gamma(ln) + U32) * Kf[starts[b]:starts[b + 1]].sum(axis=0) / ln
+    return out
+
+
+def score_error_bound_mean(qh, kmean_h, mean_err_h):
+    """fp32 q . mean_hat: gamma_d sum_j |q_j mean_j| (one rounding per FMA) plus
+    sum_j |q_j| |mean_hat_j - mean_j|, inflated 1 % for the second-order terms."""
+    d = qh.shape[-1]
+    qa = np.abs(np.asarray(qh, np.float64))
+    return 1.01 * (gamma(d) * (qa * (np.abs(kmean_h) + mean_err_h)).sum(-1) + (qa * mean_err_h).sum(-1))
+
+
+def certify_queries_mean(seed, q, K, starts_list, budget, dtype="bf16", max_retry=40):
+    """certify_queries for digest_mode = mean (selection margins vs the bound above)."""
+    q = q.copy()
+    B, Hq, d = q.shape
+    Hkv = K.shape[2]
+    g = Hq // Hkv
+    for b in range(B):
+        st = starts_list[b]
+        km = O.digests_mean(K[b], st)
+        me = mean_digest_error_bound(K[b], st)
+        for h in range(Hq):
+            r = 0
+            while True:
+                sc = O.block_scores_mean(q[b, h], km[h // g])
+                if int(st[-1] - st[0]) <= budget:
+                    break
+                eps = score_error_bound_mean(q[b, h], km[h // g], me[h // g])
+                order, rk = marginal_rank(sc, st, budget)
+                m = order[rk]
+                ok = (rk == 0 or sc[order[rk - 1]] - sc[m] > eps[order[rk - 1]] + eps[m]) and \
+                     (rk + 1 >= len(order) or sc[m] - sc[order[rk + 1]] > eps[m] + eps[order[rk + 1]])
+                if ok:
+                    break
+                r += 1
+                if r > max_retry:
+                    raise RuntimeError("could not certify a query")
+                q[b, h] = G.query_resample(seed, b, h, r, d, dtype)
+    return q

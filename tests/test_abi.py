@@ -43,8 +43,8 @@ def test_library_is_sm100a(D):
 
 def test_default_config_and_bounds(D):
     c = D.default_config()
-    assert (c.W, c.R, c.alpha_pen, c.C, c.delta, c.lambda_num, c.lambda_den, c.page_size) == \
-        (8, 128, 1.0, 32, 14, 1, 2, 16)
+    assert (c.W, c.R, c.alpha_pen, c.C, c.delta, c.lambda_num, c.lambda_den, c.page_size, c.digest_mode) == \
+        (8, 128, 1.0, 32, 14, 1, 2, 16, 0)
     # every non-final chunk has >= C - Delta tokens
     assert D.max_blocks(131072, c) == 131072 // 18 + 1 == 7282
     assert D.max_pages(131072, c) == 7282 + 8192

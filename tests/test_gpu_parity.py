@@ -447,3 +447,33 @@ def test_decode_layer_matches_separate_calls(D, S, Hq, Hkv, budget):
         assert torch.equal(getattr(sel1, name), getattr(sel2, name)), name
     res = H.oracle_decode(q, K, V, starts, budget)
     _check_attention(o1, lse1, res, B, Hq)
+
+
+# ---------------------------------------------------------------- NEXT-2: mean-pooling digests
+@pytest.mark.parametrize("dtype,S,Hq,Hkv,budget", [("bf16", 6000, 32, 8, 900), ("fp32", 3000, 8, 8, 400),
+                                                   ("bf16", 4000, 16, 2, 5000)])
+def test_mean_mode_parity(D, dtype, S, Hq, Hkv, budget):
+    """digest_mode = 1: the fp32 block means within their
+    rounding bound, the selection exactly (margin-certified queries) and the
+    attention within 2e-3, against the oracle's mean-pooling decode step."""
+    B, d = 2, 128
+    cfg = D.default_config(digest_mode=1)
+    toks = np.stack([G.tokens(1700 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    qs, Ks, Vs = zip(*[G.decode_qkv(1710 + b, S, Hq, Hkv, d, dtype=dtype) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    q = H.certify_queries_mean(1710, q, K, starts, budget, dtype)
+    layer = _build(D, toks, K, V, cfg, dtype, Hq)
+    qt = t(q, kv_dtype(dtype))
+    sel = D.select(qt, layer, budget)
+    o, lse = D.decode_attn(qt, layer, sel.worklist)
+    torch.cuda.synchronize()
+    mb = D.max_blocks(S, cfg)
+    dig = layer.digests.contiguous().view(torch.float32).reshape(B, Hkv, mb, -1)[..., :d].cpu().numpy()
+    for b in range(B):
+        nb = len(starts[b]) - 1
+        km = O.digests_mean(K[b], starts[b])
+        assert np.all(np.abs(dig[b, :, :nb] - km) <= H.mean_digest_error_bound(K[b], starts[b]))
+    res = [O.decode_step(q[b], K[b], V[b], starts[b], budget, digest_mode="mean") for b in range(B)]
+    _check_selection(layer, sel, res, B, Hq)
+    _check_attention(o, lse, res, B, Hq)
