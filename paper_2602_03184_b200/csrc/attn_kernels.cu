@@ -85,22 +85,6 @@ DSK_DEVICE void ffma2(float& a0, float& a1, float b0, float b1, uint64_t cc) {
 }
 
 template <typename T> struct QK;
-template <> struct QK<bf16> {
-  static constexpr int kChunks = kD * 2 / 16;  // 16 chunks of 8 bf16
-  // a0 += even elements, a1 += odd elements (two independent FHFMA chains)
-  static DSK_DEVICE void dot2(uint4 qc, uint4 kc, float& a0, float& a1) {
-    const uint32_t qs[4] = {qc.x, qc.y, qc.z, qc.w};
-    const uint32_t ks[4] = {kc.x, kc.y, kc.z, kc.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      unsigned short ql, qh, kl, kh;
-      split_bf16x2(qs[e], ql, qh);
-      split_bf16x2(ks[e], kl, kh);
-      a0 = fma_bf16(ql, kl, a0);
-      a1 = fma_bf16(qh, kh, a1);
-    }
-  }
-};
 template <> struct QK<float> {
   static constexpr int kChunks = kD * 4 / 16;  // 32 chunks of 4 fp32
   static DSK_DEVICE void dot2(uint4 qc, uint4 kc, float& a0, float& a1) {

@@ -180,36 +180,17 @@ DSK_DEVICE void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, u
       ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-// 16-byte cp.async (LDGSTS, bypassing L1) with an L2 cache policy.
-DSK_DEVICE void cp_async16_hint(void* dst_smem, const void* src_gmem, uint64_t policy) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-               ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "l"(policy) : "memory");
-}
-// 16-byte cp.async (LDGSTS, bypassing L1) without a cache policy.  (ptxas
+// 16-byte cp.async (LDGSTS, bypassing L1).  No L2 cache-policy hint: ptxas
 // 12.9 mis-encodes two back-to-back hinted LDGSTS with an odd uniform
-// descriptor register -> illegal instruction; the un-hinted form is safe.)
+// descriptor register (illegal instruction at run time).
 DSK_DEVICE void cp_async16_cg(void* dst_smem, const void* src_gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem)
                : "memory");
-}
-// Arrive on `bar` when all of this thread's prior cp.async have completed
-// (does not increment the expected count: the barrier's count includes it).
-DSK_DEVICE void cp_async_mbar_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 DSK_DEVICE uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
-}
-DSK_DEVICE uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-// Bulk prefetch of [src, src + bytes) into L2 (bytes % 16 == 0, 16-byte aligned).
-DSK_DEVICE void prefetch_l2_bulk(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 // Programmatic dependent launch: wait until the preceding kernel in the
 // stream has completed (and its writes are visible) / allow the next kernel
