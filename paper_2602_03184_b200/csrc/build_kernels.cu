@@ -7,70 +7,154 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cooperative_groups.h>
+#include <stdint.h>
+
 #include <math_constants.h>
 
 namespace dsk {
+namespace cg = cooperative_groups;
 
 // ============================================================================
-// a2: weight table.  grid (B), 256 threads.  Per id: sum of the valid s_i in
-// fp64 (each thread a contiguous position range, then a fixed-order tree),
-// count; then mean, min-max over ids present, round half-up to tenths.
+// a2: weight table.  One cluster of kWtCl CTAs per sequence (grid (kWtCl, B),
+// 256 threads); CTA r takes the r-th contiguous 1/kWtCl of the positions.
+// Tiles of kWtTile positions are staged in smem with coalesced 16-byte loads
+// (tokens and scores); thread t walks positions t, t + 256, ... of the tile,
+// finds the token's id index through a 256-slot open-addressing hash of the
+// ids (~1 probe; most tokens are not delimiters) and adds a valid s_i to its
+// own fp64 row acc[j][t] (count likewise), so every sum has a fixed order.
+// Per id: the 256 rows are summed in a fixed tree (8 per lane in order, then an
+// xor butterfly); rank 0 adds the kWtCl CTAs' sums in rank order through
+// DSMEM, then mean, min-max over the ids present, round half-up to tenths.
 // ============================================================================
-__global__ void __launch_bounds__(256) k_weight_table(const int32_t* __restrict__ tokens,
-                                                      const int32_t* __restrict__ delim_ids, int n_ids,
-                                                      const float* __restrict__ s, uint8_t* __restrict__ w10,
-                                                      int S) {
-  __shared__ double red_s[256];
-  __shared__ int red_c[256];
+constexpr int kWtNT = 256;
+constexpr int kWtTile = 4096;  // positions per smem tile (2048 above 48 ids: the fp64 rows grow)
+constexpr int kWtCl = 8;
+constexpr int kWtHash = 256;
+constexpr int32_t kWtEmpty = INT32_MIN;  // empty hash slot (an id of INT32_MIN is never matched)
+
+static int weight_table_tile(int n_ids) { return n_ids > 48 ? kWtTile / 2 : kWtTile; }
+static size_t weight_table_smem(int n_ids) {
+  return (size_t)weight_table_tile(n_ids) * 8 + (size_t)n_ids * kWtNT * (sizeof(double) + sizeof(int));
+}
+
+DSK_DEVICE uint32_t wt_hash(int32_t t) { return ((uint32_t)t * 0x9E3779B1u) >> 24; }
+
+__global__ void __cluster_dims__(kWtCl, 1, 1) __launch_bounds__(kWtNT)
+    k_weight_table(const int32_t* __restrict__ tokens, const int32_t* __restrict__ delim_ids, int n_ids,
+                   const float* __restrict__ s, uint8_t* __restrict__ w10, int S, int tile_n) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem[];
+  int32_t* t_tok = reinterpret_cast<int32_t*>(smem);                 // [tile_n]
+  float* t_s = reinterpret_cast<float*>(t_tok + tile_n);             // [tile_n]
+  double* acc = reinterpret_cast<double*>(t_s + tile_n);             // [n_ids][kWtNT]
+  int* cnt = reinterpret_cast<int*>(acc + (size_t)n_ids * kWtNT);    // [n_ids][kWtNT]
+  __shared__ int h_key[kWtHash], h_val[kWtHash];
+  __shared__ double csum[64];   // this CTA's per-id sums (read by rank 0)
+  __shared__ int ccnt[64];
   __shared__ double means[64];
   __shared__ int cnts[64];
-  const int b = blockIdx.x, tid = threadIdx.x;
-  const int chunk = (S + 255) / 256;
-  const int p0 = tid * chunk, p1 = min(S, p0 + chunk);
+  const int r = (int)cluster.block_rank(), b = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t* tk = tokens + (size_t)b * S;
   const float* sb = s + (size_t)b * S;
+  for (int i = tid; i < kWtHash; i += kWtNT) h_key[i] = kWtEmpty;
   for (int j = 0; j < n_ids; ++j) {
-    const int id = delim_ids[j];
-    double acc = 0.0;
-    int c = 0;
-    for (int p = p0; p < p1; ++p) {
-      if (tk[p] == id) {
-        const float v = sb[p];
+    acc[j * kWtNT + tid] = 0.0;
+    cnt[j * kWtNT + tid] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < n_ids; ++j) {  // the first occurrence of an id owns it (as a linear search would)
+      const int32_t id = delim_ids[j];
+      uint32_t hh = wt_hash(id);
+      while (h_key[hh] != kWtEmpty && h_key[hh] != id) hh = (hh + 1) & (kWtHash - 1);
+      if (h_key[hh] == kWtEmpty) {
+        h_key[hh] = id;
+        h_val[hh] = j;
+      }
+    }
+  }
+  // this CTA's range, a multiple of 4 positions (16-byte tiles)
+  const int per = ((S + kWtCl - 1) / kWtCl + 3) & ~3;
+  const int lo = min(S, r * per), hi = min(S, lo + per);
+  const bool vec = ((reinterpret_cast<uintptr_t>(tk) | reinterpret_cast<uintptr_t>(sb)) & 15) == 0;
+  for (int p0 = lo; p0 < hi; p0 += tile_n) {
+    const int n = min(tile_n, hi - p0);
+    __syncthreads();  // previous tile consumed (and the hash / zeroed rows visible)
+    if (vec && (n & 3) == 0) {
+      for (int c = tid; c < n / 4; c += kWtNT) {
+        reinterpret_cast<int4*>(t_tok)[c] = __ldg(reinterpret_cast<const int4*>(tk + p0) + c);
+        reinterpret_cast<float4*>(t_s)[c] = __ldg(reinterpret_cast<const float4*>(sb + p0) + c);
+      }
+    } else {
+      for (int c = tid; c < n; c += kWtNT) {
+        t_tok[c] = __ldg(tk + p0 + c);
+        t_s[c] = __ldg(sb + p0 + c);
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int q = tid; q < n; q += kWtNT) {
+      const int32_t t = t_tok[q];
+      uint32_t hh = wt_hash(t);
+      int key;
+      while ((key = h_key[hh]) != kWtEmpty && key != t) hh = (hh + 1) & (kWtHash - 1);
+      if (key == t && t != kWtEmpty) {
+        const float v = t_s[q];
         if (!isnan(v)) {
-          acc += (double)v;
-          ++c;
+          const int j = h_val[hh];
+          acc[j * kWtNT + tid] += (double)v;
+          cnt[j * kWtNT + tid] += 1;
         }
       }
     }
-    red_s[tid] = acc;
-    red_c[tid] = c;
-    __syncthreads();
-    for (int st = 128; st > 0; st >>= 1) {
-      if (tid < st) {
-        red_s[tid] += red_s[tid + st];
-        red_c[tid] += red_c[tid + st];
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      cnts[j] = red_c[0];
-      means[j] = red_c[0] ? red_s[0] / (double)red_c[0] : 0.0;
-    }
-    __syncthreads();
   }
+  __syncthreads();
+  for (int j = warp; j < n_ids; j += kWtNT / 32) {
+    double a = 0.0;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < kWtNT / 32; ++k) {
+      a += acc[j * kWtNT + lane * (kWtNT / 32) + k];
+      c += cnt[j * kWtNT + lane * (kWtNT / 32) + k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      csum[j] = a;
+      ccnt[j] = c;
+    }
+  }
+  cluster.sync();  // every CTA's csum / ccnt are visible to rank 0
+  if (r == 0 && tid < n_ids) {
+    double a = 0.0;
+    int c = 0;
+    for (int rr = 0; rr < kWtCl; ++rr) {  // rank order
+      a += cluster.map_shared_rank(csum, rr)[tid];
+      c += cluster.map_shared_rank(ccnt, rr)[tid];
+    }
+    cnts[tid] = c;
+    means[tid] = c ? a / (double)c : 0.0;
+  }
+  cluster.sync();  // the peers' shared memory stays alive until rank 0 has read it
+  if (r != 0) return;
   if (tid == 0) {
     bool any = false;
-    double lo = 0.0, hi = 0.0;
+    double lo_m = 0.0, hi_m = 0.0;
     for (int j = 0; j < n_ids; ++j) {
       if (!cnts[j]) continue;
-      if (!any || means[j] < lo) lo = means[j];
-      if (!any || means[j] > hi) hi = means[j];
+      if (!any || means[j] < lo_m) lo_m = means[j];
+      if (!any || means[j] > hi_m) hi_m = means[j];
       any = true;
     }
     for (int j = 0; j < n_ids; ++j) {
       int w = 0;
       if (cnts[j]) {
-        const double ww = (hi == lo) ? 1.0 : (means[j] - lo) / (hi - lo);
+        const double ww = (hi_m == lo_m) ? 1.0 : (means[j] - lo_m) / (hi_m - lo_m);
         w = (int)floor(10.0 * ww + 0.5);
       }
       w10[(size_t)b * n_ids + j] = (uint8_t)w;
@@ -348,7 +432,13 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
 // ============================================================================
 cudaError_t launch_weight_table(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
                                 const float* s, uint8_t* w10, int B, int S, cudaStream_t st) {
-  k_weight_table<<<B, 256, 0, st>>>(tokens, delim_ids, n_ids, s, w10, S);
+  const size_t smem = weight_table_smem(n_ids);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_weight_table, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_weight_table<<<dim3(kWtCl, B), kWtNT, smem, st>>>(tokens, delim_ids, n_ids, s, w10, S,
+                                                      weight_table_tile(n_ids));
   return post_launch(__func__, st);
 }
 

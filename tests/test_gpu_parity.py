@@ -90,6 +90,31 @@ def test_weight_table_parity(D, seed):
         assert w10[b].tolist() == ref.tolist()
 
 
+@pytest.mark.parametrize("S,n_ids", [(3 * 4096 + 123, 13), (2 * 4096, 13), (9000, 64), (131072, 13)])
+def test_weight_table_parity_tiles(D, S, n_ids):
+    """Several 4096-position smem tiles plus a ragged tail; 64 ids (the API
+    maximum: the largest shared-memory footprint); the 128K C5 length."""
+    B = 2
+    r = G.rng(S + n_ids, 22)
+    if n_ids == 13:
+        ids = G.T7_IDS
+        toks = np.stack([G.tokens(S + b, S) for b in range(B)])
+    else:
+        ids = np.arange(1000, 1000 + n_ids, dtype=np.int32)
+        toks = r.integers(900, 1000 + n_ids + 100, size=(B, S)).astype(np.int32)
+    for tries in range(20):
+        s = r.standard_normal((B, S)).astype(np.float32)
+        s[r.random((B, S)) < 0.1] = np.nan
+        if all(_table_certified(toks[b], s[b], ids) for b in range(B)):
+            break
+    else:
+        pytest.fail("no certified table")
+    w10 = D.weight_table(t(toks), t(ids), t(s)).cpu().numpy()
+    for b in range(B):
+        ref, _ = O.weight_table(toks[b], s[b], ids)
+        assert w10[b].tolist() == ref.tolist()
+
+
 # ---------------------------------------------------------------- a4 map + repack + digest
 @pytest.mark.parametrize("dtype,P,S", [("bf16", 16, 4099), ("fp32", 16, 2000), ("bf16", 8, 1500),
                                        ("bf16", 32, 777), ("bf16", 16, 1)])

@@ -44,7 +44,10 @@ t1, s = timed(lambda: D.score_delimiters(toks, ids, Qs, Ks, cfg))
 t2, w10 = timed(lambda: D.weight_table(toks, ids, s))
 t3, (bs, nb) = timed(lambda: D.segment(toks, ids, w10, cfg))
 t4a, (pf, pb, pv, npg) = timed(lambda: D.map_pages(bs, nb, S, cfg))
-t4b, _ = timed(lambda: D.repack_digest(K, V, bs, nb, pf, cfg))
+# outputs preallocated once: an allocation inside the timed loop (cudaMalloc of
+# ~2.5 GiB at 128K, B = 4) would be timed as kernel time
+kvd = D.repack_digest(K, V, bs, nb, pf, cfg)
+t4b, _ = timed(lambda: D.repack_digest(K, V, bs, nb, pf, cfg, out=kvd))
 rows = np.arange(S, dtype=np.float64) + 1
 flop = 2.0 * d * Hq * rows.sum() * B
 bytes4 = 2 * 2 * B * S * Hkv * d * 2 + int(nb.sum()) * Hkv * 2 * d * 2
