@@ -7,9 +7,9 @@ Workload (config.workload): BASELINE.json config 3's per-GPU shard -- a
 Llama-3-8B-shaped decode step (32 layers, 32 Q / 8 KV heads, d = 128, bf16 KV)
 at 128K context, token budget 4096, `--batch-per-gpu` sequences per GPU
 (default 1, so N = 8 is config 3's batch 8 sharded by batch).  A step = one
-decode token through all 32 layers: per layer a5 block scoring + a6 budgeted
-selection + a7/a8 split-K sparse attention with LSE merge, all in
-libdynsplit.so kernels, replayed as one CUDA graph.  Sequences are independent
+decode token through all 32 layers: per layer dynsplit_decode_layer = a5 block
+scoring + a6 budgeted selection + a7/a8 split-K sparse attention with LSE
+merge, all in libdynsplit.so kernels, replayed as one CUDA graph.  Sequences are independent
 (no data-path collective); scaling is weak (fixed work per GPU).
 
 value = aggregate algorithmic HBM bytes per step (digests + GQA-union of the
@@ -276,10 +276,14 @@ def main():
     def attn_layer(l):
         return D.decode_attn(qs[l], layers[l], sel_out[l][4], out=attn_out[l], ws=ws_dec)
 
+    ws_step = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer_step")
+
     def step():
+        # the public per-layer call (a5 -> a6 -> a7+a8, PDL-ordered)
         for l in range(L):
-            sel_layer(l)
-            attn_layer(l)
+            _, ns, mg, kp, wl = sel_out[l]
+            D.decode_layer(qs[l], layers[l], budget, out=(ns, mg, kp, wl, attn_out[l][0], attn_out[l][1]),
+                           ws=ws_step)
 
     def dense_step():
         for l in range(L):

@@ -41,10 +41,18 @@ ws_dec = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "deco
 
 
 FUSED = True  # dynsplit_select (a5 + a6 through one ABI call)
+# TL_MODE=layer: dynsplit_decode_layer per layer; default: dynsplit_select +
+# dynsplit_decode_attn
+LAYER = os.environ.get("TL_MODE") == "layer"
+ws_lay = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer")
 
 
 def step():
     for l in range(L):
+        if LAYER:
+            _, ns, mg, kp, wl = sels[l]
+            D.decode_layer(qs[l], layers[l], budget, out=(ns, mg, kp, wl, outs[l][0], outs[l][1]), ws=ws_lay)
+            continue
         if FUSED:
             sb, ns, mg, kp, wl = sels[l]
             D.select(qs[l], layers[l], budget, out=(sb, ns, mg, kp, wl, None), ws=ws_sel)
