@@ -371,8 +371,10 @@ dynsplit_status dynsplit_score_blocks(const dynsplit_shape* s, const dynsplit_co
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!q || !digests || !n_blocks || !scores) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  // expected blocks per sequence: DD-Select averages C tokens per block; 25 % slack
+  const int nb_hint = (int)(((int64_t)s->S * 5 + 4 * c->C - 1) / (4 * c->C));
   return cuda_status(launch_score_blocks(s->kv_dtype, s->Hq / s->Hkv, q, digests, n_blocks, scores,
-                                         s->B, s->Hq, s->Hkv, dynsplit_max_blocks(s->S, c),
+                                         s->B, s->Hq, s->Hkv, dynsplit_max_blocks(s->S, c), nb_hint,
                                          c->digest_mode, static_cast<cudaStream_t>(stream)));
 }
 

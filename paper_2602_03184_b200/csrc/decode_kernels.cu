@@ -254,13 +254,20 @@ __global__ void k_merge_partials(const float* __restrict__ o_parts, const float*
 // to 192 KiB of digests per CTA (blocks beyond it are read from HBM directly).
 template <typename T>
 static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const int32_t* nb,
-                                  float* scores, int B, int Hq, int Hkv, int maxb, int mean_mode,
-                                  cudaStream_t st) {
+                                  float* scores, int B, int Hq, int Hkv, int maxb, int nb_hint,
+                                  int mean_mode, cudaStream_t st) {
   const int sms = num_sms();
   const int reserve = min(B * Hq, sms / 4);
-  const int chunks = max(1, min((sms - reserve) / max(1, B * Hkv), (maxb + 31) / 32));
   const int rb = 2 * kD * (int)sizeof(T);
-  const int cap = min((maxb + chunks - 1) / chunks, (192 * 1024) / rb);
+  const int cap_max = (192 * 1024) / rb;  // blocks one CTA can stage in shared memory
+  // One wave on the SMs not reserved for the select CTAs when that covers the
+  // expected blocks (B = 1); otherwise enough CTAs that every CTA's range fits
+  // its shared-memory stage (several waves, still one HBM pass: the blocks
+  // past the stage would be loaded by dependent global loads).
+  const int base = (sms - reserve) / max(1, B * Hkv);
+  const int need = (min(nb_hint, maxb) + cap_max - 1) / cap_max;
+  const int chunks = max(1, min(max(base, need), (maxb + 31) / 32));
+  const int cap = min((maxb + chunks - 1) / chunks, cap_max);
   const size_t smem = (size_t)cap * rb;
   dim3 grid(chunks, Hkv, B);
   const T* qq = static_cast<const T*>(q);
@@ -288,10 +295,11 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
 }
 
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
-                                float* scores, int B, int Hq, int Hkv, int maxb, int mean_mode,
-                                cudaStream_t st) {
-  if (dtype == 0) return score_blocks_t<bf16>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, mean_mode, st);
-  return score_blocks_t<float>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, mean_mode, st);
+                                float* scores, int B, int Hq, int Hkv, int maxb, int nb_hint,
+                                int mean_mode, cudaStream_t st) {
+  if (dtype == 0)
+    return score_blocks_t<bf16>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, nb_hint, mean_mode, st);
+  return score_blocks_t<float>(G, q, dig, nb, scores, B, Hq, Hkv, maxb, nb_hint, mean_mode, st);
 }
 
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,

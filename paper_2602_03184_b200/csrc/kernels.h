@@ -58,8 +58,8 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 cudaError_t post_launch(const char* where, cudaStream_t st);
 // decode (decode_kernels.cu, select_kernels.cu, attn_kernels.cu)
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
-                                float* scores, int B, int Hq, int Hkv, int maxb, int mean_mode,
-                                cudaStream_t st);
+                                float* scores, int B, int Hq, int Hkv, int maxb, int nb_hint,
+                                int mean_mode, cudaStream_t st);  // nb_hint: expected blocks per sequence
 size_t select_smem_needed(int maxb, int G);  // (size_t)-1 if it cannot fit
 cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const int32_t* nb,
                           const int32_t* pf, int B, int Hq, int Hkv, int maxb, int max_sel,
