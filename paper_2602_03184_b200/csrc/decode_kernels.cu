@@ -19,9 +19,10 @@ namespace dsk {
 // because kmax >= kmin element-wise; for bf16 the per-head choice is one
 // byte-permute per bf16 pair (signs of q fixed per lane) and the product is
 // an exact bf16 x bf16 FHFMA into fp32.  The per-block reduction order (8
-// sequential terms, then a 16-lane xor tree) is fixed and independent of the
-// grid, so every launch configuration (and every sequence-split rank) yields
-// identical fp32 scores.
+// sequential terms, then the 16-lane multi-head butterfly of
+// halfwarp_reduce_heads) is fixed and independent of the grid, so every
+// launch configuration (and every sequence-split rank) yields identical fp32
+// scores.
 // ============================================================================
 template <typename T> struct DigestDot;
 template <> struct DigestDot<bf16> {
@@ -107,6 +108,38 @@ template <> struct DigestDot<float> {
     return a;
   }
 };
+
+// Sum G per-lane partials over the 16 lanes of a half-warp with G - 1 + log2(16 / G)
+// shuffles instead of 4 G: at offsets 8, 4, ... while a lane still holds more
+// than one head, the lower lane of each pair keeps the first half of its
+// heads and the upper lane the second half, each adding its partner's copy
+// of what it keeps; then a plain xor tree over the remaining offsets.  The
+// order depends only on the lane (dimension) positions, so the scores stay
+// grid-independent.  Returns the sum of head `head`; every lane with
+// (hl & (16 / G - 1)) == 0 holds a distinct head.
+template <int G>
+DSK_DEVICE float halfwarp_reduce_heads(const float (&a)[G], int hl, int& head) {
+  static_assert(G >= 1 && G <= 16 && (G & (G - 1)) == 0, "G must be a power of two <= 16");
+  float v[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) v[g] = a[g];
+  head = 0;
+  int o = 8;
+#pragma unroll
+  for (int c = G; c > 1; c >>= 1, o >>= 1) {
+    const bool up = (hl & o) != 0;
+#pragma unroll
+    for (int g = 0; g < c / 2; ++g) {
+      const float keep = up ? v[g + c / 2] : v[g];
+      const float send = up ? v[g] : v[g + c / 2];
+      v[g] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    head += up ? c / 2 : 0;
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
 
 // Optional per-CTA phase timestamps (debug only; dynsplit_debug_score_timer).
 __device__ unsigned long long* g_score_dbg = nullptr;
@@ -201,15 +234,9 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
 #pragma unroll
       for (int g = 0; g < G; ++g) acc[g] = DD::dot(qv[g], kb);
     }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-    }
-    if (hl == 0 && i < n) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) sbase[(size_t)g * maxb + lo + i] = acc[g];
-    }
+    int hd;
+    const float r = halfwarp_reduce_heads<G>(acc, hl, hd);
+    if ((hl & (16 / G - 1)) == 0 && i < n) sbase[(size_t)hd * maxb + lo + i] = r;
   }
   sstamp(2);
 }
