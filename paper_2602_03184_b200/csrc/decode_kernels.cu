@@ -208,12 +208,13 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
   __syncthreads();  // the barrier's initialisation is visible
   mbar_wait(&bar, 0);
   __syncwarp();
+  sstamp(3);
 
-  // a half-warp per block; lane hl owns dims [8 hl, 8 hl + 8) of kmax / kmin
+  // a half-warp per block; lane hl owns dims [8 hl, 8 hl + 8) of kmax / kmin.
+  // Two passes per iteration (blocks base + half and base + 32 + half): two
+  // independent load -> dot -> butterfly chains in flight per warp.
   const T* sd = reinterpret_cast<const T*>(smem);
-  for (int base = warp * 2; base < n; base += 32) {  // warp-uniform trip count
-    const int i = base + half;
-    float acc[G];
+  auto block_dots = [&](int i, float (&acc)[G]) {
     if (mean_mode) {
       // NEXT-2 mean pooling: q . mean, the fp32 mean row in the block's digest slot
       float mrow[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -234,9 +235,19 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
 #pragma unroll
       for (int g = 0; g < G; ++g) acc[g] = DD::dot(qv[g], kb);
     }
-    int hd;
-    const float r = halfwarp_reduce_heads<G>(acc, hl, hd);
-    if ((hl & (16 / G - 1)) == 0 && i < n) sbase[(size_t)hd * maxb + lo + i] = r;
+  };
+  for (int base = warp * 2; base < n; base += 64) {  // warp-uniform trip count
+    const int i0 = base + half, i1 = base + 32 + half;
+    float a0[G], a1[G];
+    block_dots(i0, a0);
+    block_dots(i1, a1);
+    int h0, h1;
+    const float r0 = halfwarp_reduce_heads<G>(a0, hl, h0);
+    const float r1 = halfwarp_reduce_heads<G>(a1, hl, h1);
+    if ((hl & (16 / G - 1)) == 0) {
+      if (i0 < n) sbase[(size_t)h0 * maxb + lo + i0] = r0;
+      if (i1 < n) sbase[(size_t)h1 * maxb + lo + i1] = r1;
+    }
   }
   sstamp(2);
 }

@@ -105,7 +105,7 @@ def show(name, arr, cols):
         print(f"{name:7s} {n:13s} n={len(r):4d} min {r.min():7.2f} p50 {np.median(r):7.2f} max {r.max():7.2f} us")
 
 
-show("score", sc, ["start", "pdl_wait", "end"])
+show("score", sc, ["start", "pdl_wait", "end", "digests_in"])
 se = bufs["select"].view(-1, 16).cpu().numpy().astype(np.float64)
 se = se[se[:, 0] > 0]
 show("select", se, ["start", "plan", "pdl_wait", "keys", "threshold", "bits+arrive", "wait+peers",
