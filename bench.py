@@ -337,14 +337,18 @@ def main():
     # ---- timed region 1: whole-step graph
     cur = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(cur)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            step_evs[i].record(cur)
             g_step.replay()
+        step_evs[-1].record(cur)
         ev1.record(cur)
         barrier()
     step_ms = ev0.elapsed_time(ev1) / args.steps
+    per_step = np.array([step_evs[i].elapsed_time(step_evs[i + 1]) for i in range(args.steps)])
 
     # ---- timed region 2: the step's kernel groups, each as an L-layer graph
     barrier()
@@ -499,6 +503,7 @@ def main():
                        "page_size": cfg.page_size, "parallelism": f"batch-shard x{world}",
                        "l2": "no flush: ~%.0f MiB touched per step >> 126 MB L2" % (step_bytes / 2**20)},
             "us_per_step": step_ms * 1e3,
+            "step_ms_p10_p50_p90": [float(np.percentile(per_step, p)) for p in (10, 50, 90)],
             "us_per_layer": step_ms * 1e3 / L,
             "bytes_per_step": step_bytes,
             "union_factor": union_rows / (L * B * Hkv * budget),

@@ -636,6 +636,17 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
     const size_t row = (size_t)b * Hq + hk * G + h;
     const float* pl = part_lse + row * n_split;
     const float4* po_base = reinterpret_cast<const float4*>(part_o + row * n_split * kD) + lane;
+    // the first 16 partial-o loads of this part are issued together with the
+    // lse loads, so their L2 latency overlaps the weight reductions
+    float4 po[16];
+    auto load_po = [&](int s0) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int s = s0 + k * R;
+        po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    load_po(part);
     const float l0 = lane < n_eff ? __ldcg(pl + lane) : -CUDART_INF_F;
     const float l1 = lane + 32 < n_eff ? __ldcg(pl + lane + 32) : -CUDART_INF_F;
     float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -646,12 +657,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
       L = M + logf(sum);
       const float w0 = expf(l0 - L), w1 = expf(l1 - L);
       for (int s0 = part; s0 < n_eff; s0 += 16 * R) {
-        float4 po[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int s = s0 + k * R;
-          po[k] = s < n_eff ? __ldcg(po_base + (size_t)s * (kD / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        if (s0 != part) load_po(s0);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int s = s0 + k * R;

@@ -294,12 +294,11 @@ __global__ void __launch_bounds__(128) k_lse_band(const int32_t* __restrict__ to
 //     dims each, bf16 in, fp32 accumulate) into one of two 128-column TMEM
 //     accumulators; tcgen05.commit frees the K stage and publishes S.
 //   warps 0-7 (epilogue): warp w reads TMEM lane quadrant w % 4 (rows
-//     32 (w % 4) + lane) and column group w / 4 (64 keys) of every tile with
-//     tcgen05.ld 32x32b.x32; a row's column groups keep separate online (max,
-//     sum) in the exp2 domain (pass 1) and separate band sums Ov[w], Fut[w]
-//     (pass 2: p = exp2(z - lse2) over the band tiles), combined through
-//     shared memory in fixed group order.  Per candidate, rows summed in row
-//     order.
+//     32 (w % 4) + lane) and column half w / 4 of every tile with tcgen05.ld
+//     32x32b; a row's two halves keep separate online (max, sum) in the exp2
+//     domain (pass 1) and separate band sums Ov[w], Fut[w] (pass 2:
+//     p = exp2(z - lse2) over the band tiles), combined once through shared
+//     memory in fixed order.  Per candidate, rows summed in row order.
 // TMEM: 256 columns (2 accumulators); smem 3 x 32 KiB + 1 KiB alignment.
 // ============================================================================
 constexpr int kTcRows = 128;   // rows per CTA (M) = keys per tile (N)
@@ -333,9 +332,7 @@ DSK_DEVICE void tc_ld32(uint32_t addr, float (&f)[32]) {
   for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
 }
 
-constexpr int kTcEpiWarps = 8;   // two warps per TMEM lane quadrant: column halves (16 warps / quarters measured slower: 6.31 vs 5.76 ms at 32K)
-constexpr int kTcNQ = kTcEpiWarps / 4;         // column groups
-constexpr int kTcCols = kTcRows / kTcNQ;       // keys per warp per tile (32)
+constexpr int kTcEpiWarps = 8;  // two warps per TMEM lane quadrant: column halves
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;
 
 // TMA: one 2-D box of 64 dims x 128 rows (128-byte swizzle, rows past S zero-filled)
@@ -362,7 +359,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
   unsigned char* sK = smem + kTcTileBytes;        // [kTcStage][2 halves][128 rows][128 B]
   float* cbuf = reinterpret_cast<float*>(sK);     // [128][kMaxW], after the last MMA
   constexpr int kX = 2 + 2 * kMaxW + 1;
-  __shared__ float xch[kTcRows * kTcNQ * kX];     // [row][quarter][kX] exchange
+  __shared__ float xch[kTcRows * kX];             // half-row exchange (live while K stages are)
   __shared__ __align__(8) uint64_t kfull[kTcStage], kempty[kTcStage], sfull[2], sempty[2];
   __shared__ uint32_t s_tmem;
   __shared__ int s_ids[64];
@@ -444,7 +441,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
       __syncwarp();
     }
   } else {  // ---------------------------------------------------- epilogue
-    // warp w: TMEM lane quadrant q = w % 4 (rows 32 q + lane), column group hw = w / 4
+    // warp w: TMEM lane quadrant q = w % 4 (rows 32 q + lane), column half hw = w / 4
     const int q = warp & 3, hw = warp >> 2;
     const int lr = q * 32 + lane, row = r0 + lr;
     float m = -CUDART_INF_F, l = 0.f, lse2 = 0.f;
@@ -455,33 +452,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
       const int bb = i & 1, kt = tile_of(i);
       mbar_wait(&sfull[bb], (i >> 1) & 1);
       tc_fence_after();
-      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(bb * kTcRows + hw * kTcCols);
-      if (i == n1) {  // pass 1 complete: combine the row's column groups (fixed order)
-        float* xr = xch + lr * kTcNQ * kX;
-        xr[hw * kX + 0] = m;
-        xr[hw * kX + 1] = l;
-        named_bar_sync(1, kTcEpiWarps * 32);
-        float mm = -CUDART_INF_F;
-#pragma unroll
-        for (int u = 0; u < kTcNQ; ++u) mm = fmaxf(mm, xr[u * kX]);
-        float ll = 0.f;
-#pragma unroll
-        for (int u = 0; u < kTcNQ; ++u) {
-          const float mu = xr[u * kX];
-          ll += mu == -CUDART_INF_F ? 0.f : xr[u * kX + 1] * ex2(mu - mm);
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(bb * kTcRows + hw * 64);
+      if (i == n1) {  // pass 1 complete: combine the two column halves of the row
+        float* xr = xch + lr * kX;
+        if (hw) {
+          xr[0] = m;
+          xr[1] = l;
         }
-        lse2 = mm + __log2f(ll);  // every group computes the same value in the same order
+        named_bar_sync(1, kTcEpiWarps * 32);
+        const float m2 = hw ? m : xr[0], l2 = hw ? l : xr[1];
+        const float mm = hw ? m : fmaxf(m, m2);
+        float ll = l;
+        if (!hw) {
+          ll = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mm)) + (m2 == -CUDART_INF_F ? 0.f : l2 * ex2(m2 - mm));
+          xr[0] = mm + __log2f(ll);
+        }
+        named_bar_sync(1, kTcEpiWarps * 32);
+        lse2 = xr[0];
       }
-      for (int c0 = 0; c0 < kTcCols; c0 += 32) {
+      for (int c0 = 0; c0 < 64; c0 += 32) {
         float z[32];
         __syncwarp();  // .aligned TMEM loads need the converged warp
         tc_ld32(base + (uint32_t)c0, z);
-        if (c0 == kTcCols - 32) {  // the accumulator may be overwritten now
+        if (c0 == 32) {  // the accumulator may be overwritten now
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sempty[bb]);
         }
-        const int key0 = kt * kTcRows + hw * kTcCols + c0;
+        const int key0 = kt * kTcRows + hw * 64 + c0;
         if (i < n1) {
           // raw logits; the scale (> 0) is folded into one FFMA per element below
           if (kt == T) {  // diagonal tile: causal mask
@@ -525,26 +523,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
       }
     }
     // every MMA has completed (the last sfull was waited): the K stages are free.
-    // Combine the column groups of each row (group 0 + 1 + 2 + 3, fixed order).
-    float* xr = xch + lr * kTcNQ * kX;
+    // Combine the two column halves of each row (half 0 + half 1, fixed order).
+    named_bar_sync(1, kTcEpiWarps * 32);
+    float* xr = xch + lr * kX;
     if (hw) {
-      xr[hw * kX + 2] = ov_all;
+      xr[2] = ov_all;
 #pragma unroll
       for (int w = 0; w < kMaxW; ++w) {
-        xr[hw * kX + 3 + w] = ov[w];
-        xr[hw * kX + 3 + kMaxW + w] = fu[w];
+        xr[3 + w] = ov[w];
+        xr[3 + kMaxW + w] = fu[w];
       }
     }
     named_bar_sync(1, kTcEpiWarps * 32);
     if (!hw) {
+      ov_all += xr[2];
 #pragma unroll
-      for (int u = 1; u < kTcNQ; ++u) {
-        ov_all += xr[u * kX + 2];
-#pragma unroll
-        for (int w = 0; w < kMaxW; ++w) {
-          ov[w] += xr[u * kX + 3 + w];
-          fu[w] += xr[u * kX + 3 + kMaxW + w];
-        }
+      for (int w = 0; w < kMaxW; ++w) {
+        ov[w] += xr[3 + w];
+        fu[w] += xr[3 + kMaxW + w];
       }
     }
     const int32_t* tk = tokens + (size_t)b * S;
