@@ -39,6 +39,22 @@ DSK_DEVICE float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Packed fp32 pair arithmetic (sm_100 FFMA2 / FADD2): two independent
+// IEEE-rounded operations per instruction, bit-identical to two scalar ones.
+DSK_DEVICE void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+DSK_DEVICE void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
 DSK_DEVICE void cp_async16(void* dst, const void* src, bool pred) {
   const int n = pred ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n)
@@ -494,10 +510,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_lse_band_tc(const __grid_cons
           const float mn = fmaxf(m, tmax * scale_log2);
           if (mn == -CUDART_INF_F) continue;  // nothing valid yet in this row
           const float nmn = -mn;
-          float ls[4] = {0.f, 0.f, 0.f, 0.f};
+          // four running sums, ls[r] over columns j = r (mod 4) in order, as
+          // two packed pairs: FFMA2 for the scaled logits, FADD2 for the sums
+          float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) ls[j & 3] += ex2(fmaf(z[j], scale_log2, nmn));
-          l = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mn)) + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
+          for (int j = 0; j < 32; j += 2) {
+            float x0, x1;
+            fma2(x0, x1, z[j], z[j + 1], scale_log2, scale_log2, nmn, nmn);
+            const float e0 = ex2(x0), e1 = ex2(x1);
+            if ((j & 2) == 0) add2(ls0, ls1, ls0, ls1, e0, e1);
+            else add2(ls2, ls3, ls2, ls3, e0, e1);
+          }
+          l = (m == -CUDART_INF_F ? 0.f : l * ex2(m - mn)) + ((ls0 + ls1) + (ls2 + ls3));
           m = mn;
         } else {
           // band: dk = row - key in [0, band]
