@@ -1,7 +1,8 @@
 """Full-size parity at BASELINE.json's sizes, in the launch configuration
-bench.py times (same C-ABI calls, same grids): config 3 per-GPU shard
-(128K, 32Q/8KV, budget 4096, bf16), config 4 heads (40 MHA) at 128K and the
-config 5 prefill scoring at 64K on sampled candidates.
+bench.py times (dynsplit_decode_layer, same grids): config 3 per-GPU shard
+(128K, 32Q/8KV, budget 4096, bf16), config 4 heads (40 MHA) at 128K, config 2
+(32K, budget 2K) and the config 5 prefill scoring at 64K on sampled
+candidates.
 
 Outputs the oracle can compute directly (plans, page maps, every head's
 selection and attention output) are compared in full; digests and delimiter
@@ -22,10 +23,12 @@ def t(x, dtype=None):
     return torch.as_tensor(np.ascontiguousarray(x)).to(DEV, dtype=dtype)
 
 
-@pytest.mark.parametrize("Hq,Hkv,budget", [(32, 8, 4096), (40, 40, 4096)])
-def test_decode_128k(Hq, Hkv, budget):
+@pytest.mark.parametrize("S,Hq,Hkv,budget", [(131072, 32, 8, 4096), (131072, 40, 40, 4096),
+                                             (32768, 32, 8, 2048)])
+def test_decode_128k(S, Hq, Hkv, budget):
+    """Configs 3 (per-GPU shard), 4 (40 MHA heads) and 2 (32K, budget 2K)."""
     from paper_2602_03184_b200 import dynsplit as D
-    S, d = 131072, 128
+    d = 128
     cfg = D.default_config()
     toks = G.tokens(2000, S)
     q, K, V = G.decode_qkv(2001, S, Hq, Hkv, d)
@@ -37,7 +40,9 @@ def test_decode_128k(Hq, Hkv, budget):
     sel = D.select(qt, layer, budget)
     o, lse = D.decode_attn(qt, layer, sel.worklist)
     o_d, lse_d = D.decode_attn(qt, layer, None)
+    o_l, lse_l, sel_l = D.decode_layer(qt, layer, budget)   # the call bench.py times
     torch.cuda.synchronize()
+    assert torch.equal(o_l, o) and torch.equal(lse_l, lse) and torch.equal(sel_l.n_sel, sel.n_sel)
     nb = int(layer.n_blocks[0])
     assert layer.block_starts[0, : nb + 1].tolist() == starts
     pf, pb, pv = O.page_map(starts, cfg.page_size)
