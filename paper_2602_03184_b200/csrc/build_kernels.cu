@@ -327,6 +327,11 @@ DSK_DEVICE void unpack16(const uint4& u, float* x) {
   }
 }
 
+// tokens per thread per iteration (2 kRpU 16-byte loads in flight); measured at
+// 128K, B = 4 with a one-wave grid: 2 -> 804 us, 4 -> 838 us, 8 -> 910 us (fewer
+// registers, more resident warps)
+constexpr int kRpU = 2;
+
 template <typename T>
 __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, const T* __restrict__ V,
                                                        const int32_t* __restrict__ block_starts,
@@ -356,16 +361,16 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
       }
       const size_t page_base = ((size_t)b * Hkv + h) * maxp;
       int t = 0;
-      for (; t + 4 <= len; t += 4) {
-        uint4 kk[4], vv[4];
+      for (; t + kRpU <= len; t += kRpU) {
+        uint4 kk[kRpU], vv[kRpU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kRpU; ++u) {
           const size_t src = (((size_t)b * S + st + t + u) * Hkv + h) * kD + c * EPC;
           kk[u] = __ldg(reinterpret_cast<const uint4*>(K + src));
           vv[u] = __ldg(reinterpret_cast<const uint4*>(V + src));
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kRpU; ++u) {
           const int tt = t + u;
           const size_t dst = ((page_base + p0 + tt / P) * P + tt % P) * kD + c * EPC;
           *reinterpret_cast<uint4*>(Kp + dst) = kk[u];
@@ -465,7 +470,19 @@ cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const 
                                  const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
                                  int maxb, int maxp, int P, int mean_mode, void* Kp, void* Vp, void* dig,
                                  cudaStream_t st) {
-  const int ctas = max(1, min(maxb, num_sms() * 8 / max(1, B)));
+  // exactly one resident wave (CTAs stride over the blocks): a grid past the
+  // occupancy leaves a lone partial second wave
+  static int occ[2] = {0, 0};
+  int& oc = occ[dtype == 0 ? 0 : 1];
+  if (!oc) {
+    cudaError_t e = dtype == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_repack_digest<bf16>, 128, 0)
+                               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_repack_digest<float>, 128, 0);
+    if (e != cudaSuccess || oc < 1) {
+      cudaGetLastError();
+      oc = 4;
+    }
+  }
+  const int ctas = max(1, min(maxb, num_sms() * oc / max(1, B)));
   dim3 grid(ctas, B);
   if (dtype == 0)
     k_repack_digest<bf16><<<grid, 128, 0, st>>>(
