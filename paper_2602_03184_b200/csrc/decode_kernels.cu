@@ -9,6 +9,7 @@
 #include "kernels.h"
 
 #include <math_constants.h>
+#include <stdlib.h>
 
 namespace dsk {
 
@@ -252,7 +253,124 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
   sstamp(2);
 }
 
+// Test hook: 1 forces the CUDA-core k_score_blocks for bf16 too (parity of the
+// two a5 kernels); initial value from DYNSPLIT_A5_CUDA_CORE.
+static bool g_score_cuda_core = getenv("DYNSPLIT_A5_CUDA_CORE") != nullptr;
+
+// ============================================================================
+// a5 on the tensor cores (bf16 digests, min/max mode).  The block score is a
+// 256-long dot product:  sum_j max(q_j kmax_j, q_j kmin_j)
+//   = sum_j max(q_j, 0) kmax_j + sum_j min(q_j, 0) kmin_j            (kmax >= kmin)
+//   = A_h . B_blk,  A_h = [q+ | q-] (bf16, exact),  B_blk = [kmax | kmin]
+// i.e. exactly the digest row.  One m16n8k16 tile = G (<= 8) heads x 8 blocks
+// x 16 dims; 16 k-steps per 8 blocks (bf16 x bf16 products exact, fp32
+// accumulation in a fixed k order: a block's score does not depend on the CTA,
+// so sequence-split ranks still agree).  The per-block half-warp dot products
+// of k_score_blocks issue ~10x more instructions; this is the same HBM read.
+// grid / staging as k_score_blocks, but the CTA's digest rows are staged with
+// 16-byte cp.async into rows padded to 528 B (conflict-free ldmatrix) before
+// the PDL wait (one 512-byte TMA bulk copy per row measured slower: small-copy
+// issue rate); a range longer than the stage is processed in rounds.
+// ============================================================================
+constexpr int kTcDigRow = 2 * kD * 2 + 16;  // padded smem row (bytes)
+
+template <int G>
+__global__ void __launch_bounds__(512, 1) k_score_blocks_tc(const bf16* __restrict__ q,
+                                                            const bf16* __restrict__ dig,
+                                                            const int32_t* __restrict__ n_blocks,
+                                                            float* __restrict__ scores, int Hq, int Hkv,
+                                                            int maxb, int cap) {
+  static_assert(G >= 1 && G <= 8, "G heads per KV head <= 8 (A rows 0..7)");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int hk = blockIdx.y, b = blockIdx.z;
+  const int nb = n_blocks[b];
+  const int per = (nb + gridDim.x - 1) / gridDim.x;
+  const int lo = blockIdx.x * per;
+  const int hi = min(nb, lo + per);
+  const int n = max(hi - lo, 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  sstamp(0);
+  const unsigned char* dbase = reinterpret_cast<const unsigned char*>(dig + ((size_t)b * Hkv + hk) * (size_t)maxb * 2 * kD);
+  float* sbase = scores + ((size_t)b * Hq + hk * G) * maxb;
+  constexpr int kRowB = 2 * kD * 2;  // digest row bytes in HBM
+  auto stage = [&](int r0, int cnt) {  // rows lo + r0 .. + cnt -> padded smem rows 0 .. cnt
+    for (int c = threadIdx.x; c < cnt * 32; c += blockDim.x) {
+      const int r = c >> 5, k = c & 31;
+      cp_async16_cg(smem + (size_t)r * kTcDigRow + k * 16, dbase + (size_t)(lo + r0 + r) * kRowB + k * 16);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int first = min(n, cap);
+  stage(0, first);  // resident data: overlaps the preceding kernel under PDL
+  pdl_trigger();
+  pdl_wait();
+  sstamp(1);
+  // A fragments of lane (g = lane / 4, t = lane % 4): head g's [q+ | q-] at
+  // k = 16 ks + 2t (+1) and 16 ks + 2t + 8 (+9); heads >= G are zero rows
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t a0[16], a2[16];
+  {
+    uint32_t w0[8], w2[8];  // q_g[16 i + 2t .. +1], q_g[16 i + 2t + 8 .. +9], i < 8
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w0[i] = w2[i] = 0u;
+    if (g < G) {
+      const uint32_t* qg = reinterpret_cast<const uint32_t*>(q + ((size_t)b * Hq + hk * G + g) * kD);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        w0[i] = qg[8 * i + t];
+        w2[i] = qg[8 * i + t + 4];
+      }
+    }
+    const __nv_bfloat162 z2 = __floats2bfloat162_rn(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const __nv_bfloat162 x0 = *reinterpret_cast<const __nv_bfloat162*>(&w0[i]);
+      const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&w2[i]);
+      const __nv_bfloat162 p0 = __hmax2(x0, z2), p2 = __hmax2(x2, z2);  // q+ (exact)
+      const __nv_bfloat162 m0 = __hmin2(x0, z2), m2 = __hmin2(x2, z2);  // q- (exact)
+      a0[i] = *reinterpret_cast<const uint32_t*>(&p0);
+      a2[i] = *reinterpret_cast<const uint32_t*>(&p2);
+      a0[8 + i] = *reinterpret_cast<const uint32_t*>(&m0);
+      a2[8 + i] = *reinterpret_cast<const uint32_t*>(&m2);
+    }
+  }
+  // ldmatrix.x4 lane address: matrix l / 8 = dims 8 (l / 8) .. +7 of the row (l % 8)
+  const uint32_t s0 = smem_u32(smem) + (uint32_t)((lane & 7) * kTcDigRow + (lane >> 3) * 16);
+  for (int r0 = 0; r0 < n; r0 += cap) {
+    const int cnt = min(cap, n - r0);
+    if (r0) {
+      __syncthreads();  // the previous round's rows are consumed
+      stage(r0, cnt);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (r0 == 0) sstamp(3);
+    for (int grp = warp; grp * 8 < cnt; grp += 16) {
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint32_t rb = s0 + (uint32_t)(grp * 8 * kTcDigRow);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {  // two k-steps (32 dims) per ldmatrix.x4
+        uint32_t bk[4];
+        ldsm_x4(bk, rb + kk * 64);
+        mma_rows8(c, a0[2 * kk], a2[2 * kk], bk[0], bk[1]);
+        mma_rows8(c, a0[2 * kk + 1], a2[2 * kk + 1], bk[2], bk[3]);
+      }
+      // c0, c1: head g, blocks grp * 8 + 2t, + 1 (rows 8..15 are zero)
+      const int i0 = r0 + grp * 8 + 2 * t;
+      if (g < G) {
+        if (i0 < n) sbase[(size_t)g * maxb + lo + i0] = c[0];
+        if (i0 + 1 < n) sbase[(size_t)g * maxb + lo + i0 + 1] = c[1];
+      }
+    }
+  }
+  sstamp(2);
+}
+
 }  // namespace dsk
+extern "C" int dynsplit_debug_a5_cuda_core(int on) {
+  dsk::g_score_cuda_core = on != 0;
+  return 0;
+}
 extern "C" int dynsplit_debug_score_timer(void* dev_ptr) {
   return (int)cudaMemcpyToSymbol(dsk::g_score_dbg, &dev_ptr, sizeof(void*));
 }
@@ -308,6 +426,34 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
   const int cap = min((maxb + chunks - 1) / chunks, cap_max);
   const size_t smem = (size_t)cap * rb;
   dim3 grid(chunks, Hkv, B);
+  if constexpr (sizeof(T) == 2) {
+    if (!mean_mode && G <= 8 && !g_score_cuda_core) {
+      // tensor-core path: rows padded to kTcDigRow, whole 8-block groups
+      const int cap_tc = max(8, min((maxb + chunks - 1) / chunks, (200 * 1024) / kTcDigRow) & ~7);
+      const size_t smem_tc = (size_t)(cap_tc + 8) * kTcDigRow;
+      const bf16* qq = static_cast<const bf16*>(q);
+      const bf16* dd = static_cast<const bf16*>(dig);
+#define DSK_SCT(GG)                                                                                  \
+  {                                                                                                  \
+    static bool attr = false;                                                                        \
+    if (!attr) {                                                                                     \
+      allow_max_dyn_smem(k_score_blocks_tc<GG>);                                                     \
+      attr = true;                                                                                   \
+    }                                                                                                \
+    launch_ex(k_score_blocks_tc<GG>, grid, 512, smem_tc, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb,     \
+              cap_tc);                                                                               \
+    return post_launch("k_score_blocks_tc", st);                                                     \
+  }
+      switch (G) {
+        case 1: DSK_SCT(1)
+        case 2: DSK_SCT(2)
+        case 4: DSK_SCT(4)
+        case 8: DSK_SCT(8)
+        default: break;
+      }
+#undef DSK_SCT
+    }
+  }
   const T* qq = static_cast<const T*>(q);
   const T* dd = static_cast<const T*>(dig);
 #define DSK_SC(GG)                                                                                   \

@@ -21,11 +21,20 @@ def gamma(n: int) -> float:
 def score_error_bound(qh, kmax_h, kmin_h, exact_products: bool) -> np.ndarray:
     """|fp32 block score - exact| <= gamma_n * sum_j |q_j| max(|kmax_j|, |kmin_j|)
     for ANY summation order (products of bf16 values are exact in fp32;
-    fp32 inputs add one rounding per product)."""
+    fp32 inputs add one rounding per product).
+
+    bf16 (exact products) is summed on the tensor cores as the 2d-term dot
+    [q+ | q-] . [kmax | kmin] (DESIGN R22): their fp32 accumulation is not
+    specified as round-to-nearest, so the bound takes n = 2d additions with
+    unit roundoff 2^-23 (one truncation per addition); it also covers the
+    CUDA-core kernel's d-term round-to-nearest sum."""
     d = qh.shape[-1]
     mag = (np.abs(qh.astype(np.float64)) *
            np.maximum(np.abs(kmax_h.astype(np.float64)), np.abs(kmin_h.astype(np.float64)))).sum(-1)
-    return gamma(d + (0 if exact_products else 1)) * mag
+    if exact_products:
+        n, u = 2 * d, 2.0 ** -23
+        return n * u / (1 - n * u) * mag
+    return gamma(d + 1) * mag
 
 
 def marginal_rank(scores, starts, budget):

@@ -219,6 +219,55 @@ def test_select_regime_B_certified(D, dtype, S, Hq, Hkv, budget):
     _check_selection(layer, sel, res, B, Hq)
 
 
+@pytest.mark.parametrize("S,Hq,Hkv,budget,integer", [(8192, 32, 8, 1024, False), (3000, 16, 2, 300, True),
+                                                      (5000, 8, 8, 640, False), (2500, 64, 8, 200, True)])
+def test_score_kernels_agree(D, S, Hq, Hkv, budget, integer):
+    """a5 on the tensor cores (k_score_blocks_tc, the bf16 default) and the
+    CUDA-core half-warp kernel (test hook): both within the score bound of the
+    oracle (exactly equal to it for integer q, K), and the same selection."""
+    import ctypes
+    B, d = 2, 128
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(1900 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    gen = G.decode_qkv_integer if integer else G.decode_qkv
+    qs, Ks, Vs = zip(*[gen(1910 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    if not integer:
+        q = H.certify_queries(1910, q, K, starts, budget, "bf16")
+    layer = _build(D, toks, K, V, cfg, "bf16", Hq)
+    lib = D.lib()
+    lib.dynsplit_debug_a5_cuda_core.argtypes = [ctypes.c_int]
+    sels = []
+    try:
+        for cc in (0, 1):
+            lib.dynsplit_debug_a5_cuda_core(cc)
+            sels.append(D.select(t(q, torch.bfloat16), layer, budget))
+            torch.cuda.synchronize()
+    finally:
+        lib.dynsplit_debug_a5_cuda_core(0)
+    res = H.oracle_decode(q, K, V, starts, budget)
+    for sel in sels:
+        sc = sel.scores.cpu().numpy()
+        for b in range(B):
+            nb = len(starts[b]) - 1
+            kmax, kmin = O.digests(K[b], starts[b])
+            for h in range(Hq):
+                if integer:
+                    assert np.array_equal(sc[b, h, :nb].astype(np.float64), res[b]["scores"][h])
+                else:
+                    eps = H.score_error_bound(q[b, h], kmax[h // (Hq // Hkv)], kmin[h // (Hq // Hkv)], True)
+                    assert np.all(np.abs(sc[b, h, :nb] - res[b]["scores"][h]) <= eps + 1e-30)
+        _check_selection(layer, sel, res, B, Hq)
+    for name in ("n_sel", "marginal_block", "marginal_keep"):
+        assert torch.equal(getattr(sels[0], name), getattr(sels[1], name)), name
+    ns = sels[0].n_sel.cpu().numpy()
+    s0, s1 = sels[0].sel_blocks.cpu().numpy(), sels[1].sel_blocks.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            assert np.array_equal(s0[b, h, :ns[b, h]], s1[b, h, :ns[b, h]]), (b, h)
+
+
 # ---------------------------------------------------------------- a7 + a8 attention
 def _check_attention(o, lse, res, B, Hq):
     o = o.cpu().numpy()
