@@ -429,10 +429,16 @@ def main():
         rows = np.arange(S_pf, dtype=np.float64) + 1
         flop = 2.0 * d * Hq * rows.sum()
         exps = Hq * rows.sum()
-        prefill = {"row": "a1 k_lse_band + k_score_reduce", "seq_len": S_pf, "heads_q": Hq, "heads_kv": Hkv,
+        try:
+            tf_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"])
+            tf_src = "MEASURED_PEAKS.json bf16_tflops_sustained"
+        except Exception:
+            tf_peak, tf_src = 1395.5, "fallback (B200_PROFILING.md sustained bf16)"
+        prefill = {"row": "a1 k_lse_band_tc + k_score_reduce", "seq_len": S_pf, "heads_q": Hq, "heads_kv": Hkv,
                    "ms": pf_ms, "tflops": flop / (pf_ms * 1e-3) / 1e12,
-                   "tflops_peak": 1395.5, "exp_per_s": exps / (pf_ms * 1e-3),
-                   "note": "tcgen05 (UMMA 128x128x16, TMEM) + MUFU ex2; peak = MEASURED_PEAKS bf16 sustained"}
+                   "tflops_peak": tf_peak, "tflops_frac": flop / (pf_ms * 1e-3) / 1e12 / tf_peak,
+                   "exp_per_s": exps / (pf_ms * 1e-3),
+                   "note": "tcgen05 (UMMA 128x128x16, TMEM) + MUFU ex2; peak = " + tf_src}
         del Qs, Ks
 
     # ---- dense baseline (row a9): every page, every head
@@ -519,7 +525,7 @@ def main():
                          "step_frac_of_peak": (step_bytes / (step_ms * 1e-3) / 1e9) / peak},
             "e2e": {"value": all_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "gpu_launches": 3 * L * args.steps,   # k_score_blocks, k_select_reg, k_decode_attn per layer
+            "gpu_launches": 3 * L * args.steps,   # k_score_blocks_tc, k_select_reg, k_decode_attn per layer
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
