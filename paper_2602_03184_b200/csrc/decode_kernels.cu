@@ -8,6 +8,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math_constants.h>
 #include <stdlib.h>
 
@@ -267,41 +269,63 @@ static bool g_score_cuda_core = getenv("DYNSPLIT_A5_CUDA_CORE") != nullptr;
 // accumulation in a fixed k order: a block's score does not depend on the CTA,
 // so sequence-split ranks still agree).  The per-block half-warp dot products
 // of k_score_blocks issue ~10x more instructions; this is the same HBM read.
-// grid / staging as k_score_blocks, but the CTA's digest rows are staged with
-// 16-byte cp.async into rows padded to 528 B (conflict-free ldmatrix) before
-// the PDL wait (one 512-byte TMA bulk copy per row measured slower: small-copy
-// issue rate); a range longer than the stage is processed in rounds.
+// Staging (before the PDL wait, under the preceding kernel): TMA tensor copies
+// of 64-dim x 32-row boxes with the 128-byte hardware swizzle into four
+// 64-dim slabs, so the ldmatrix row reads are conflict-free; a CTA's range is
+// a multiple of 32 rows (whole boxes).  A range longer than the stage is
+// processed in rounds.
 // ============================================================================
-constexpr int kTcDigRow = 2 * kD * 2 + 16;  // padded smem row (bytes)
+constexpr int kA5BoxRows = 32;  // rows per TMA box
+constexpr int kA5SlabRowB = 128;  // bytes per row of one 64-dim slab
+
+DSK_DEVICE void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 
 template <int G>
-__global__ void __launch_bounds__(512, 1) k_score_blocks_tc(const bf16* __restrict__ q,
-                                                            const bf16* __restrict__ dig,
+__global__ void __launch_bounds__(512, 1) k_score_blocks_tc(const __grid_constant__ CUtensorMap tmD,
+                                                            const bf16* __restrict__ q,
                                                             const int32_t* __restrict__ n_blocks,
                                                             float* __restrict__ scores, int Hq, int Hkv,
                                                             int maxb, int cap) {
   static_assert(G >= 1 && G <= 8, "G heads per KV head <= 8 (A rows 0..7)");
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  // 1024-byte aligned slabs (the swizzle atoms are address-based)
+  const uint32_t raw_s = smem_u32(smem_raw);
+  unsigned char* smem = smem_raw + (((raw_s + 1023u) & ~1023u) - raw_s);
+  const size_t slab = (size_t)cap * kA5SlabRowB;  // one 64-dim slab of `cap` rows
   const int hk = blockIdx.y, b = blockIdx.z;
   const int nb = n_blocks[b];
-  const int per = (nb + gridDim.x - 1) / gridDim.x;
+  const int per = (((nb + gridDim.x - 1) / gridDim.x) + kA5BoxRows - 1) & ~(kA5BoxRows - 1);
   const int lo = blockIdx.x * per;
   const int hi = min(nb, lo + per);
   const int n = max(hi - lo, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   sstamp(0);
-  const unsigned char* dbase = reinterpret_cast<const unsigned char*>(dig + ((size_t)b * Hkv + hk) * (size_t)maxb * 2 * kD);
+  const int row0 = (b * Hkv + hk) * maxb + lo;  // tensor-map row of this CTA's first block
   float* sbase = scores + ((size_t)b * Hq + hk * G) * maxb;
-  constexpr int kRowB = 2 * kD * 2;  // digest row bytes in HBM
-  auto stage = [&](int r0, int cnt) {  // rows lo + r0 .. + cnt -> padded smem rows 0 .. cnt
-    for (int c = threadIdx.x; c < cnt * 32; c += blockDim.x) {
-      const int r = c >> 5, k = c & 31;
-      cp_async16_cg(smem + (size_t)r * kTcDigRow + k * 16, dbase + (size_t)(lo + r0 + r) * kRowB + k * 16);
+  auto stage = [&](int r0, int cnt) {  // rows r0 .. r0 + cnt of the range -> smem rows 0 ..
+    if (threadIdx.x == 0) {
+      const int nbox = (cnt + kA5BoxRows - 1) / kA5BoxRows;
+      mbar_arrive_expect_tx(&bar, (uint32_t)(nbox * 4 * kA5BoxRows * kA5SlabRowB));
+      for (int j = 0; j < nbox; ++j)
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl)
+          tma_load_2d(smem + sl * slab + (size_t)j * kA5BoxRows * kA5SlabRowB, &tmD, sl * 64,
+                      row0 + r0 + j * kA5BoxRows, &bar);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
   const int first = min(n, cap);
-  stage(0, first);  // resident data: overlaps the preceding kernel under PDL
+  if (first > 0) stage(0, first);  // resident data: overlaps the preceding kernel under PDL
   pdl_trigger();
   pdl_wait();
   sstamp(1);
@@ -334,24 +358,30 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks_tc(const bf16* __restri
       a2[8 + i] = *reinterpret_cast<const uint32_t*>(&m2);
     }
   }
-  // ldmatrix.x4 lane address: matrix l / 8 = dims 8 (l / 8) .. +7 of the row (l % 8)
-  const uint32_t s0 = smem_u32(smem) + (uint32_t)((lane & 7) * kTcDigRow + (lane >> 3) * 16);
-  for (int r0 = 0; r0 < n; r0 += cap) {
+  __syncthreads();  // the barrier's initialisation is visible to every warp
+  // ldmatrix.x4: lane l addresses row (l % 8) of the 8-block group, 16-byte
+  // chunk (l / 8) of the 32-dim window (kk); slab = kk / 2, chunk in slab =
+  // 4 (kk % 2) + l / 8, swizzled with the row within its 8-row atom
+  const int lr = lane & 7, lc = lane >> 3;
+  const uint32_t sbase_u = smem_u32(smem);
+  uint32_t phase = 0;
+  for (int r0 = 0; r0 < n; r0 += cap, phase ^= 1u) {
     const int cnt = min(cap, n - r0);
     if (r0) {
       __syncthreads();  // the previous round's rows are consumed
       stage(r0, cnt);
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
+    mbar_wait(&bar, phase);
     if (r0 == 0) sstamp(3);
     for (int grp = warp; grp * 8 < cnt; grp += 16) {
       float c[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t rb = s0 + (uint32_t)(grp * 8 * kTcDigRow);
+      const int r = grp * 8 + lr;
+      const uint32_t rowa = sbase_u + (uint32_t)(r * kA5SlabRowB);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {  // two k-steps (32 dims) per ldmatrix.x4
+        const uint32_t chunk = (uint32_t)((((kk & 1) << 2) | lc) ^ (r & 7));
         uint32_t bk[4];
-        ldsm_x4(bk, rb + kk * 64);
+        ldsm_x4(bk, rowa + (uint32_t)((kk >> 1) * slab) + (chunk << 4));
         mma_rows8(c, a0[2 * kk], a2[2 * kk], bk[0], bk[1]);
         mma_rows8(c, a0[2 * kk + 1], a2[2 * kk + 1], bk[2], bk[3]);
       }
@@ -428,11 +458,30 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
   dim3 grid(chunks, Hkv, B);
   if constexpr (sizeof(T) == 2) {
     if (!mean_mode && G <= 8 && !g_score_cuda_core) {
-      // tensor-core path: rows padded to kTcDigRow, whole 8-block groups
-      const int cap_tc = max(8, min((maxb + chunks - 1) / chunks, (200 * 1024) / kTcDigRow) & ~7);
-      const size_t smem_tc = (size_t)(cap_tc + 8) * kTcDigRow;
+      // tensor-core path: whole 32-row TMA boxes per CTA (device: per rounded up to 32)
+      static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+      if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess || !fn)
+          return cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      }
+      const int rows_hint = (min(nb_hint, maxb) + chunks - 1) / chunks;
+      const int cap_tc = min(((rows_hint + kA5BoxRows - 1) / kA5BoxRows) * kA5BoxRows, 384);
+      const size_t smem_tc = (size_t)cap_tc * 4 * kA5SlabRowB + 1024;
+      // digests [B * Hkv * maxb rows][256] bf16 -> boxes of 64 dims x 32 rows, 128-byte swizzle
+      CUtensorMap tm;
+      const cuuint64_t dims[2] = {(cuuint64_t)2 * kD, (cuuint64_t)B * Hkv * maxb};
+      const cuuint64_t strides[1] = {(cuuint64_t)2 * kD * 2};
+      const cuuint32_t box[2] = {64, (cuuint32_t)kA5BoxRows};
+      const cuuint32_t es[2] = {1, 1};
+      if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(dig), dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
       const bf16* qq = static_cast<const bf16*>(q);
-      const bf16* dd = static_cast<const bf16*>(dig);
 #define DSK_SCT(GG)                                                                                  \
   {                                                                                                  \
     static bool attr = false;                                                                        \
@@ -440,7 +489,7 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
       allow_max_dyn_smem(k_score_blocks_tc<GG>);                                                     \
       attr = true;                                                                                   \
     }                                                                                                \
-    launch_ex(k_score_blocks_tc<GG>, grid, 512, smem_tc, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb,     \
+    launch_ex(k_score_blocks_tc<GG>, grid, 512, smem_tc, st, 1, tm, qq, nb, scores, Hq, Hkv, maxb,    \
               cap_tc);                                                                               \
     return post_launch("k_score_blocks_tc", st);                                                     \
   }
