@@ -268,6 +268,50 @@ def test_score_kernels_agree(D, S, Hq, Hkv, budget, integer):
             assert np.array_equal(s0[b, h, :ns[b, h]], s1[b, h, :ns[b, h]]), (b, h)
 
 
+@pytest.mark.parametrize("cuda_core", [0, 1])
+def test_short_blocks_score_rounds(D, cuda_core):
+    """A plan of minimum-length blocks (C - Delta = 18 tokens everywhere, the
+    shortest DD-Select can emit) has more blocks than the launchers expect
+    (1.25 S / C): the tensor-core a5 runs its staging rounds, the CUDA-core a5
+    its beyond-the-stage global loads.  Integer q, K: scores exact; selection
+    and attention against the oracle on the same plan."""
+    import ctypes
+    B, S, Hq, Hkv, d, budget = 2, 20000, 32, 8, 128, 1500
+    cfg = D.default_config()
+    L = cfg.C - cfg.delta
+    starts = list(range(0, S, L)) + [S]
+    assert len(starts) - 1 > 1.25 * S / cfg.C
+    qs, Ks, Vs = zip(*[G.decode_qkv_integer(1950 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    toks = np.stack([G.tokens(1960 + b, S) for b in range(B)])
+    base = _build(D, toks, K, V, cfg, "bf16", Hq)          # shapes, w10
+    mb = D.max_blocks(S, cfg)
+    bs = torch.full((B, mb + 1), S, dtype=torch.int32)
+    bs[:, : len(starts)] = torch.tensor(starts, dtype=torch.int32)
+    bs = bs.cuda()
+    nb = torch.full((B,), len(starts) - 1, dtype=torch.int32, device="cuda")
+    pf, pb, pv, npg = D.map_pages(bs, nb, S, cfg)
+    Kp, Vp, dig = D.repack_digest(t(K, torch.bfloat16), t(V, torch.bfloat16), bs, nb, pf, cfg)
+    layer = D.PagedLayer(base.shape, cfg, base.w10, bs, nb, pf, pb, pv, npg, Kp, Vp, dig)
+    lib = D.lib()
+    lib.dynsplit_debug_a5_cuda_core.argtypes = [ctypes.c_int]
+    try:
+        lib.dynsplit_debug_a5_cuda_core(cuda_core)
+        qt = t(q, torch.bfloat16)
+        sel = D.select(qt, layer, budget)
+        o, lse = D.decode_attn(qt, layer, sel.worklist)
+        torch.cuda.synchronize()
+    finally:
+        lib.dynsplit_debug_a5_cuda_core(0)
+    res = H.oracle_decode(q, K, V, [starts] * B, budget)
+    sc = sel.scores.cpu().numpy()
+    for b in range(B):
+        for h in range(Hq):
+            assert np.array_equal(sc[b, h, : len(starts) - 1].astype(np.float64), res[b]["scores"][h]), (b, h)
+    _check_selection(layer, sel, res, B, Hq)
+    _check_attention(o, lse, res, B, Hq)
+
+
 # ---------------------------------------------------------------- a7 + a8 attention
 def _check_attention(o, lse, res, B, Hq):
     o = o.cpu().numpy()
