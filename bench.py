@@ -321,6 +321,13 @@ def main():
     with torch.cuda.graph(g_sel_all):
         for l in range(L):
             sel_layer(l)
+    # a5 alone (block scores into the select workspace), for the a5 / a6 split
+    mb_ = D.max_blocks(S, cfg)
+    score_buf = torch.empty(B, Hq, mb_, dtype=torch.float32, device=dev)
+    g_score_all = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_score_all):
+        for l in range(L):
+            D.score_blocks(qs[l], layers[l], out=score_buf)
     with torch.cuda.graph(g_attn_all):
         for l in range(L):
             attn_layer(l)
@@ -352,7 +359,7 @@ def main():
 
     # ---- timed region 2: the step's kernel groups, each as an L-layer graph
     barrier()
-    t0, t1, t2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    t0, t1, t2, t3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
     t0.record(cur)
     for _ in range(args.steps):
         g_sel_all.replay()
@@ -360,9 +367,13 @@ def main():
     for _ in range(args.steps):
         g_attn_all.replay()
     t2.record(cur)
+    for _ in range(args.steps):
+        g_score_all.replay()
+    t3.record(cur)
     barrier()
     sel_ms = t0.elapsed_time(t1) / (args.steps * L)
     attn_ms = t1.elapsed_time(t2) / (args.steps * L)
+    score_ms = t2.elapsed_time(t3) / (args.steps * L)
     split_step_ms = t0.elapsed_time(t2) / args.steps
 
     # ---- e2e: the step's inputs from pinned HOST memory (every layer's q, one
@@ -460,13 +471,13 @@ def main():
         dense_ms = ev0.elapsed_time(ev1) / nd
 
     # ---- max over ranks
-    vals = torch.tensor([step_ms, attn_ms, sel_ms, e2e_ms, split_step_ms, dense_ms or 0.0],
+    vals = torch.tensor([step_ms, attn_ms, sel_ms, e2e_ms, split_step_ms, dense_ms or 0.0, score_ms],
                         dtype=torch.float64, device=dev)
     tot_bytes = torch.tensor([float(step_bytes)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot_bytes, op=dist.ReduceOp.SUM)
-    step_ms, attn_ms, sel_ms, e2e_ms, split_step_ms, dense_ms_v = vals.tolist()
+    step_ms, attn_ms, sel_ms, e2e_ms, split_step_ms, dense_ms_v, score_ms = vals.tolist()
     all_bytes = tot_bytes.item()
 
     cpu = None
@@ -521,6 +532,8 @@ def main():
                          "timing": "CUDA events around an L-layer graph of the kernel's launches (back to back, "
                                    "PDL-chained), per launch",
                          "select_us_per_layer": sel_ms * 1e3,
+                         "score_us_per_layer": score_ms * 1e3,
+                         "score_frac_of_peak": score_bytes_per_launch / (score_ms * 1e-3) / 1e9 / peak,
                          "select_bytes_per_launch": score_bytes_per_launch,
                          "step_frac_of_peak": (step_bytes / (step_ms * 1e-3) / 1e9) / peak},
             "e2e": {"value": all_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
