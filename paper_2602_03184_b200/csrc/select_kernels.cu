@@ -423,11 +423,12 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
 //  * a boundary bucket with <= 32 candidates is resolved by one warp ranking
 //    them with shuffles (no sort); larger ones narrow the bucket and repeat;
 //  * each head's selection is published as a bitmask (one ballot word per 32
-//    blocks); the cluster exchanges the G bitmasks once through DSMEM, then
+//    blocks) pushed into every peer's smem by DSMEM stores before one cluster
+//    barrier (no remote reads), then
 //    every CTA computes the union page counts for all blocks (16 contiguous
 //    blocks per thread, one block-wide scan) and writes 1/G of the worklist;
 //    sel_blocks positions are popcount prefixes of the head's own bitmask;
-//  * split cluster barriers (arrive early, wait late).
+//  * one split cluster barrier (arrive after the pushes, wait before the union).
 // ============================================================================
 constexpr int kRK = 16;
 constexpr int kRMax = kSelNT * kRK;  // 8192 blocks
@@ -658,19 +659,25 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
   __syncthreads();
   stamp(4);
 
-  // ---- 3. this head's selection bitmask (ballot words), published to the cluster
+  // ---- 3. this head's selection bitmask (ballot words), pushed into every
+  //         peer's smem slot c (DSMEM stores) together with (marginal, keep,
+  //         key, all_fit): after the cluster barrier each CTA holds all G
+  //         selections locally (no remote reads, no second barrier)
   const int m_c = s_info[0], keep_c = s_info[1], all_c = s_info[3];
   const uint32_t T_c = (uint32_t)s_info[2];
+  // lane g of each warp stores the words into CTA g's copy (g == c: local)
+  uint32_t* const my_peer_bits = cluster.map_shared_rank(&sbits[c][0], lane < G ? lane : c);
 #pragma unroll
   for (int k = 0; k < kRK; ++k) {
     const int i = k * kSelNT + tid;
     const uint32_t k0 = skey0[i];
     const bool sel = i < nb && (all_c || k0 > T_c || (k0 == T_c && i <= m_c));
     const uint32_t word = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0) sbits[c][k * kSelW + warp] = word;
+    if (lane < G) my_peer_bits[k * kSelW + warp] = word;
   }
+  if (tid < G * 4) cluster.map_shared_rank(&s_pinfo[c][0], tid / 4)[tid % 4] = s_info[tid % 4];
   __syncthreads();
-  cluster_arrive_rel();  // s_info and sbits[c] are visible to the peers
+  cluster_arrive_rel();  // this CTA's pushes are released to the peers
   stamp(5);
 
   // ---- 4. sel_blocks of this head (ascending): popcount prefix over its words
@@ -696,16 +703,9 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
     }
   }
 
-  // ---- 5. the peers' selections (DSMEM), then the union worklist
-  cluster_wait_acq();
+  // ---- 5. every head's selection is in this CTA's smem; the union worklist
+  cluster_wait_acq();  // the peers' pushes have landed
   stamp(6);
-  for (int j = tid; j < G * kRW; j += kSelNT) {
-    const int g = j / kRW, w = j % kRW;
-    if (g != c) sbits[g][w] = cluster.map_shared_rank(&sbits[g][0], g)[w];
-  }
-  if (tid < G * 4) s_pinfo[tid / 4][tid % 4] = cluster.map_shared_rank(s_info, tid / 4)[tid % 4];
-  __syncthreads();
-  cluster_arrive_rel();  // done reading the peers' shared memory
   int mg[G], kg[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -779,7 +779,6 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
     wl_count[(size_t)b * Hkv + hk] = wpre.y;
   }
   stamp(8);
-  cluster_wait_acq();  // peers may still be reading this CTA's s_info / sbits
   stamp(9);
 }
 
