@@ -333,6 +333,10 @@ def _check_attention(o, lse, res, B, Hq):
     ("bf16", 4000, 64, 8, 333, 0.5),       # g = 8
     ("bf16", 2000, 8, 4, 5000, 0.0),       # budget >= S -> dense
     ("bf16", 2000, 8, 4, 1, 0.0),          # budget 1
+    ("bf16", 1, 8, 2, 1, 0.0),             # a single token: one block, one page
+    ("bf16", 17, 32, 8, 5, 0.0),           # one partial block
+    ("bf16", 47, 8, 2, 20, 0.0),           # two blocks, ragged page tail
+    ("fp32", 50, 8, 8, 20, 0.0),
 ])
 def test_sparse_decode_parity(D, dtype, S, Hq, Hkv, budget, rho):
     B, d = 2, 128
