@@ -517,11 +517,27 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
   stamp(2);
   // ---- 1. keys of this CTA's head
   uint32_t key[kRK];
+  // weak L1-allocating loads (ld.global.ca): the scores are the preceding
+  // kernel's output, visible after the PDL wait, and no line of them was
+  // cached by this launch before it.  (__ldcg compiled to strong LDG.STRONG.GPU
+  // loads that ptxas issued one after another, ~2 us for the 16.)
+  float sv[kRK];
 #pragma unroll
   for (int k = 0; k < kRK; ++k) {
     const int i = k * kSelNT + tid;
-    key[k] = i < nb ? float_key(__ldcg(sc + i)) : 0u;
+    sv[k] = i < nb ? __ldca(sc + i) : 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < kRK; ++k) {
+    const int i = k * kSelNT + tid;
+    key[k] = i < nb ? float_key(sv[k]) : 0u;
     skey0[i] = key[k];
+#ifdef DSK_DEBUG
+    if (k == 0) {  // debug timeline: latency of the first score load alone
+      if (key[0] == 0x12345678u && g_sel_dbg) g_sel_dbg[0] = 0;
+      stamp(10);
+    }
+#endif
   }
   stamp(3);
 

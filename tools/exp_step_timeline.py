@@ -109,7 +109,7 @@ show("score", sc, ["start", "pdl_wait", "end", "digests_in"])
 se = bufs["select"].view(-1, 16).cpu().numpy().astype(np.float64)
 se = se[se[:, 0] > 0]
 show("select", se, ["start", "plan", "pdl_wait", "keys", "threshold", "bits+arrive", "wait+peers",
-                    "union_scan", "writes", "final_wait"])
+                    "union_scan", "writes", "final_wait", "first_key"])
 at = bufs["attn"].view(-1, 8).cpu().numpy().astype(np.float64)
 at = at[at[:, 0] > 0]
 show("attn", at, ["start", "pdl_wait", "first_page", "consumed", "partial", "merged", "entries+cnt", "issued"])
