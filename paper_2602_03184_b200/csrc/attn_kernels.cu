@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
         const uint32_t pv = (uint32_t)page_valid[(size_t)b * max_pages + e];
         e_r0 = e_r1 = pv * 0x01010101u;
       } else {
-        const int4 en = *reinterpret_cast<const int4*>(wl + (size_t)e * BH + bh);
+        // weak coherent load (not the read-only .nc path): the worklist is the
+        // output of the PDL primary, which may still be running at launch
+        const int4 en = __ldca(reinterpret_cast<const int4*>(wl + (size_t)e * BH + bh));
         e_page = en.x;
         e_r0 = (uint32_t)en.z;
         e_r1 = (uint32_t)en.w;
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
     }
   };
   load_batch(0, n_split);
-  const int cnt = dense ? n_pages[b] : wl_count[bh];
+  const int cnt = dense ? n_pages[b] : __ldca(wl_count + bh);
   // splits actually used by this (b, KV head): at least kMinPagesPerSplit pages each
   const int n_eff = max(1, min(n_split, (cnt + kMinPagesPerSplit - 1) / kMinPagesPerSplit));
   if (split >= n_eff) return;

@@ -36,7 +36,7 @@ template <> struct DigestDot<bf16> {
     uint4 mx, mn;
   };
   static DSK_DEVICE void load_q(const bf16* p, Q& q) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint4 u = __ldca(reinterpret_cast<const uint4*>(p));  // may come from the PDL primary
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks_tc(const __grid_constan
       const uint32_t* qg = reinterpret_cast<const uint32_t*>(q + ((size_t)b * Hq + hk * G + g) * kD);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        w0[i] = qg[8 * i + t];
-        w2[i] = qg[8 * i + t + 4];
+        w0[i] = __ldca(qg + 8 * i + t);  // weak coherent loads: q may come from the PDL primary
+        w2[i] = __ldca(qg + 8 * i + t + 4);
       }
     }
     const __nv_bfloat162 z2 = __floats2bfloat162_rn(0.f, 0.f);

@@ -571,6 +571,68 @@ def test_decode_layer_matches_separate_calls(D, S, Hq, Hkv, budget):
     _check_attention(o1, lse1, res, B, Hq)
 
 
+def test_decode_layers_back_to_back_shared_buffers(D):
+    """Many layers through dynsplit_decode_layer back to back on ONE
+    workspace and ONE worklist buffer (as the e2e step does), PDL-chained,
+    eagerly and as a replayed CUDA graph: every layer equals its isolated,
+    synchronised call bit for bit (no stale worklist / score reads across
+    layers), and the oracle."""
+    B, S, Hq, Hkv, d, L, budget = 2, 12000, 32, 8, 128, 6, 1000
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(1400 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    layers, qs, host = [], [], []
+    for l in range(L):
+        qkv = [G.decode_qkv(1410 + 10 * l + b, S, Hq, Hkv, d) for b in range(B)]
+        q, K, V = (np.stack(x) for x in zip(*qkv))
+        q = H.certify_queries(1410 + 10 * l, q, K, starts, budget, "bf16")
+        layers.append(_build(D, toks, K, V, cfg, "bf16", Hq))
+        qs.append(t(q, torch.bfloat16))
+        host.append((q, K, V))
+    ref = []
+    for l in range(L):                                     # isolated calls
+        o, lse, sel = D.decode_layer(qs[l], layers[l], budget)
+        torch.cuda.synchronize()
+        ref.append((o.clone(), lse.clone(), sel.n_sel.clone()))
+    shape = D._decode_shape(qs[0], layers[0])
+    ws = torch.zeros(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dtype=torch.uint8, device="cuda")
+    _, ns, mg, kp, wl = D._sel_outputs(shape, cfg, budget, qs[0].device, want_blocks=False)
+    outs = [(torch.empty(B, Hq, d, device="cuda"), torch.empty(B, Hq, device="cuda")) for _ in range(L)]
+    nsl = [torch.empty_like(ns) for _ in range(L)]
+
+    def run_all():
+        for l in range(L):
+            D.decode_layer(qs[l], layers[l], budget, out=(nsl[l], mg, kp, wl, outs[l][0], outs[l][1]), ws=ws)
+
+    def check():
+        for l in range(L):
+            assert torch.equal(outs[l][0], ref[l][0]) and torch.equal(outs[l][1], ref[l][1]), l
+            assert torch.equal(nsl[l], ref[l][2]), l
+
+    for _ in range(3):
+        run_all()
+    torch.cuda.synchronize()
+    check()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        run_all()
+    torch.cuda.current_stream().wait_stream(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run_all()
+    for _ in range(4):
+        for o in outs:
+            o[0].fill_(float("nan"))
+        g.replay()
+    torch.cuda.synchronize()
+    check()
+    for l in (0, L - 1):
+        q, K, V = host[l]
+        res = H.oracle_decode(q, K, V, starts, budget)
+        _check_attention(outs[l][0], outs[l][1], res, B, Hq)
+
+
 # ---------------------------------------------------------------- NEXT-2: mean-pooling digests
 @pytest.mark.parametrize("dtype,S,Hq,Hkv,budget", [("bf16", 6000, 32, 8, 900), ("fp32", 3000, 8, 8, 400),
                                                    ("bf16", 4000, 16, 2, 5000)])
