@@ -495,6 +495,10 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
   const float* sc = scores + ((size_t)b * Hq + hk * G + c) * maxb;
 
   stamp(0);
+  // every CTA of the cluster must have started before a peer writes into its
+  // shared memory (phase 3): arrive now, wait just before the pushes (by then
+  // the whole cluster has long arrived, so the wait costs nothing)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   // ---- 0. resident plan (overlaps the preceding kernel under PDL)
   int len[kRK];
   int tsum = 0;
@@ -681,6 +685,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
   //         selections locally (no remote reads, no second barrier)
   const int m_c = s_info[0], keep_c = s_info[1], all_c = s_info[3];
   const uint32_t T_c = (uint32_t)s_info[2];
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // all peers have started
   // lane g of each warp stores the words into CTA g's copy (g == c: local)
   uint32_t* const my_peer_bits = cluster.map_shared_rank(&sbits[c][0], lane < G ? lane : c);
 #pragma unroll
