@@ -11,7 +11,7 @@
 // CTA c of the cluster owns query head hk*G + c:
 //   1. block lengths -> smem (all blocks), total;
 //   2. the head's marginal block, exactly:
-//        - bucket the live scores into 2048 buckets of [min, max] (a monotone
+//        - bucket the live scores into kBkt = 1024 buckets of [min, max] (a monotone
 //          map), length-weighted smem histogram, suffix scan -> the bucket
 //          where the budget is reached;
 //        - if it holds <= 512 blocks: bitonic sort of (key, ~index) and a
@@ -38,7 +38,7 @@ namespace dsk {
 
 constexpr int kSelNT = 512;
 constexpr int kSelW = kSelNT / 32;
-constexpr int kBkt = 2048;
+constexpr int kBkt = 1024;  // histogram buckets (2048: 0.5 % slower step; 512: same as 1024, wider boundary buckets)
 constexpr int kBPT = kBkt / kSelNT;
 constexpr int kCap = 512;
 
