@@ -571,6 +571,29 @@ def test_decode_layer_matches_separate_calls(D, S, Hq, Hkv, budget):
     _check_attention(o1, lse1, res, B, Hq)
 
 
+@pytest.mark.parametrize("B,S,Hq,Hkv,budget", [(8, 3000, 32, 8, 400), (16, 1500, 8, 2, 200)])
+def test_decode_large_batch(D, B, S, Hq, Hkv, budget):
+    """Many sequences per launch: few attention splits per (b, KV head), a5 /
+    a6 grids over B * Hkv, ragged block counts across the batch; through
+    dynsplit_decode_layer, against the oracle."""
+    d = 128
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(1500 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    qs, Ks, Vs = zip(*[G.decode_qkv(1600 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    q = H.certify_queries(1600, q, K, starts, budget, "bf16")
+    layer = _build(D, toks, K, V, cfg, "bf16", Hq)
+    qt = t(q, torch.bfloat16)
+    o, lse, sel_l = D.decode_layer(qt, layer, budget)
+    sel = D.select(qt, layer, budget)
+    torch.cuda.synchronize()
+    res = H.oracle_decode(q, K, V, starts, budget)
+    _check_selection(layer, sel, res, B, Hq)
+    assert torch.equal(sel_l.n_sel, sel.n_sel)
+    _check_attention(o, lse, res, B, Hq)
+
+
 def test_decode_layers_back_to_back_shared_buffers(D):
     """Many layers through dynsplit_decode_layer back to back on ONE
     workspace and ONE worklist buffer (as the e2e step does), PDL-chained,
