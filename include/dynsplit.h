@@ -19,11 +19,32 @@
  *    workspace) return a status BEFORE anything is launched.  A launch failure
  *    returns DYNSPLIT_ERR_CUDA (cudaGetLastError is consumed).
  *  - Workspaces (`ws`) are sized by dynsplit_workspace_bytes(op, ...), must
- *    be 256-byte aligned and zero-filled once before first use (the decode
- *    workspace starts with split-merge counters at a fixed offset, which the
- *    library leaves zeroed after every call).  A workspace may be reused by
+ *    be 256-byte aligned and zero-filled once before first use.  Every
+ *    workspace starts with a 256-byte header whose first int32 is the DEVICE
+ *    ERROR WORD: data-dependent errors that only the kernels can see (a plan
+ *    that does not tile the sequence, S:267 PlanCoverageMismatch; a plan that
+ *    does not end where an append says it does, S:210 PlanMismatch; page or
+ *    selection capacity exceeded) are OR-ed into it as DYNSPLIT_DEVERR_* bits
+ *    and the offending sequence is skipped (its outputs are unspecified, no
+ *    out-of-bounds write happens).  dynsplit_read_device_error() synchronises
+ *    and reads it; dynsplit_clear_device_error() resets it.  The decode
+ *    workspace also holds split-merge counters at a fixed offset, which the
+ *    library leaves zeroed after every call.  A workspace may be reused by
  *    consecutive calls of any shape on the same stream, never concurrently.
- *  - Functions are stateless and thread-safe; every one is graph-capturable.
+ *  - No entry point keeps state between calls.  Launch-time caches (kernel
+ *    attributes, occupancy, SM count) are per device and mutex-protected, so
+ *    the functions are thread-safe and may drive several devices from one
+ *    process; every one is graph-capturable.
+ *  - Ordering (programmatic dependent launch): the decode kernels are
+ *    launched with PDL and read RESIDENT inputs (plan, pages, digests) before
+ *    waiting for the preceding kernel of the stream; inputs that belong to
+ *    the step (q, scores, worklist) are read after the wait.  Every dynsplit
+ *    entry point that writes resident inputs (build, map, repack, append)
+ *    ends with dynsplit_stream_fence(); a caller whose own kernel writes them
+ *    immediately before a decode call must call dynsplit_stream_fence() in
+ *    between.
+ *  - Every entry point opens an NVTX range named after itself (no cost
+ *    without an attached tool).
  *  - Query head h reads KV head h / (Hq/Hkv) (GQA).  head_dim d must be 128.
  *  - Symbol notation follows the paper: W, R, alpha (Alg. 1); C,
  *    Delta, lambda (DD-Select); P = page size of the
@@ -58,8 +79,26 @@ typedef enum {
   DYNSPLIT_OP_SELECT = 3,
   DYNSPLIT_OP_DECODE_ATTN = 4,
   DYNSPLIT_OP_DECODE_LAYER = 5,
-  DYNSPLIT_OP_APPEND = 6
+  DYNSPLIT_OP_APPEND = 6,
+  DYNSPLIT_OP_MAP_PAGES = 7,   /* header only (the device error word) */
+  DYNSPLIT_OP_REPACK = 8       /* header only */
 } dynsplit_op;
+
+/* Bits of the device error word (first int32 of every workspace). */
+enum {
+  DYNSPLIT_DEVERR_PLAN_COVERAGE = 1,   /* block_starts do not tile [0, L): starts not strictly
+                                          increasing, first != 0, last != L, or n_blocks outside
+                                          [1, max_blocks]  (SPEC S:267 PlanCoverageMismatch) */
+  DYNSPLIT_DEVERR_PLAN_MISMATCH = 2,   /* append: the stored plan does not end at L_prev
+                                          (SPEC S:210 PlanMismatch) */
+  DYNSPLIT_DEVERR_PAGE_CAPACITY = 4,   /* the plan needs more pages than the page capacity */
+  DYNSPLIT_DEVERR_SELECT_OVERFLOW = 8, /* a head selected more than max_selected blocks (a plan
+                                          with blocks shorter than C - Delta); sel_blocks clamped */
+  DYNSPLIT_DEVERR_BLOCK_TOO_LONG = 16, /* a block longer than the decode kernels support
+                                          (more than 255 pages) */
+  DYNSPLIT_DEVERR_SYNC_TIMEOUT = 32    /* the fused decode kernel's CTAs of one KV head could not
+                                          all become resident (another kernel held the SMs) */
+};
 
 typedef struct {
   int32_t B;               /* sequences in the batch */
@@ -82,6 +121,10 @@ typedef struct {
   int32_t digest_mode;     /* block compression: 0 = element-wise max/min rows (V2F, the
                               default); 1 = mean pooling (Appendix A.2): the fp32 mean
                               of the block's keys in the same digest slot, scored as q . mean */
+  int32_t page_cap;        /* pages allocated per (sequence, KV head) in Kp/Vp; 0 = the worst-case
+                              bound dynsplit_max_pages() derives from S.  A plan needing more sets
+                              DYNSPLIT_DEVERR_PAGE_CAPACITY.  (The bound is ~1.9x what DD-Select
+                              plans use at C = 32; a caller that knows n_pages can allocate tightly.) */
 } dynsplit_config;
 
 /* Fills the defaults above. */
@@ -90,7 +133,8 @@ void dynsplit_default_config(dynsplit_config* cfg);
 /* Upper bound on blocks of one sequence: floor(S/(C-Delta)) + 1 (every
  * non-final DD-Select chunk has >= C-Delta tokens). */
 int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* cfg);
-/* Upper bound on pages of one sequence: max_blocks + ceil(S/P). */
+/* Page capacity of one (sequence, KV head): cfg->page_cap if > 0, else the
+ * bound max_blocks + ceil(S/P).  Also the row stride (in pages) of Kp/Vp. */
 int32_t dynsplit_max_pages(int32_t S, const dynsplit_config* cfg);
 /* Upper bound on blocks one head selects under `budget` tokens. */
 int32_t dynsplit_max_selected(int32_t budget, int32_t S, const dynsplit_config* cfg);
@@ -108,6 +152,16 @@ const char* dynsplit_version(void);
  * "" if none.  Set DYNSPLIT_DEBUG=1 to synchronise after every launch so that
  * asynchronous faults are attributed to the launcher that caused them. */
 const char* dynsplit_last_error(void);
+
+/* Device error word of a workspace (its first int32, DYNSPLIT_DEVERR_* bits):
+ * synchronises `stream`, then reads it.  Returns -1 if the read fails. */
+int32_t dynsplit_read_device_error(const void* ws, void* stream);
+/* Resets the device error word of `ws` (asynchronous, on `stream`). */
+dynsplit_status dynsplit_clear_device_error(void* ws, void* stream);
+/* Launches an empty kernel WITHOUT programmatic dependent launch: every write
+ * of the preceding work of `stream` is visible to anything launched after it,
+ * including the pre-wait prologues of the PDL-launched decode kernels. */
+dynsplit_status dynsplit_stream_fence(void* stream);
 
 /* ---------------------------------------------------------------------------
  * Prefill, row a1: delimiter importance scoring, Algorithm 1 with
@@ -159,11 +213,16 @@ dynsplit_status dynsplit_segment(const dynsplit_shape* shape, const dynsplit_con
  * page_block[j] = owning block (-1 past n_pages); page_valid[j] =
  * min(P, len_b - P*(j - page_first[b])) (0 past n_pages).
  *   page_first int32 [B, max_blocks+1]; page_block int32 [B, max_pages];
- *   page_valid int16 [B, max_pages]; n_pages int32 [B] */
+ *   page_valid int16 [B, max_pages]; n_pages int32 [B]
+ * The plan must tile [0, S) (else DYNSPLIT_DEVERR_PLAN_COVERAGE, n_pages[b] =
+ * -1, nothing else written for b) and fit the page capacity (else
+ * DYNSPLIT_DEVERR_PAGE_CAPACITY, likewise).  ws: DYNSPLIT_OP_MAP_PAGES
+ * workspace for the device error word, or NULL (errors then only visible as
+ * n_pages[b] = -1). */
 dynsplit_status dynsplit_map_pages(const dynsplit_shape* shape, const dynsplit_config* cfg,
                                    const int32_t* block_starts, const int32_t* n_blocks,
                                    int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                                   int32_t* n_pages, void* stream);
+                                   int32_t* n_pages, void* ws, size_t ws_bytes, void* stream);
 
 /* Prefill, row a4 (part 2): repack one layer's K and V into pages and build the
  * V2F digests (element-wise max and min of each block's keys).
@@ -171,11 +230,15 @@ dynsplit_status dynsplit_map_pages(const dynsplit_shape* shape, const dynsplit_c
  * padding slots are zeroed.
  *   K, V     kv dtype [B, S, Hkv, d] (token-major, as produced by a model)
  *   Kp, Vp   (out) kv dtype [B, Hkv, max_pages, P, d]
- *   digests  (out) kv dtype [B, Hkv, max_blocks, 2, d]  ([..,0,:] = kmax, [..,1,:] = kmin) */
+ *   digests  (out) kv dtype [B, Hkv, max_blocks, 2, d]  ([..,0,:] = kmax, [..,1,:] = kmin)
+ * A sequence whose plan does not tile [0, S) or whose pages exceed the
+ * capacity is skipped and flagged in the device error word of `ws`
+ * (DYNSPLIT_OP_REPACK workspace, or NULL). */
 dynsplit_status dynsplit_repack_digest(const dynsplit_shape* shape, const dynsplit_config* cfg,
                                        const void* K, const void* V, const int32_t* block_starts,
                                        const int32_t* n_blocks, const int32_t* page_first,
-                                       void* Kp, void* Vp, void* digests, void* stream);
+                                       void* Kp, void* Vp, void* digests, void* ws, size_t ws_bytes,
+                                       void* stream);
 
 /* Prefill, rows a1-a4 for one layer's K/V.  static_w10 == NULL: dynamic mode
  * (a1 scoring on Qs/Ks, a2 table, written to w10); else static mode (a host

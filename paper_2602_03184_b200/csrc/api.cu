@@ -7,59 +7,113 @@
 #include "kernels.h"
 
 #include <math.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
+#include <utility>
+
 namespace dsk {
 
-int num_sms() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
-      cudaGetLastError();
-      n = 148;
-    }
-    cached = n;
+// ---------------------------------------------------------------- per-device launch caches
+// One mutex guards every cache; keys include the current device, so a thread
+// driving device 1 never reuses device 0's attributes or occupancy.
+namespace {
+std::mutex g_mu;
+std::map<int, int> g_sms, g_smem;
+std::set<std::pair<const void*, int>> g_prepared;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+
+int device_attr(std::map<int, int>& cache, cudaDeviceAttr attr, int fallback) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fallback;
   }
-  return cached;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, attr, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = fallback;
+  }
+  cache[dev] = n;
+  return n;
+}
+}  // namespace
+
+int num_sms() { return device_attr(g_sms, cudaDevAttrMultiProcessorCount, 148); }
+int max_smem_optin() { return device_attr(g_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 227 * 1024); }
+
+void prepare_kernel(const void* kern) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int optin = max_smem_optin();
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_prepared.insert({kern, dev}).second) return;
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, kern) == cudaSuccess)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaGetLastError();
 }
 
-int max_smem_optin() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
-        n <= 0) {
-      cudaGetLastError();
-      n = 227 * 1024;
-    }
-    cached = n;
+int occupancy(const void* kern, int threads, size_t smem) {
+  prepare_kernel(kern);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, dev, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
   }
-  return cached;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_occ[key] = n;
+  return n;
+}
+
+void* tensor_map_encoder() {
+  static void* fn = []() -> void* {  // thread-safe one-time initialisation
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return f;
+  }();
+  return fn;
 }
 
 bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const bool on = [] {
     const char* e = getenv("DYNSPLIT_NO_PDL");
-    on = (e && *e && *e != '0') ? 0 : 1;
-  }
-  return on == 1;
+    return !(e && *e && *e != '0');
+  }();
+  return on;
 }
 
 static thread_local char g_last_error[512] = "";
 const char* last_error();
 
 cudaError_t post_launch(const char* where, cudaStream_t st) {
-  static int debug = -1;
-  if (debug < 0) {
+  static const int debug = [] {
     const char* e = getenv("DYNSPLIT_DEBUG");
-    debug = (e && *e && *e != '0') ? 1 : 0;
-  }
+    return (e && *e && *e != '0') ? 1 : 0;
+  }();
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && debug) {
     e = cudaStreamSynchronize(st);
@@ -76,6 +130,13 @@ const char* last_error() { return g_last_error; }
 using namespace dsk;
 
 namespace {
+
+// NVTX range per C-ABI call (a push/pop pair; free without an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define DSK_NVTX NvtxRange dsk_nvtx_range_(__func__)
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -103,6 +164,7 @@ dynsplit_status check_cfg(const dynsplit_config* c) {
     return DYNSPLIT_ERR_UNSUPPORTED;  // P: power of two in [1, 64]
   if (c->W < 1 || c->R < 1 || !(c->alpha_pen >= 0.f)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (c->digest_mode != 0 && c->digest_mode != 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->page_cap < 0) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return DYNSPLIT_OK;
 }
 
@@ -115,6 +177,9 @@ inline dynsplit_status cuda_status(cudaError_t e) {
     dynsplit_status _s = (x);                    \
     if (_s != DYNSPLIT_OK) return _s;            \
   } while (0)
+
+inline int* err_word(void* ws) { return static_cast<int*>(ws); }
+inline char* ws_body(void* ws) { return static_cast<char*>(ws) + kWsHdr; }
 
 // Worklist capacity per (b, KV head): every page of the sequence (the union
 // of the selected pages is a subset).  Budget-independent, so the attention
@@ -138,43 +203,49 @@ inline WorklistView worklist_view(void* wl, const dynsplit_shape* s) {
   return v;
 }
 
-size_t select_ws(const dynsplit_shape* s, const dynsplit_config* c) {
+// ---- workspace layouts: [kWsHdr header: device error word][body]
+size_t select_body(const dynsplit_shape* s, const dynsplit_config* c) {
   const int maxb = dynsplit_max_blocks(s->S, c);
   return align_up((size_t)s->B * s->Hq * maxb * 4) + align_up((size_t)s->B * s->Hq * 16);
 }
-// Decode workspace: [split-merge counters, fixed kMaxCounters ints at offset 0]
-// [part_o] [part_lse].  Counters sit at a shape-independent offset so that a
-// zero-filled workspace stays valid when reused with any shape.
+size_t select_ws(const dynsplit_shape* s, const dynsplit_config* c) { return kWsHdr + select_body(s, c); }
+// Decode body: [split-merge counters, fixed kMaxCounters ints][part_o][part_lse].
+// Counters sit at a shape-independent offset so that a zero-filled workspace
+// stays valid when reused with any shape.  The fused decode kernel keeps its
+// per-(b, KV head) group-barrier words in the upper half.
 constexpr size_t kMaxCounters = 65536;
-size_t decode_ws(const dynsplit_shape* s) {
+size_t decode_body(const dynsplit_shape* s) {
   return kMaxCounters * 4 + align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4) +
          align_up((size_t)s->B * s->Hq * kMaxSplit * 4);
 }
-size_t segment_ws(const dynsplit_shape* s) { return align_up((size_t)s->B * s->S * 4); }
-size_t score_ws(const dynsplit_shape* s) {
-  return align_up(score_ws_bytes(s->n_score_layers, s->B, s->S, s->Hq));
-}
+size_t decode_ws(const dynsplit_shape* s) { return kWsHdr + decode_body(s); }
+size_t segment_body(const dynsplit_shape* s) { return align_up((size_t)s->B * s->S * 4); }
+size_t segment_ws(const dynsplit_shape* s) { return kWsHdr + segment_body(s); }
+size_t score_body(const dynsplit_shape* s) { return align_up(score_ws_bytes(s->n_score_layers, s->B, s->S, s->Hq)); }
+size_t score_ws(const dynsplit_shape* s) { return kWsHdr + score_body(s); }
 size_t build_ws(const dynsplit_shape* s) {
-  // scoring partials + delim scores (if not returned) + segment next[]
-  return score_ws(s) + align_up((size_t)s->B * s->S * 4) + segment_ws(s);
+  // header + scoring partials + delim scores (if not returned) + segment next[]
+  return kWsHdr + score_body(s) + align_up((size_t)s->B * s->S * 4) + segment_body(s);
 }
-// dynsplit_decode_layer: decode workspace (counters at offset 0) then select's.
+// dynsplit_decode_layer: header, decode body (counters at a fixed offset), select body.
 size_t layer_ws(const dynsplit_shape* s, const dynsplit_config* c) {
-  return decode_ws(s) + select_ws(s, c);
+  return kWsHdr + decode_body(s) + select_body(s, c);
 }
 size_t step_host_extra(const dynsplit_shape* s) {
   return align_up((size_t)s->B * s->Hq * kD * esize(s)) + align_up((size_t)s->B * s->Hq * kD * 4) +
          align_up((size_t)s->B * s->Hq * 4) + 3 * align_up((size_t)s->B * s->Hq * 4);
 }
 
+}  // namespace
+
+namespace dsk {
 struct W10Table {
   uint8_t w[64];
 };
 __global__ void k_fill_w10(W10Table t, int n_ids, uint8_t* w10) {
   if (threadIdx.x < n_ids) w10[(size_t)blockIdx.x * n_ids + threadIdx.x] = t.w[threadIdx.x];
 }
-
-}  // namespace
+}  // namespace dsk
 
 extern "C" {
 
@@ -189,6 +260,7 @@ void dynsplit_default_config(dynsplit_config* c) {
   c->lambda_den = 2;
   c->page_size = 16;
   c->digest_mode = 0;
+  c->page_cap = 0;
 }
 
 int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* c) {
@@ -198,6 +270,7 @@ int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* c) {
 
 int32_t dynsplit_max_pages(int32_t S, const dynsplit_config* c) {
   if (!c || c->page_size < 1) return 0;
+  if (c->page_cap > 0) return c->page_cap;
   return dynsplit_max_blocks(S, c) + (S + c->page_size - 1) / c->page_size;
 }
 
@@ -225,7 +298,9 @@ size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* s, const dynsp
     case DYNSPLIT_OP_SELECT: return select_ws(s, c);
     case DYNSPLIT_OP_DECODE_ATTN: return decode_ws(s);
     case DYNSPLIT_OP_DECODE_LAYER: return layer_ws(s, c);
-    case DYNSPLIT_OP_APPEND: return append_ws_bytes(s->B);
+    case DYNSPLIT_OP_APPEND: return kWsHdr + append_ws_bytes(s->B);
+    case DYNSPLIT_OP_MAP_PAGES: return kWsHdr;
+    case DYNSPLIT_OP_REPACK: return kWsHdr;
     default: return 0;
   }
 }
@@ -233,7 +308,7 @@ size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* s, const dynsp
 size_t dynsplit_step_host_workspace_bytes(const dynsplit_shape* s, const dynsplit_config* c,
                                           int32_t budget) {
   if (check_shape(s) != DYNSPLIT_OK || check_cfg(c) != DYNSPLIT_OK || budget < 1) return 0;
-  return select_ws(s, c) + decode_ws(s) + step_host_extra(s);
+  return layer_ws(s, c) + step_host_extra(s);
 }
 
 const char* dynsplit_status_string(int32_t st) {
@@ -249,15 +324,39 @@ const char* dynsplit_status_string(int32_t st) {
   }
 }
 
-const char* dynsplit_version(void) { return "dynsplit-b200 0.1 (sm_100a)"; }
+const char* dynsplit_version(void) { return "dynsplit-b200 0.2 (sm_100a)"; }
 
 const char* dynsplit_last_error(void) { return dsk::last_error(); }
+
+int32_t dynsplit_read_device_error(const void* ws, void* stream) {
+  DSK_NVTX;
+  if (!ws) return -1;
+  int32_t v = 0;
+  if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess ||
+      cudaMemcpy(&v, ws, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return v;
+}
+
+dynsplit_status dynsplit_clear_device_error(void* ws, void* stream) {
+  DSK_NVTX;
+  if (!ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(cudaMemsetAsync(ws, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_stream_fence(void* stream) {
+  DSK_NVTX;
+  return cuda_status(launch_fence(static_cast<cudaStream_t>(stream)));
+}
 
 // ------------------------------------------------------------------ prefill
 dynsplit_status dynsplit_score_delimiters(const dynsplit_shape* s, const dynsplit_config* c,
                                           const int32_t* tokens, const int32_t* delim_ids,
                                           int32_t n_ids, const void* Qs, const void* Ks,
                                           float* out, void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!tokens || !delim_ids || !Qs || !Ks || !out || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
@@ -266,12 +365,13 @@ dynsplit_status dynsplit_score_delimiters(const dynsplit_shape* s, const dynspli
   if (ws_bytes < score_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   return cuda_status(launch_score_delimiters(tokens, delim_ids, n_ids, Qs, Ks, s->n_score_layers,
                                              s->B, s->S, s->Hq, s->Hkv, c->W, c->R, c->alpha_pen,
-                                             out, ws, static_cast<cudaStream_t>(stream)));
+                                             out, ws_body(ws), static_cast<cudaStream_t>(stream)));
 }
 
 dynsplit_status dynsplit_weight_table(const dynsplit_shape* s, const int32_t* tokens,
                                       const int32_t* delim_ids, int32_t n_ids,
                                       const float* delim_scores, uint8_t* w10, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   if (!tokens || !delim_ids || !delim_scores || !w10) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (n_ids < 1 || n_ids > 64) return DYNSPLIT_ERR_INVALID_ARGUMENT;
@@ -283,6 +383,7 @@ dynsplit_status dynsplit_segment(const dynsplit_shape* s, const dynsplit_config*
                                  const int32_t* tokens, const int32_t* delim_ids, int32_t n_ids,
                                  const uint8_t* w10, int32_t* block_starts, int32_t* n_blocks,
                                  void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!tokens || !delim_ids || !w10 || !block_starts || !n_blocks || !ws)
@@ -291,28 +392,30 @@ dynsplit_status dynsplit_segment(const dynsplit_shape* s, const dynsplit_config*
   if (ws_bytes < segment_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   return cuda_status(launch_segment(tokens, delim_ids, n_ids, w10, s->B, s->S, c->C, c->delta,
                                     c->lambda_num, c->lambda_den, dynsplit_max_blocks(s->S, c),
-                                    static_cast<int32_t*>(ws), block_starts, n_blocks,
+                                    reinterpret_cast<int32_t*>(ws_body(ws)), block_starts, n_blocks,
                                     static_cast<cudaStream_t>(stream)));
 }
 
-dynsplit_status dynsplit_map_pages(const dynsplit_shape* s, const dynsplit_config* c,
-                                   const int32_t* block_starts, const int32_t* n_blocks,
-                                   int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                                   int32_t* n_pages, void* stream) {
+}  // extern "C"
+
+static dynsplit_status map_pages_impl(const dynsplit_shape* s, const dynsplit_config* c,
+                                      const int32_t* block_starts, const int32_t* n_blocks,
+                                      int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                                      int32_t* n_pages, int* err, void* stream) {
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!block_starts || !n_blocks || !page_first || !page_block || !page_valid || !n_pages)
     return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return cuda_status(launch_map_pages(block_starts, n_blocks, s->B, dynsplit_max_blocks(s->S, c),
-                                      dynsplit_max_pages(s->S, c), c->page_size, page_first,
-                                      page_block, page_valid, n_pages,
+                                      dynsplit_max_pages(s->S, c), c->page_size, s->S, page_first,
+                                      page_block, page_valid, n_pages, err,
                                       static_cast<cudaStream_t>(stream)));
 }
 
-dynsplit_status dynsplit_repack_digest(const dynsplit_shape* s, const dynsplit_config* c,
-                                       const void* K, const void* V, const int32_t* block_starts,
-                                       const int32_t* n_blocks, const int32_t* page_first,
-                                       void* Kp, void* Vp, void* digests, void* stream) {
+static dynsplit_status repack_impl(const dynsplit_shape* s, const dynsplit_config* c, const void* K,
+                                   const void* V, const int32_t* block_starts, const int32_t* n_blocks,
+                                   const int32_t* page_first, void* Kp, void* Vp, void* digests, int* err,
+                                   void* stream) {
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!K || !V || !block_starts || !n_blocks || !page_first || !Kp || !Vp || !digests)
@@ -320,7 +423,32 @@ dynsplit_status dynsplit_repack_digest(const dynsplit_shape* s, const dynsplit_c
   return cuda_status(launch_repack_digest(s->kv_dtype, K, V, block_starts, n_blocks, page_first,
                                           s->B, s->S, s->Hkv, dynsplit_max_blocks(s->S, c),
                                           dynsplit_max_pages(s->S, c), c->page_size, c->digest_mode, Kp, Vp,
-                                          digests, static_cast<cudaStream_t>(stream)));
+                                          digests, err, static_cast<cudaStream_t>(stream)));
+}
+
+extern "C" {
+
+dynsplit_status dynsplit_map_pages(const dynsplit_shape* s, const dynsplit_config* c,
+                                   const int32_t* block_starts, const int32_t* n_blocks,
+                                   int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                                   int32_t* n_pages, void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  if (ws && ws_bytes < kWsHdr) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  DSK_TRY(map_pages_impl(s, c, block_starts, n_blocks, page_first, page_block, page_valid, n_pages,
+                         ws ? err_word(ws) : nullptr, stream));
+  return cuda_status(launch_fence(static_cast<cudaStream_t>(stream)));
+}
+
+dynsplit_status dynsplit_repack_digest(const dynsplit_shape* s, const dynsplit_config* c,
+                                       const void* K, const void* V, const int32_t* block_starts,
+                                       const int32_t* n_blocks, const int32_t* page_first,
+                                       void* Kp, void* Vp, void* digests, void* ws, size_t ws_bytes,
+                                       void* stream) {
+  DSK_NVTX;
+  if (ws && ws_bytes < kWsHdr) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  DSK_TRY(repack_impl(s, c, K, V, block_starts, n_blocks, page_first, Kp, Vp, digests,
+                      ws ? err_word(ws) : nullptr, stream));
+  return cuda_status(launch_fence(static_cast<cudaStream_t>(stream)));
 }
 
 dynsplit_status dynsplit_build_blocks(const dynsplit_shape* s, const dynsplit_config* c,
@@ -331,16 +459,18 @@ dynsplit_status dynsplit_build_blocks(const dynsplit_shape* s, const dynsplit_co
                                       int32_t* n_blocks, int32_t* page_first, int32_t* page_block,
                                       int16_t* page_valid, int32_t* n_pages, void* Kp, void* Vp,
                                       void* digests, void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!tokens || !delim_ids || !w10 || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (n_ids < 1 || n_ids > 64) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < build_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  char* w = static_cast<char*>(ws);
-  void* score_part = w;
-  float* tmp_scores = reinterpret_cast<float*>(w + score_ws(s));
-  int32_t* next_ws = reinterpret_cast<int32_t*>(w + score_ws(s) + align_up((size_t)s->B * s->S * 4));
+  char* w = ws_body(ws);
+  float* tmp_scores = reinterpret_cast<float*>(w + score_body(s));
+  // the score / segment sub-workspaces are addressed through their own (header) view
+  void* score_view = w - kWsHdr;   // body of the scoring call = w
+  void* seg_view = w + score_body(s) + align_up((size_t)s->B * s->S * 4) - kWsHdr;
   if (static_w10_host) {
     W10Table t;
     memset(&t, 0, sizeof(t));
@@ -350,24 +480,28 @@ dynsplit_status dynsplit_build_blocks(const dynsplit_shape* s, const dynsplit_co
   } else {
     if (!Qs || !Ks) return DYNSPLIT_ERR_INVALID_ARGUMENT;
     float* sc = delim_scores ? delim_scores : tmp_scores;
-    DSK_TRY(dynsplit_score_delimiters(s, c, tokens, delim_ids, n_ids, Qs, Ks, sc, score_part,
-                                      score_ws(s), stream));
+    if (launch_score_delimiters(tokens, delim_ids, n_ids, Qs, Ks, s->n_score_layers, s->B, s->S, s->Hq,
+                                s->Hkv, c->W, c->R, c->alpha_pen, sc, ws_body(score_view), st) != cudaSuccess)
+      return DYNSPLIT_ERR_CUDA;
     DSK_TRY(dynsplit_weight_table(s, tokens, delim_ids, n_ids, sc, w10, stream));
   }
-  DSK_TRY(dynsplit_segment(s, c, tokens, delim_ids, n_ids, w10, block_starts, n_blocks, next_ws,
-                           segment_ws(s), stream));
-  DSK_TRY(dynsplit_map_pages(s, c, block_starts, n_blocks, page_first, page_block, page_valid,
-                             n_pages, stream));
+  if (launch_segment(tokens, delim_ids, n_ids, w10, s->B, s->S, c->C, c->delta, c->lambda_num, c->lambda_den,
+                     dynsplit_max_blocks(s->S, c), reinterpret_cast<int32_t*>(ws_body(seg_view)), block_starts,
+                     n_blocks, st) != cudaSuccess)
+    return DYNSPLIT_ERR_CUDA;
+  DSK_TRY(map_pages_impl(s, c, block_starts, n_blocks, page_first, page_block, page_valid, n_pages,
+                         err_word(ws), stream));
   if (K || V || Kp || Vp || digests)
-    DSK_TRY(dynsplit_repack_digest(s, c, K, V, block_starts, n_blocks, page_first, Kp, Vp, digests,
-                                   stream));
-  return DYNSPLIT_OK;
+    DSK_TRY(repack_impl(s, c, K, V, block_starts, n_blocks, page_first, Kp, Vp, digests, err_word(ws),
+                        stream));
+  return cuda_status(launch_fence(st));
 }
 
 // ------------------------------------------------------------------ decode
 dynsplit_status dynsplit_score_blocks(const dynsplit_shape* s, const dynsplit_config* c,
                                       const void* q, const void* digests, const int32_t* n_blocks,
                                       float* scores, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!q || !digests || !n_blocks || !scores) return DYNSPLIT_ERR_INVALID_ARGUMENT;
@@ -380,30 +514,30 @@ dynsplit_status dynsplit_score_blocks(const dynsplit_shape* s, const dynsplit_co
 
 }  // extern "C"
 // a6 (shared by dynsplit_select_from_scores and dynsplit_decode_layer).
+// err: the device error word of the caller's workspace.
 static dynsplit_status select_impl(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,
                                    const float* scores, const int32_t* block_starts,
                                    const int32_t* n_blocks, const int32_t* page_first, int32_t blk_lo,
                                    int32_t blk_hi, int32_t* sel_blocks, int32_t* n_sel,
                                    int32_t* marginal_block, int32_t* marginal_keep, void* worklist,
-                                   void* ws, size_t ws_bytes, void* stream) {
+                                   int* err, void* stream) {
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (budget < 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (!scores || !block_starts || !n_blocks || !page_first || !n_sel || !marginal_block ||
-      !marginal_keep || !worklist || !ws)
+      !marginal_keep || !worklist)
     return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (blk_lo < 0 || blk_hi < blk_lo) return DYNSPLIT_ERR_INVALID_ARGUMENT;
-  if (ws_bytes < select_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   const int maxb = dynsplit_max_blocks(s->S, c);
   // smem-resident keys (S up to ~300K), 8-bit page counts per block, 16-bit block lengths
   if (select_smem_needed(maxb, s->Hq / s->Hkv) == (size_t)-1) return DYNSPLIT_ERR_UNSUPPORTED;
   if ((c->C + c->delta + c->page_size - 1) / c->page_size > 255) return DYNSPLIT_ERR_UNSUPPORTED;
   WorklistView v = worklist_view(worklist, s);
   return cuda_status(launch_select(s->Hq / s->Hkv, scores, block_starts, n_blocks, page_first, s->B,
-                                   s->Hq, s->Hkv, maxb, dynsplit_max_selected(budget, s->S, c),
+                                   s->Hq, s->Hkv, maxb, s->S, dynsplit_max_selected(budget, s->S, c),
                                    max_wl_of(s, c, budget), c->page_size, budget, blk_lo, blk_hi,
                                    sel_blocks, n_sel, marginal_block, marginal_keep, v.count,
-                                   v.entries, static_cast<cudaStream_t>(stream)));
+                                   v.entries, err, static_cast<cudaStream_t>(stream)));
 }
 extern "C" {
 
@@ -414,8 +548,13 @@ dynsplit_status dynsplit_select_from_scores(const dynsplit_shape* s, const dynsp
                                             int32_t blk_hi, int32_t* sel_blocks, int32_t* n_sel,
                                             int32_t* marginal_block, int32_t* marginal_keep,
                                             void* worklist, void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < select_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   return select_impl(s, c, budget, scores, block_starts, n_blocks, page_first, blk_lo, blk_hi,
-                     sel_blocks, n_sel, marginal_block, marginal_keep, worklist, ws, ws_bytes, stream);
+                     sel_blocks, n_sel, marginal_block, marginal_keep, worklist, err_word(ws), stream);
 }
 
 
@@ -425,34 +564,33 @@ dynsplit_status dynsplit_select(const dynsplit_shape* s, const dynsplit_config* 
                                 float* scores_out, int32_t* sel_blocks, int32_t* n_sel,
                                 int32_t* marginal_block, int32_t* marginal_keep, void* worklist,
                                 void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < select_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
-  float* sc = scores_out ? scores_out : static_cast<float*>(ws);
+  float* sc = scores_out ? scores_out : reinterpret_cast<float*>(ws_body(ws));
   DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
-  return dynsplit_select_from_scores(s, c, budget, sc, block_starts, n_blocks, page_first, 0,
-                                     0x7fffffff, sel_blocks, n_sel, marginal_block, marginal_keep,
-                                     worklist, ws, ws_bytes, stream);
+  return select_impl(s, c, budget, sc, block_starts, n_blocks, page_first, 0, 0x7fffffff, sel_blocks,
+                     n_sel, marginal_block, marginal_keep, worklist, err_word(ws), stream);
 }
 
-dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_config* c,
-                                     const void* q, const void* Kp, const void* Vp,
-                                     const int16_t* page_valid, const int32_t* n_pages,
-                                     const void* worklist, float scale, float* o, float* lse,
-                                     void* ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+static dynsplit_status decode_attn_impl(const dynsplit_shape* s, const dynsplit_config* c, const void* q,
+                                        const void* Kp, const void* Vp, const int16_t* page_valid,
+                                        const int32_t* n_pages, const void* worklist, float scale, float* o,
+                                        float* lse, char* body, void* stream) {
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
-  if (!q || !Kp || !Vp || !o || !lse || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (!q || !Kp || !Vp || !o || !lse) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   const int dense = worklist == nullptr;
   if (dense && (!n_pages || !page_valid)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
-  if (ws_bytes < decode_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)kD);
-  if ((size_t)s->B * s->Hkv > kMaxCounters) return DYNSPLIT_ERR_UNSUPPORTED;
-  char* w = static_cast<char*>(ws);
-  int* counters = reinterpret_cast<int*>(w);
-  float* part_o = reinterpret_cast<float*>(w + kMaxCounters * 4);
-  float* part_lse = reinterpret_cast<float*>(w + kMaxCounters * 4 +
+  if ((size_t)s->B * s->Hkv > kMaxCounters / 2) return DYNSPLIT_ERR_UNSUPPORTED;
+  int* counters = reinterpret_cast<int*>(body);
+  float* part_o = reinterpret_cast<float*>(body + kMaxCounters * 4);
+  float* part_lse = reinterpret_cast<float*>(body + kMaxCounters * 4 +
                                              align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4));
   const int32_t* hdr = nullptr;
   const int32_t* cnt = nullptr;
@@ -470,6 +608,61 @@ dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_con
                                         static_cast<cudaStream_t>(stream)));
 }
 
+extern "C" {
+
+dynsplit_status dynsplit_decode_attn(const dynsplit_shape* s, const dynsplit_config* c,
+                                     const void* q, const void* Kp, const void* Vp,
+                                     const int16_t* page_valid, const int32_t* n_pages,
+                                     const void* worklist, float scale, float* o, float* lse,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  if (!ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < decode_ws(s)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  return decode_attn_impl(s, c, q, Kp, Vp, page_valid, n_pages, worklist, scale, o, lse, ws_body(ws), stream);
+}
+
+}  // extern "C"
+
+static dynsplit_status decode_layer_impl(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,
+                                         const void* q, const void* digests, const int32_t* block_starts,
+                                         const int32_t* n_blocks, const int32_t* page_first, const void* Kp,
+                                         const void* Vp, float scale, int32_t* n_sel, int32_t* marginal_block,
+                                         int32_t* marginal_keep, void* worklist, float* o, float* lse,
+                                         void* ws, void* stream) {
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!q || !digests || !Kp || !Vp || !o || !lse || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (budget < 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (!block_starts || !n_blocks || !page_first || !n_sel || !marginal_block || !marginal_keep || !worklist)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  char* body = ws_body(ws);
+  char* dec_body = body;  // counters first: shape-independent offset
+  float* sc = reinterpret_cast<float*>(body + decode_body(s));
+  if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)kD);
+  // the fused single-kernel layer (a5 + a6 + a7 + a8) where the shape allows it
+  {
+    const int maxb = dynsplit_max_blocks(s->S, c);
+    WorklistView v = worklist_view(worklist, s);
+    int* counters = reinterpret_cast<int*>(dec_body);
+    float* part_o = reinterpret_cast<float*>(dec_body + kMaxCounters * 4);
+    float* part_lse = reinterpret_cast<float*>(dec_body + kMaxCounters * 4 +
+                                               align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4));
+    const cudaError_t e = launch_decode_fused(
+        s->kv_dtype, c->digest_mode, s->Hq / s->Hkv, q, digests, block_starts, n_blocks, page_first, Kp, Vp,
+        s->B, s->Hq, s->Hkv, maxb, dynsplit_max_pages(s->S, c), c->page_size, budget, scale, sc, counters,
+        counters + kMaxCounters / 2, part_o, part_lse, n_sel, marginal_block, marginal_keep, v.hdr, v.count,
+        v.entries, o, lse, err_word(ws), static_cast<cudaStream_t>(stream));
+    if (e != cudaErrorNotSupported) return cuda_status(e);
+  }
+  DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
+  DSK_TRY(select_impl(s, c, budget, sc, block_starts, n_blocks, page_first, 0, 0x7fffffff, nullptr, n_sel,
+                      marginal_block, marginal_keep, worklist, err_word(ws), stream));
+  return decode_attn_impl(s, c, q, Kp, Vp, nullptr, nullptr, worklist, scale, o, lse, dec_body, stream);
+}
+
+extern "C" {
+
 dynsplit_status dynsplit_decode_layer(const dynsplit_shape* s, const dynsplit_config* c,
                                       int32_t budget, const void* q, const void* digests,
                                       const int32_t* block_starts, const int32_t* n_blocks,
@@ -477,19 +670,13 @@ dynsplit_status dynsplit_decode_layer(const dynsplit_shape* s, const dynsplit_co
                                       float scale, int32_t* n_sel, int32_t* marginal_block,
                                       int32_t* marginal_keep, void* worklist, float* o, float* lse,
                                       void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
-  if (!q || !digests || !Kp || !Vp || !o || !lse || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (!ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < layer_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
-  char* w = static_cast<char*>(ws);
-  char* ws_dec = w;  // counters first: shape-independent offset
-  char* ws_sel = w + decode_ws(s);
-  float* sc = reinterpret_cast<float*>(ws_sel);
-  DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
-  DSK_TRY(select_impl(s, c, budget, sc, block_starts, n_blocks, page_first, 0, 0x7fffffff, nullptr,
-                      n_sel, marginal_block, marginal_keep, worklist, ws_sel, select_ws(s, c), stream));
-  return dynsplit_decode_attn(s, c, q, Kp, Vp, nullptr, nullptr, worklist, scale, o, lse, ws_dec,
-                              decode_ws(s), stream);
+  return decode_layer_impl(s, c, budget, q, digests, block_starts, n_blocks, page_first, Kp, Vp, scale, n_sel,
+                           marginal_block, marginal_keep, worklist, o, lse, ws, stream);
 }
 
 // ------------------------------------------------------------------ NEXT-1: append
@@ -499,6 +686,7 @@ dynsplit_status dynsplit_append_plan(const dynsplit_shape* s, const dynsplit_con
                                      int32_t* n_blocks, int32_t* page_first, int32_t* page_block,
                                      int16_t* page_valid, int32_t* n_pages, void* ws, size_t ws_bytes,
                                      void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!tokens || !delim_ids || !w10 || !block_starts || !n_blocks || !page_first || !page_block ||
@@ -508,12 +696,13 @@ dynsplit_status dynsplit_append_plan(const dynsplit_shape* s, const dynsplit_con
   if (L < 1) return DYNSPLIT_ERR_EMPTY_SEQUENCE;
   if (L_prev < 0 || L_prev > L || L > s->S) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
   if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
-  if (ws_bytes < append_ws_bytes(s->B)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
-  return cuda_status(launch_plan_append(
+  if (ws_bytes < kWsHdr + append_ws_bytes(s->B)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DSK_TRY(cuda_status(launch_plan_append(
       tokens, delim_ids, n_ids, w10, s->B, s->S, dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
       c->C, c->delta, c->lambda_num, c->lambda_den, c->page_size, L_prev, L, block_starts, n_blocks,
-      page_first, page_block, page_valid, n_pages, static_cast<int32_t*>(ws),
-      static_cast<cudaStream_t>(stream)));
+      page_first, page_block, page_valid, n_pages, reinterpret_cast<int32_t*>(ws_body(ws)), err_word(ws), st)));
+  return cuda_status(launch_fence(st));
 }
 
 dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynsplit_config* c,
@@ -522,6 +711,7 @@ dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynspli
                                           const int32_t* block_starts, const int32_t* n_blocks,
                                           const int32_t* page_first, const void* ws, void* const* Kp,
                                           void* const* Vp, void* const* digests, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!block_starts || !n_blocks || !page_first || !ws || !Kp || !Vp || !digests)
@@ -534,11 +724,13 @@ dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynspli
     if (L > L_prev && (!K_new || !V_new || !K_new[l] || !V_new[l])) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   }
   if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
-  return cuda_status(launch_kv_append(s->kv_dtype, n_layers, K_new, V_new, L - L_prev, s->B, s->Hkv,
-                                      dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
-                                      c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks,
-                                      page_first, static_cast<const int32_t*>(ws), Kp, Vp, digests,
-                                      c->digest_mode, static_cast<cudaStream_t>(stream)));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DSK_TRY(cuda_status(launch_kv_append(
+      s->kv_dtype, n_layers, K_new, V_new, L - L_prev, s->B, s->Hkv, dynsplit_max_blocks(s->S, c),
+      dynsplit_max_pages(s->S, c), c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks, page_first,
+      reinterpret_cast<const int32_t*>(static_cast<const char*>(ws) + kWsHdr), Kp, Vp, digests, c->digest_mode,
+      st)));
+  return cuda_status(launch_fence(st));
 }
 
 dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_config* c, int32_t L_prev,
@@ -558,6 +750,7 @@ dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_confi
 dynsplit_status dynsplit_merge_partials(const float* o_parts, const float* lse_parts,
                                         int32_t n_parts, int32_t rows, int32_t d, float* o,
                                         float* lse, void* stream) {
+  DSK_NVTX;
   if (!o_parts || !lse_parts || !o || !lse || n_parts < 1 || rows < 1 || d < 1)
     return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return cuda_status(launch_merge(o_parts, lse_parts, n_parts, rows, d, o, lse,
@@ -571,16 +764,14 @@ dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* s, const dynspli
                                           const int16_t* page_valid, float scale, float* o_host,
                                           float* lse_host, void* worklist, void* ws,
                                           size_t ws_bytes, void* stream) {
+  DSK_NVTX;
   DSK_TRY(check_shape(s));
   DSK_TRY(check_cfg(c));
   if (!q_host || !o_host || !lse_host || !ws || !worklist) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < dynsplit_step_host_workspace_bytes(s, c, budget))
     return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  char* w = static_cast<char*>(ws);
-  char* ws_dec = w;                      // counters first: shape-independent offset
-  char* ws_sel = w + decode_ws(s);
-  char* extra = ws_sel + select_ws(s, c);
+  char* extra = static_cast<char*>(ws) + layer_ws(s, c);
   const size_t qbytes = (size_t)s->B * s->Hq * kD * esize(s);
   void* q_dev = extra;
   float* o_dev = reinterpret_cast<float*>(extra + align_up(qbytes));
@@ -591,10 +782,8 @@ dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* s, const dynspli
   if (cudaMemcpyAsync(q_dev, q_host, qbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return DYNSPLIT_ERR_CUDA;
   (void)page_valid;
-  (void)ws_sel;
-  DSK_TRY(dynsplit_decode_layer(s, c, budget, q_dev, digests, block_starts, n_blocks, page_first, Kp,
-                                Vp, scale, nsel, marg, keep, worklist, o_dev, lse_dev, ws_dec,
-                                layer_ws(s, c), stream));
+  DSK_TRY(decode_layer_impl(s, c, budget, q_dev, digests, block_starts, n_blocks, page_first, Kp, Vp, scale, nsel,
+                            marg, keep, worklist, o_dev, lse_dev, ws, stream));
   if (cudaMemcpyAsync(o_host, o_dev, (size_t)s->B * s->Hq * kD * 4, cudaMemcpyDeviceToHost, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(lse_host, lse_dev, (size_t)s->B * s->Hq * 4, cudaMemcpyDeviceToHost, st) !=

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
                                                     int32_t* __restrict__ page_block,
                                                     int16_t* __restrict__ page_valid,
                                                     int32_t* __restrict__ n_pages,
-                                                    int32_t* __restrict__ ws) {
+                                                    int32_t* __restrict__ ws, int* __restrict__ err) {
   __shared__ int s_ids[64], s_w[64];
   const int b = blockIdx.x, lane = threadIdx.x;
   for (int j = lane; j < n_ids; j += 32) {
@@ -59,6 +59,22 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
   int32_t* w = ws + (size_t)b * kAppendWs;
   const int32_t* tk = tokens + (size_t)b * S;
 
+  // ---- 0. the stored plan must cover exactly the L_prev planned tokens
+  //         (S:210 PlanMismatch); otherwise the sequence is left untouched
+  //         (f = -1 tells k_kv_append to skip it)
+  if (L_prev > 0) {
+    const int nb_old = n_blocks[b];
+    const bool ok = nb_old >= 1 && nb_old <= maxb && bs[0] == 0 && bs[nb_old] == L_prev &&
+                    n_pages[b] >= 0 && n_pages[b] <= maxp;
+    if (!ok) {
+      if (lane == 0) {
+        w[0] = -1;
+        w[1] = w[2] = 0;
+        raise_err(err, kErrPlanMismatch);
+      }
+      return;
+    }
+  }
   // ---- 1. first non-frozen block of the old plan, old tail locations
   int f = 0, s0 = 0, n_old = 0;
   if (L_prev > 0) {
@@ -135,6 +151,19 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
   int32_t* pb = page_block + (size_t)b * maxp;
   int16_t* pv = page_valid + (size_t)b * maxp;
   const int np_old = n_pages[b];
+  {  // the re-planned tail must fit the page capacity
+    int need = 0;
+    for (int j = f + lane; j < nb; j += 32) need += (bs[j + 1] - bs[j] + P - 1) / P;
+    need = warp_sum_i(need);
+    if (pf[f] + need > maxp) {
+      if (lane == 0) {
+        w[0] = -1;
+        n_pages[b] = -1;
+        raise_err(err, kErrPageCapacity);
+      }
+      return;
+    }
+  }
   int carry = pf[f];
   for (int j0 = f; j0 < nb; j0 += 32) {
     const int j = j0 + lane;
@@ -179,6 +208,7 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int32_t* w = ws + (size_t)b * kAppendWs;
   const int f = w[0], s0 = w[1], n_old = w[2];
+  if (f < 0) return;  // k_plan_append flagged this sequence (plan mismatch / capacity)
   const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
   const int32_t* pf = page_first + (size_t)b * (maxb + 1);
   const size_t page_base = ((size_t)b * Hkv + hk) * maxp;
@@ -203,6 +233,8 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
   const T* vn = V_new + ((size_t)b * n_new * Hkv + hk) * kD;
   for (int j = f + warp; j < nb; j += nw) {
     const int t0 = bs[j], t1 = bs[j + 1];
+    // a page table that does not fit the capacity (a failed whole-prefix map) is never written past
+    if (t1 <= t0 || pf[j] < 0 || pf[j] + (t1 - t0 + P - 1) / P > maxp) continue;
     float mx[LE], mn[LE], sm[LE];
 #pragma unroll
     for (int e = 0; e < LE; ++e) {
@@ -277,14 +309,14 @@ cudaError_t launch_plan_append(const int32_t* tokens, const int32_t* delim_ids, 
                                int B, int S, int maxb, int maxp, int C, int delta, int lam_num, int lam_den,
                                int P, int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
                                int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                               int32_t* n_pages, int32_t* ws, cudaStream_t st) {
+                               int32_t* n_pages, int32_t* ws, int* err, cudaStream_t st) {
   k_plan_append<<<B, 32, 0, st>>>(tokens, delim_ids, n_ids, w10, S, maxb, maxp, C, delta, lam_num, lam_den, P,
                                    L_prev, L, block_starts, n_blocks, page_first, page_block, page_valid,
-                                   n_pages, ws);
+                                   n_pages, ws, err);
   cudaError_t e = post_launch(__func__, st);
   if (e != cudaSuccess || L_prev > 0) return e;
-  return launch_map_pages(block_starts, n_blocks, B, maxb, maxp, P, page_first, page_block, page_valid,
-                          n_pages, st);
+  return launch_map_pages(block_starts, n_blocks, B, maxb, maxp, P, L, page_first, page_block, page_valid,
+                          n_pages, err, st);
 }
 
 cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, const void* const* V_new,
@@ -305,19 +337,11 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
   const size_t smem = 2 * (size_t)max(max_tail, 1) * kD * esz;
   dim3 grid(Hkv, B, n_layers);
   if (dtype == 0) {
-    static bool attr = false;
-    if (!attr) {
-      allow_max_dyn_smem(k_kv_append<bf16>);
-      attr = true;
-    }
+    allow_max_dyn_smem(k_kv_append<bf16>);
     k_kv_append<bf16><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
                                                block_starts, n_blocks, page_first, ws, mean_mode);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      allow_max_dyn_smem(k_kv_append<float>);
-      attr = true;
-    }
+    allow_max_dyn_smem(k_kv_append<float>);
     k_kv_append<float><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
                                                 block_starts, n_blocks, page_first, ws, mean_mode);
   }

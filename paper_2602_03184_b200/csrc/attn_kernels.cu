@@ -164,22 +164,30 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
   const int bh = b * Hkv + hk;
 
   if (threadIdx.x == 0) astamp(0);
-  // prologue independent of the preceding kernel (PDL overlap): q, V ring reset
-  {
-    constexpr int QCH = G * kD * (int)sizeof(T) / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD);
-    for (int c = threadIdx.x; c < QCH; c += blockDim.x) reinterpret_cast<uint4*>(s_q)[c] = src[c];
-    if (kTC) {
-      const int nz = (int)(kstage / 16);
-      for (int s2 = 0; s2 < NW * nd; ++s2) {
-        uint4* vz = reinterpret_cast<uint4*>(smem + s2 * stage + kstage);
-        for (int c = threadIdx.x; c < nz; c += blockDim.x) vz[c] = make_uint4(0u, 0u, 0u, 0u);
-      }
+  // prologue independent of the preceding kernel (PDL overlap): V ring reset
+  if (kTC) {
+    const int nz = (int)(kstage / 16);
+    for (int s2 = 0; s2 < NW * nd; ++s2) {
+      uint4* vz = reinterpret_cast<uint4*>(smem + s2 * stage + kstage);
+      for (int c = threadIdx.x; c < nz; c += blockDim.x) vz[c] = make_uint4(0u, 0u, 0u, 0u);
     }
   }
   pdl_trigger();
-  pdl_wait();  // the worklist is the previous kernel's output
+  pdl_wait();  // q and the worklist belong to the step: read only after the wait
   if (threadIdx.x == 0) astamp(1);
+  // q of the G heads: loads issued now, stored to smem after the worklist
+  // loads below are in flight (their latencies overlap)
+  constexpr int QCH = G * kD * (int)sizeof(T) / 16;
+  constexpr int QPT = (QCH + NW * 32 - 1) / (NW * 32);
+  uint4 qreg[QPT];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD);
+#pragma unroll
+    for (int k = 0; k < QPT; ++k) {
+      const int c = threadIdx.x + k * NW * 32;
+      if (c < QCH) qreg[k] = __ldcg(src + c);
+    }
+  }
 
   // Pages are dealt round-robin: split s of n_eff takes worklist entries
   // e = s + k n_eff, k = 0, 1, ...; warp w takes k = w + j NW.  Entry e of
@@ -211,6 +219,11 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
   };
   load_batch(0, n_split);
   const int cnt = dense ? n_pages[b] : __ldca(wl_count + bh);
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    const int c = threadIdx.x + k * NW * 32;
+    if (c < QCH) reinterpret_cast<uint4*>(s_q)[c] = qreg[k];
+  }
   // splits actually used by this (b, KV head): at least kMinPagesPerSplit pages each
   const int n_eff = max(1, min(n_split, (cnt + kMinPagesPerSplit - 1) / kMinPagesPerSplit));
   if (split >= n_eff) return;
@@ -238,6 +251,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
       int rmax = 0;
 #pragma unroll
       for (int g = 0; g < G; ++g) rmax = max(rmax, (int)(((g < 4 ? a : c) >> (8 * (g & 3))) & 0xffu));
+      if ((unsigned)pg >= (unsigned)max_pages) rmax = 0;  // a corrupt worklist is never read past the pages
 #ifdef DSK_DEBUG
       if (g_attn_noload) rmax = 0;
 #endif
@@ -620,9 +634,10 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
   // parts are added in part order through shared memory.
   constexpr int R = NW >= G ? NW / G : 1;
   float* mrg = reinterpret_cast<float*>(smem);  // [G][R][kD]
-  const int hm = warp % G, part = warp / G;
-  if (warp < G * R) {
-    const int h = hm;
+  // warp w merges (head, part) pairs hp = w, w + NW, ...: with NW < G (e.g. 4
+  // warps, G = 8) a warp takes several heads; R parts per head when NW >= G
+  for (int hp = warp; hp < G * R; hp += NW) {
+    const int h = hp % G, part = hp / G;
     const size_t row = (size_t)b * Hq + hk * G + h;
     const float* pl = part_lse + row * n_split;
     const float4* po_base = reinterpret_cast<const float4*>(part_o + row * n_split * kD) + lane;
@@ -706,12 +721,11 @@ static size_t attn_smem(int P) {
 // 3-deep rings): measured best at 128K / budget 4096 (15.4 us vs 17.7 with
 // 4 warps x 3 CTAs per SM): fewer split partials to merge.
 static int attn_nw() {
-  static int nw = 0;
-  if (!nw) {
+  static const int nw = [] {
     const char* e = getenv("DYNSPLIT_ATTN_NW");
     const int v = e ? atoi(e) : 8;
-    nw = (v == 4 || v == 12) ? v : 8;
-  }
+    return (v == 4 || v == 12) ? v : 8;
+  }();
   return nw;
 }
 
@@ -719,21 +733,7 @@ template <typename T, int G, int NW>
 struct AttnLaunch {
   static constexpr int D = 2;  // pages in flight per warp while it computes one (3 measured slower)
   static int occupancy(int P) {
-    static int occ = 0, lastP = -1;
-    if (occ == 0 || lastP != P) {
-      auto kern = k_decode_attn<T, G, NW, D>;
-      allow_max_dyn_smem(kern);
-      int n = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, NW * 32, attn_smem<T, G, NW, D>(P)) !=
-              cudaSuccess ||
-          n < 1) {
-        cudaGetLastError();
-        n = 1;
-      }
-      occ = n;
-      lastP = P;
-    }
-    return occ;
+    return occupancy_of(k_decode_attn<T, G, NW, D>, NW * 32, attn_smem<T, G, NW, D>(P));
   }
   static cudaError_t run(const void* q, const void* Kp, const void* Vp, const int16_t* pv,
                          const int32_t* n_pages, const int32_t* wl_hdr, const int32_t* wl_count,
@@ -741,6 +741,7 @@ struct AttnLaunch {
                          float scale_log2, float* part_o, float* part_lse, int* counters,
                          float* o, float* lse, cudaStream_t st) {
     const int occ = occupancy(P);
+    allow_max_dyn_smem(k_decode_attn<T, G, NW, D>);
     const int n_split = max(1, min(kMaxSplit, (num_sms() * occ) / max(1, B * Hkv)));
     launch_ex(k_decode_attn<T, G, NW, D>, dim3(n_split, Hkv, B), dim3(NW * 32),
               attn_smem<T, G, NW, D>(P), st, 1, static_cast<const T*>(q), static_cast<const T*>(Kp),

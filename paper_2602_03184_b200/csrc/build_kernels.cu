@@ -256,14 +256,18 @@ __global__ void __launch_bounds__(1024) k_dd_walk(const int32_t* __restrict__ ne
 }
 
 // ============================================================================
-// a4 (part 1): uniform page map.  grid (B), 1024 threads.
+// a4 (part 1): uniform page map.  grid (B), 1024 threads.  A validation pass
+// first: the plan must tile [0, L_end) (n_blocks in [1, maxb], starts from 0
+// strictly increasing to L_end; S:267 PlanCoverageMismatch) and fit the page
+// capacity maxp; otherwise n_pages[b] = -1, the error bit is raised and
+// nothing else of sequence b is written.
 // ============================================================================
 __global__ void __launch_bounds__(1024) k_map_pages(const int32_t* __restrict__ block_starts,
                                                     const int32_t* __restrict__ n_blocks, int maxb,
-                                                    int maxp, int P, int32_t* __restrict__ page_first,
+                                                    int maxp, int P, int L_end, int32_t* __restrict__ page_first,
                                                     int32_t* __restrict__ page_block,
                                                     int16_t* __restrict__ page_valid,
-                                                    int32_t* __restrict__ n_pages) {
+                                                    int32_t* __restrict__ n_pages, int* __restrict__ err) {
   __shared__ int sm[33];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = n_blocks[b];
@@ -271,6 +275,41 @@ __global__ void __launch_bounds__(1024) k_map_pages(const int32_t* __restrict__ 
   int32_t* pf = page_first + (size_t)b * (maxb + 1);
   int32_t* pb = page_block + (size_t)b * maxp;
   int16_t* pv = page_valid + (size_t)b * maxp;
+  // ---- validation: coverage and page capacity
+  if (nb < 1 || nb > maxb) {
+    if (tid == 0) {
+      n_pages[b] = -1;
+      raise_err(err, kErrPlanCoverage);
+    }
+    return;
+  }
+  int bad = tid == 0 && (bs[0] != 0 || bs[nb] != L_end);
+  long long need = 0;
+  for (int blk = tid; blk < nb; blk += 1024) {
+    const int len = bs[blk + 1] - bs[blk];
+    bad |= len <= 0;
+    need += (len + P - 1) / P;
+  }
+  for (int o = 16; o > 0; o >>= 1) need += __shfl_xor_sync(0xffffffffu, need, o);
+  __shared__ long long s_need[32];
+  if (lane == 0) s_need[warp] = need;
+  bad = __syncthreads_or(bad);
+  if (bad) {
+    if (tid == 0) {
+      n_pages[b] = -1;
+      raise_err(err, kErrPlanCoverage);
+    }
+    return;
+  }
+  long long tot_need = 0;
+  for (int w = 0; w < 32; ++w) tot_need += s_need[w];
+  if (tot_need > maxp) {
+    if (tid == 0) {
+      n_pages[b] = -1;
+      raise_err(err, kErrPageCapacity);
+    }
+    return;
+  }
   int carry = 0;
   for (int c0 = 0; c0 < nb; c0 += 1024) {
     const int blk = c0 + tid;
@@ -339,7 +378,8 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
                                                        const int32_t* __restrict__ page_first, int S,
                                                        int Hkv, int maxb, int maxp, int P,
                                                        int mean_mode, T* __restrict__ Kp,
-                                                       T* __restrict__ Vp, T* __restrict__ dig) {
+                                                       T* __restrict__ Vp, T* __restrict__ dig,
+                                                       int* __restrict__ err) {
   constexpr int EPC = 16 / sizeof(T);     // elements per 16-byte chunk
   constexpr int CPR = kD / EPC;           // chunks per head row
   const int b = blockIdx.y;
@@ -347,9 +387,19 @@ __global__ void __launch_bounds__(128) k_repack_digest(const T* __restrict__ K, 
   const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
   const int32_t* pf = page_first + (size_t)b * (maxb + 1);
   const int HC = Hkv * CPR;
+  // the plan must tile [0, S) and its pages fit the capacity: a bad
+  // sequence (or block) is skipped and flagged, never written out of bounds
+  if (nb < 1 || nb > maxb || bs[0] != 0 || bs[nb] != S) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_err(err, kErrPlanCoverage);
+    return;
+  }
   for (int blk = blockIdx.x; blk < nb; blk += gridDim.x) {
     const int st = bs[blk], len = bs[blk + 1] - st, p0 = pf[blk];
     const int npg = (len + P - 1) / P;
+    if (len <= 0 || st < 0 || st + len > S || p0 < 0 || p0 + npg > maxp) {
+      if (threadIdx.x == 0) raise_err(err, len <= 0 || st < 0 || st + len > S ? kErrPlanCoverage : kErrPageCapacity);
+      continue;
+    }
     for (int hc = threadIdx.x; hc < HC; hc += blockDim.x) {
       const int h = hc / CPR, c = hc % CPR;
       float mx[EPC], mn[EPC], sm[EPC];
@@ -460,38 +510,39 @@ cudaError_t launch_segment(const int32_t* tokens, const int32_t* delim_ids, int 
 }
 
 cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int maxb, int maxp, int P,
-                             int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                             int32_t* n_pages, cudaStream_t st) {
-  k_map_pages<<<B, 1024, 0, st>>>(bs, nb, maxb, maxp, P, page_first, page_block, page_valid, n_pages);
+                             int L_end, int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                             int32_t* n_pages, int* err, cudaStream_t st) {
+  k_map_pages<<<B, 1024, 0, st>>>(bs, nb, maxb, maxp, P, L_end, page_first, page_block, page_valid, n_pages,
+                                  err);
+  return post_launch(__func__, st);
+}
+
+// dynsplit_stream_fence: an empty kernel launched WITHOUT the PDL attribute
+// (full stream ordering: the writes of everything before it are visible to
+// everything after it, including PDL prologues).
+__global__ void k_stream_fence() {}
+cudaError_t launch_fence(cudaStream_t st) {
+  k_stream_fence<<<1, 32, 0, st>>>();
   return post_launch(__func__, st);
 }
 
 cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
                                  const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
                                  int maxb, int maxp, int P, int mean_mode, void* Kp, void* Vp, void* dig,
-                                 cudaStream_t st) {
+                                 int* err, cudaStream_t st) {
   // exactly one resident wave (CTAs stride over the blocks): a grid past the
   // occupancy leaves a lone partial second wave
-  static int occ[2] = {0, 0};
-  int& oc = occ[dtype == 0 ? 0 : 1];
-  if (!oc) {
-    cudaError_t e = dtype == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_repack_digest<bf16>, 128, 0)
-                               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_repack_digest<float>, 128, 0);
-    if (e != cudaSuccess || oc < 1) {
-      cudaGetLastError();
-      oc = 4;
-    }
-  }
+  const int oc = dtype == 0 ? occupancy_of(k_repack_digest<bf16>, 128, 0) : occupancy_of(k_repack_digest<float>, 128, 0);
   const int ctas = max(1, min(maxb, num_sms() * oc / max(1, B)));
   dim3 grid(ctas, B);
   if (dtype == 0)
     k_repack_digest<bf16><<<grid, 128, 0, st>>>(
         static_cast<const bf16*>(K), static_cast<const bf16*>(V), bs, nb, pf, S, Hkv, maxb, maxp, P,
-        mean_mode, static_cast<bf16*>(Kp), static_cast<bf16*>(Vp), static_cast<bf16*>(dig));
+        mean_mode, static_cast<bf16*>(Kp), static_cast<bf16*>(Vp), static_cast<bf16*>(dig), err);
   else
     k_repack_digest<float><<<grid, 128, 0, st>>>(
         static_cast<const float*>(K), static_cast<const float*>(V), bs, nb, pf, S, Hkv, maxb, maxp,
-        P, mean_mode, static_cast<float*>(Kp), static_cast<float*>(Vp), static_cast<float*>(dig));
+        P, mean_mode, static_cast<float*>(Kp), static_cast<float*>(Vp), static_cast<float*>(dig), err);
   return post_launch(__func__, st);
 }
 

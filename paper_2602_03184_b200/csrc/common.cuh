@@ -14,6 +14,21 @@ constexpr int kMaxSplit = 64;    // split-K partials per (b, KV head)
 
 typedef __nv_bfloat16 bf16;
 
+// Every workspace starts with a header of kWsHdr bytes; its first int32 is the
+// device error word (DYNSPLIT_DEVERR_* bits of include/dynsplit.h).
+constexpr size_t kWsHdr = 256;
+enum : int {
+  kErrPlanCoverage = 1,   // DYNSPLIT_DEVERR_PLAN_COVERAGE
+  kErrPlanMismatch = 2,   // DYNSPLIT_DEVERR_PLAN_MISMATCH
+  kErrPageCapacity = 4,   // DYNSPLIT_DEVERR_PAGE_CAPACITY
+  kErrSelectOverflow = 8, // DYNSPLIT_DEVERR_SELECT_OVERFLOW
+  kErrBlockTooLong = 16,  // DYNSPLIT_DEVERR_BLOCK_TOO_LONG
+  kErrSyncTimeout = 32    // DYNSPLIT_DEVERR_SYNC_TIMEOUT
+};
+__device__ __forceinline__ void raise_err(int* err, int bit) {
+  if (err) atomicOr(err, bit);
+}
+
 // One worklist entry: a page of one (b, KV head) and, per packed query head
 // of the group, how many leading rows of the page that head attends to.
 struct __align__(16) WLEntry {

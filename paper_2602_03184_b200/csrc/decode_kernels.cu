@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(512, 1) k_score_blocks(const T* __restrict__ q
 
 // Test hook: 1 forces the CUDA-core k_score_blocks for bf16 too (parity of the
 // two a5 kernels); initial value from DYNSPLIT_A5_CUDA_CORE.
-static bool g_score_cuda_core = getenv("DYNSPLIT_A5_CUDA_CORE") != nullptr;
+static volatile bool g_score_cuda_core = getenv("DYNSPLIT_A5_CUDA_CORE") != nullptr;
 
 // ============================================================================
 // a5 on the tensor cores (bf16 digests, min/max mode).  The block score is a
@@ -459,15 +459,8 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
   if constexpr (sizeof(T) == 2) {
     if (!mean_mode && G <= 8 && !g_score_cuda_core) {
       // tensor-core path: whole 32-row TMA boxes per CTA (device: per rounded up to 32)
-      static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-      if (!encode) {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult qr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
-            qr != cudaDriverEntryPointSuccess || !fn)
-          return cudaErrorNotSupported;
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-      }
+      const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+      if (!encode) return cudaErrorNotSupported;
       const int rows_hint = (min(nb_hint, maxb) + chunks - 1) / chunks;
       const int cap_tc = min(((rows_hint + kA5BoxRows - 1) / kA5BoxRows) * kA5BoxRows, 384);
       const size_t smem_tc = (size_t)cap_tc * 4 * kA5SlabRowB + 1024;
@@ -484,11 +477,7 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
       const bf16* qq = static_cast<const bf16*>(q);
 #define DSK_SCT(GG)                                                                                  \
   {                                                                                                  \
-    static bool attr = false;                                                                        \
-    if (!attr) {                                                                                     \
-      allow_max_dyn_smem(k_score_blocks_tc<GG>);                                                     \
-      attr = true;                                                                                   \
-    }                                                                                                \
+    allow_max_dyn_smem(k_score_blocks_tc<GG>);                                                       \
     launch_ex(k_score_blocks_tc<GG>, grid, 512, smem_tc, st, 1, tm, qq, nb, scores, Hq, Hkv, maxb,    \
               cap_tc);                                                                               \
     return post_launch("k_score_blocks_tc", st);                                                     \
@@ -507,11 +496,7 @@ static cudaError_t score_blocks_t(int G, const void* q, const void* dig, const i
   const T* dd = static_cast<const T*>(dig);
 #define DSK_SC(GG)                                                                                   \
   {                                                                                                  \
-    static bool attr = false;                                                                        \
-    if (!attr) {                                                                                     \
-      allow_max_dyn_smem(k_score_blocks<T, GG>);                                                     \
-      attr = true;                                                                                   \
-    }                                                                                                \
+    allow_max_dyn_smem(k_score_blocks<T, GG>);                                                       \
     launch_ex(k_score_blocks<T, GG>, grid, 512, smem, st, 1, qq, dd, nb, scores, Hq, Hkv, maxb, cap,   \
               mean_mode);                                                                            \
     break;                                                                                           \

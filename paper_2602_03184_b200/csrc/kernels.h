@@ -7,21 +7,28 @@ namespace dsk {
 
 struct WLEntry;
 
-int num_sms();
-int max_smem_optin();
+// Launch-time device queries and one-time kernel setup.  All caches are keyed
+// by the CURRENT device and guarded by one mutex (api.cu), so launchers are
+// thread-safe and correct when one process drives several GPUs.
+int num_sms();          // SMs of the current device
+int max_smem_optin();   // opt-in shared memory per block of the current device
 // Allow the largest dynamic smem the kernel can use (opt-in limit minus its
-// static smem).
+// static smem) and the full smem carveout; done once per (kernel, device).
+void prepare_kernel(const void* kern);
 template <typename F>
 inline void allow_max_dyn_smem(F* kern) {
-  cudaFuncAttributes a;
-  if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(kern)) == cudaSuccess)
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         max_smem_optin() - (int)a.sharedSizeBytes);
-  cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
-                       cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaGetLastError();
+  prepare_kernel(reinterpret_cast<const void*>(kern));
 }
+// Resident blocks per SM (cudaOccupancyMaxActiveBlocksPerMultiprocessor after
+// prepare_kernel), cached per (kernel, device, threads, smem); >= 1.
+int occupancy(const void* kern, int threads, size_t smem);
+template <typename F>
+inline int occupancy_of(F* kern, int threads, size_t smem) {
+  return occupancy(reinterpret_cast<const void*>(kern), threads, smem);
+}
+// cuTensorMapEncodeTiled through the runtime's driver entry point (resolved
+// once, thread-safe); nullptr if unavailable.
+void* tensor_map_encoder();
 // Launch with programmatic stream serialization (PDL) and an optional
 // cluster shape; DYNSPLIT_NO_PDL=1 disables PDL (A/B measurements).
 bool pdl_enabled();
@@ -56,21 +63,35 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 // attributed to the launcher that caused them.  Errors are recorded for
 // dynsplit_last_error().
 cudaError_t post_launch(const char* where, cudaStream_t st);
+// Empty kernel launched without PDL (dynsplit_stream_fence).
+cudaError_t launch_fence(cudaStream_t st);
 // decode (decode_kernels.cu, select_kernels.cu, attn_kernels.cu)
 cudaError_t launch_score_blocks(int dtype, int G, const void* q, const void* dig, const int32_t* nb,
                                 float* scores, int B, int Hq, int Hkv, int maxb, int nb_hint,
                                 int mean_mode, cudaStream_t st);  // nb_hint: expected blocks per sequence
 size_t select_smem_needed(int maxb, int G);  // (size_t)-1 if it cannot fit
+// S: capacity (the plan must tile [0, L) with L <= S); err: device error word
 cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const int32_t* nb,
-                          const int32_t* pf, int B, int Hq, int Hkv, int maxb, int max_sel,
+                          const int32_t* pf, int B, int Hq, int Hkv, int maxb, int S, int max_sel,
                           int max_wl, int P, int budget, int blk_lo, int blk_hi,
                           int32_t* sel_blocks, int32_t* n_sel, int32_t* marg, int32_t* keep,
-                          int32_t* wl_count, WLEntry* wl, cudaStream_t st);
+                          int32_t* wl_count, WLEntry* wl, int* err, cudaStream_t st);
 cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, const void* Vp,
                                const int16_t* pv, const int32_t* n_pages, const int32_t* wl_hdr,
                                const int32_t* wl_count, const WLEntry* wl, int dense, int B, int Hq, int Hkv,
                                int max_pages, int P, float scale, float* part_o, float* part_lse,
                                int* counters, float* o, float* lse, cudaStream_t st);
+// Fused decode layer (a5 + a6 + a7 + a8 in one kernel, fused_kernels.cu).
+// Returns cudaErrorNotSupported (nothing launched) when the shape or mode is
+// outside what the fused kernel handles; the caller then runs the three
+// kernels.  bar: per-(b, KV head) group-barrier words (zeroed workspace).
+cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q, const void* dig,
+                                const int32_t* bs, const int32_t* nb, const int32_t* pf, const void* Kp,
+                                const void* Vp, int B, int Hq, int Hkv, int maxb, int max_pages, int P,
+                                int budget, float scale, float* scores, int* counters, int* bar,
+                                float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
+                                int32_t* wl_hdr, int32_t* wl_count, WLEntry* wl, float* o, float* lse,
+                                int* err, cudaStream_t st);
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,
                          float* o, float* lse, cudaStream_t st);
 
@@ -81,13 +102,14 @@ cudaError_t launch_segment(const int32_t* tokens, const int32_t* delim_ids, int 
                            const uint8_t* w10, int B, int S, int C, int delta, int lam_num,
                            int lam_den, int maxb, int32_t* next_ws, int32_t* block_starts,
                            int32_t* n_blocks, cudaStream_t st);
+// L_end: the plan must tile [0, L_end); err: device error word or nullptr
 cudaError_t launch_map_pages(const int32_t* bs, const int32_t* nb, int B, int maxb, int maxp, int P,
-                             int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                             int32_t* n_pages, cudaStream_t st);
+                             int L_end, int32_t* page_first, int32_t* page_block, int16_t* page_valid,
+                             int32_t* n_pages, int* err, cudaStream_t st);
 cudaError_t launch_repack_digest(int dtype, const void* K, const void* V, const int32_t* bs,
                                  const int32_t* nb, const int32_t* pf, int B, int S, int Hkv,
                                  int maxb, int maxp, int P, int mean_mode, void* Kp, void* Vp, void* dig,
-                                 cudaStream_t st);
+                                 int* err, cudaStream_t st);
 
 // NEXT-1 decode-time append (append_kernels.cu)
 constexpr int kAppendMaxLayers = 64;
@@ -97,7 +119,7 @@ cudaError_t launch_plan_append(const int32_t* tokens, const int32_t* delim_ids, 
                                int B, int S, int maxb, int maxp, int C, int delta, int lam_num, int lam_den,
                                int P, int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
                                int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                               int32_t* n_pages, int32_t* ws, cudaStream_t st);
+                               int32_t* n_pages, int32_t* ws, int* err, cudaStream_t st);
 cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, const void* const* V_new,
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,

@@ -637,7 +637,7 @@ size_t score_ws_bytes(int Ls, int B, int S, int Hq) {
   return (size_t)Ls * B * Hq * S * 2 * sizeof(float);
 }
 
-static bool g_a1_mmasync = getenv("DYNSPLIT_A1_MMASYNC") != nullptr;
+static volatile bool g_a1_mmasync = getenv("DYNSPLIT_A1_MMASYNC") != nullptr;
 
 cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_ids, int n_ids,
                                     const void* Qs, const void* Ks, int Ls, int B, int S, int Hq,
@@ -649,15 +649,8 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
   float* part = static_cast<float*>(ws);
   int rows_per_tile;
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!mmasync && !encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+  const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!mmasync && !encode) return cudaErrorNotSupported;
   if (!mmasync) {
     // [Ls*B][S][H][d] bf16 -> dims (d, H, S, Ls*B); box (64, 1, 128, 1), 128-byte swizzle
     auto make_map = [&](CUtensorMap* m, const void* base, int H) -> bool {
@@ -672,11 +665,7 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
     CUtensorMap tmQ, tmK;
     if (!make_map(&tmQ, Qs, Hq) || !make_map(&tmK, Ks, Hkv)) return cudaErrorInvalidValue;
     const size_t smem = (size_t)(1 + kTcStage) * kTcTileBytes + 1024;  // cbuf fits in sK
-    static bool attr_tc = false;
-    if (!attr_tc) {
-      allow_max_dyn_smem(k_lse_band_tc);
-      attr_tc = true;
-    }
+    allow_max_dyn_smem(k_lse_band_tc);
     dim3 grid((S + kTcRows - 1) / kTcRows, Hq, Ls * B);
     k_lse_band_tc<<<grid, kTcThreads, smem, st>>>(tmQ, tmK, tokens, delim_ids, n_ids, B, S, Hq, Hkv, W, R,
                                                   alpha, scale_log2, part);
@@ -684,11 +673,7 @@ cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_
   } else {
     const size_t smem = (size_t)(kRowsPerCta + 2 * kKeyTile) * kLds * sizeof(bf16) +
                         kRowsPerCta * kMaxW * sizeof(float);
-    static bool attr_done = false;
-    if (!attr_done) {
-      allow_max_dyn_smem(k_lse_band);
-      attr_done = true;
-    }
+    allow_max_dyn_smem(k_lse_band);
     dim3 grid((S + kRowsPerCta - 1) / kRowsPerCta, Hq, Ls * B);
     k_lse_band<<<grid, 128, smem, st>>>(tokens, delim_ids, n_ids, static_cast<const bf16*>(Qs),
                                         static_cast<const bf16*>(Ks), B, S, Hq, Hkv, W, R, alpha,

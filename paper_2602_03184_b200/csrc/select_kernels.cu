@@ -93,9 +93,10 @@ template <int G>
 __global__ void __launch_bounds__(kSelNT, 1) k_select(
     const float* __restrict__ scores, const int32_t* __restrict__ block_starts,
     const int32_t* __restrict__ n_blocks, const int32_t* __restrict__ page_first, int Hq, int Hkv,
-    int maxb, int max_sel, int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
+    int maxb, int S, int max_sel, int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
     int32_t* __restrict__ sel_blocks, int32_t* __restrict__ n_sel, int32_t* __restrict__ marg_out,
-    int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl) {
+    int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl,
+    int* __restrict__ err) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem[];
   const int mb4 = (maxb + 3) & ~3;
@@ -117,7 +118,8 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   const int hk = blockIdx.x / G, b = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = 1 << Pshift;
-  const int nb = n_blocks[b];
+  const int nb_raw = n_blocks[b];
+  const int nb = min(max(nb_raw, 0), maxb);
   // every block of the sequence competes; worklist entries are emitted only
   // for blocks in the output range [olo, ohi) (a sequence-split shard)
   const int lo = 0, hi = nb;
@@ -130,12 +132,34 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
 
   stamp(0);
   // ---- 1. lengths (the resident plan), then -- after the preceding kernel
-  //         (PDL) -- the keys of this CTA's head, total
-  int t = 0;
+  //         (PDL) -- the keys of this CTA's head, total.  The plan must tile
+  //         [0, L <= S); a block longer than 255 pages or 65535 tokens
+  //         is beyond the 8/16-bit counters: such a sequence selects nothing.
+  int t = 0, bad = 0, bad_long = 0, npg = 0;
+  if (tid == 0) bad = nb_raw < 1 || nb_raw > maxb || bs[0] != 0 || bs[nb] > S;
   for (int i = tid; i < nr; i += kSelNT) {
     const int len = bs[lo + i + 1] - bs[lo + i];
+    bad |= len <= 0;
+    bad_long |= len > 0xffff || ((len + P - 1) >> Pshift) > 255;
     slen[i] = (uint16_t)len;
     t += len;
+    npg += (len + P - 1) >> Pshift;
+  }
+  __shared__ int s_npg;
+  if (tid == 0) s_npg = 0;
+  __syncthreads();
+  atomicAdd(&s_npg, npg);
+  const int any_bad = __syncthreads_or(bad), any_long = __syncthreads_or(bad_long);
+  if (any_bad || any_long || s_npg > max_wl) {
+    if (tid == 0) {
+      raise_err(err, any_bad ? kErrPlanCoverage : any_long ? kErrBlockTooLong : kErrPageCapacity);
+      const size_t o = (size_t)b * Hq + hk * G + c;
+      n_sel[o] = 0;
+      marg_out[o] = -1;
+      keep_out[o] = 0;
+      if (c == 0) wl_count[(size_t)b * Hkv + hk] = 0;
+    }
+    return;
   }
   stamp(1);
   pdl_trigger();
@@ -373,7 +397,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
       const bool sel = (s >> (8 + g)) & 1u;
       taken[g] = sel ? ((blk == m[g]) ? keep[g] : len) : 0;
       if (sel) {
-        if (sel_blocks) sel_blocks[((size_t)b * Hq + hk * G + g) * max_sel + v[g]] = blk;
+        if (sel_blocks && v[g] < max_sel) sel_blocks[((size_t)b * Hq + hk * G + g) * max_sel + v[g]] = blk;
         ++v[g];
       }
     }
@@ -396,6 +420,7 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select(
   if (tid == 0) {
     const size_t o = (size_t)b * Hq + hk * G + c;
     n_sel[o] = all_tot[c];
+    if (sel_blocks && all_tot[c] > max_sel) raise_err(err, kErrSelectOverflow);
     marg_out[o] = all[c] ? -1 : m[c];
     keep_out[o] = all[c] ? 0 : keep[c];
     if (c == 0) {
@@ -464,9 +489,10 @@ template <int G>
 __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
     const float* __restrict__ scores, const int32_t* __restrict__ block_starts,
     const int32_t* __restrict__ n_blocks, const int32_t* __restrict__ page_first, int Hq, int Hkv,
-    int maxb, int max_sel, int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
+    int maxb, int S, int max_sel, int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
     int32_t* __restrict__ sel_blocks, int32_t* __restrict__ n_sel, int32_t* __restrict__ marg_out,
-    int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl) {
+    int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl,
+    int* __restrict__ err) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* slen = reinterpret_cast<uint16_t*>(smem);
@@ -488,7 +514,8 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
   const int hk = blockIdx.x / G, b = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = 1 << Pshift;
-  const int nb = n_blocks[b];
+  const int nb_raw = n_blocks[b];
+  const int nb = min(max(nb_raw, 0), min(maxb, kRMax));
   const int olo = min(max(blk_lo, 0), nb), ohi = max(min(blk_hi, nb), olo);
   const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
   const int32_t* pf = page_first + (size_t)b * (maxb + 1);
@@ -501,7 +528,12 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   // ---- 0. resident plan (overlaps the preceding kernel under PDL)
   int len[kRK];
-  int tsum = 0;
+  int tsum = 0, npg = 0;
+  // the plan must tile [0, L <= S); blocks beyond the 8/16-bit
+  // counters (> 255 pages, > 65535 tokens) are rejected: such a sequence
+  // selects nothing and the error word says why
+  int bad = tid == 0 && (nb_raw < 1 || nb_raw > min(maxb, kRMax) || bs[0] != 0 || bs[nb] > S);
+  int bad_long = 0;
 #pragma unroll
   for (int k = 0; k < kRK; ++k) {
     const int i = k * kSelNT + tid;
@@ -509,12 +541,36 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
     if (i < nb) {
       len[k] = bs[i + 1] - bs[i];
       spf[i] = pf[i];
+      bad |= len[k] <= 0;
+      bad_long |= len[k] > 0xffff || ((len[k] + P - 1) >> Pshift) > 255;
+      npg += (len[k] + P - 1) >> Pshift;
     }
     slen[i] = (uint16_t)len[k];  // 0 beyond nb (the union pass reads whole words)
     tsum += len[k];
   }
   for (int j = tid; j < kBkt; j += kSelNT) HI[j] = 0;
   if (tid == 0) s_nc = 0;
+  {
+    npg = warp_sum_i(npg);
+    if (lane == 0) red_t[warp] = npg;
+    const int any_bad = __syncthreads_or(bad), any_long = __syncthreads_or(bad_long);
+    int pages = 0;
+#pragma unroll
+    for (int w = 0; w < kSelW; ++w) pages += red_t[w];
+    if (any_bad || any_long || pages > max_wl) {
+      if (tid == 0) {
+        raise_err(err, any_bad ? kErrPlanCoverage : any_long ? kErrBlockTooLong : kErrPageCapacity);
+        const size_t o = (size_t)b * Hq + hk * G + c;
+        n_sel[o] = 0;
+        marg_out[o] = -1;
+        keep_out[o] = 0;
+        if (c == 0) wl_count[(size_t)b * Hkv + hk] = 0;
+      }
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // match the arrive above
+      return;
+    }
+    __syncthreads();  // red_t is reused by the threshold pass
+  }
   stamp(1);
   pdl_trigger();
   pdl_wait();
@@ -713,12 +769,14 @@ __global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
 #pragma unroll
       for (int k = 0; k < kRK; ++k) {
         const uint32_t word = sbits[c][k * kSelW + warp];
-        if ((word >> lane) & 1u) out[spre[k * kSelW + warp] + __popc(word & lt)] = k * kSelNT + tid;
+        const int pos = spre[k * kSelW + warp] + __popc(word & lt);
+        if (((word >> lane) & 1u) && pos < max_sel) out[pos] = k * kSelNT + tid;
       }
     }
     if (tid == 0) {
       const size_t o = (size_t)b * Hq + hk * G + c;
       n_sel[o] = pre.y;
+      if (sel_blocks && pre.y > max_sel) raise_err(err, kErrSelectOverflow);
       marg_out[o] = all_c ? -1 : m_c;
       keep_out[o] = all_c ? 0 : keep_c;
     }
@@ -811,7 +869,7 @@ extern "C" int dynsplit_debug_select_timer(void* dev_ptr) {
 // select kernels); 0 restores the default dispatch.  Initial value from
 // DYNSPLIT_SELECT_GENERIC.
 namespace dsk {
-static bool g_select_generic = getenv("DYNSPLIT_SELECT_GENERIC") != nullptr;
+static volatile bool g_select_generic = getenv("DYNSPLIT_SELECT_GENERIC") != nullptr;
 }
 extern "C" int dynsplit_debug_select_generic(int on) {
   dsk::g_select_generic = on != 0;
@@ -826,40 +884,36 @@ size_t select_smem_needed(int maxb, int G) {
 
 template <int G>
 static cudaError_t run_select(int B, int Hkv, size_t smem, const float* scores, const int32_t* bs,
-                              const int32_t* nb, const int32_t* pf, int Hq, int maxb, int max_sel,
+                              const int32_t* nb, const int32_t* pf, int Hq, int maxb, int S, int max_sel,
                               int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
                               int32_t* sel_blocks, int32_t* n_sel, int32_t* marg, int32_t* keep,
-                              int32_t* wl_count, WLEntry* wl, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    allow_max_dyn_smem(k_select<G>);
-    allow_max_dyn_smem(k_select_reg<G>);
-    attr = true;
-  }
+                              int32_t* wl_count, WLEntry* wl, int* err, cudaStream_t st) {
   if (maxb <= kRMax && !g_select_generic) {
+    allow_max_dyn_smem(k_select_reg<G>);
     launch_ex(k_select_reg<G>, dim3(Hkv * G, B), dim3(kSelNT), select_reg_smem_bytes(G), st, G, scores,
-              bs, nb, pf, Hq, Hkv, maxb, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks,
-              n_sel, marg, keep, wl_count, wl);
+              bs, nb, pf, Hq, Hkv, maxb, S, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks,
+              n_sel, marg, keep, wl_count, wl, err);
     return post_launch("k_select_reg", st);
   }
+  allow_max_dyn_smem(k_select<G>);
   launch_ex(k_select<G>, dim3(Hkv * G, B), dim3(kSelNT), smem, st, G, scores, bs, nb, pf, Hq, Hkv,
-            maxb, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep,
-            wl_count, wl);
+            maxb, S, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep,
+            wl_count, wl, err);
   return post_launch("k_select", st);
 }
 
 cudaError_t launch_select(int G, const float* scores, const int32_t* bs, const int32_t* nb,
-                          const int32_t* pf, int B, int Hq, int Hkv, int maxb, int max_sel,
+                          const int32_t* pf, int B, int Hq, int Hkv, int maxb, int S, int max_sel,
                           int max_wl, int P, int budget, int blk_lo, int blk_hi,
                           int32_t* sel_blocks, int32_t* n_sel, int32_t* marg, int32_t* keep,
-                          int32_t* wl_count, WLEntry* wl, cudaStream_t st) {
+                          int32_t* wl_count, WLEntry* wl, int* err, cudaStream_t st) {
   const size_t smem = select_smem_needed(maxb, G);
   if (smem == (size_t)-1) return cudaErrorInvalidConfiguration;
   int Pshift = 0;
   while ((1 << Pshift) < P) ++Pshift;
 #define DSK_SEL(GG)                                                                                \
-  return run_select<GG>(B, Hkv, smem, scores, bs, nb, pf, Hq, maxb, max_sel, max_wl, Pshift,       \
-                        budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep, wl_count, wl, st)
+  return run_select<GG>(B, Hkv, smem, scores, bs, nb, pf, Hq, maxb, S, max_sel, max_wl, Pshift,    \
+                        budget, blk_lo, blk_hi, sel_blocks, n_sel, marg, keep, wl_count, wl, err, st)
   switch (G) {
     case 1: DSK_SEL(1);
     case 2: DSK_SEL(2);

@@ -22,7 +22,10 @@ LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit_debug.so" if os.environ.get("D
 OK = 0
 BF16, FP32 = 0, 1
 (OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN, OP_DECODE_LAYER,
- OP_APPEND) = range(7)
+ OP_APPEND, OP_MAP_PAGES, OP_REPACK) = range(9)
+# device error word bits (include/dynsplit.h DYNSPLIT_DEVERR_*)
+DEVERR_PLAN_COVERAGE, DEVERR_PLAN_MISMATCH, DEVERR_PAGE_CAPACITY = 1, 2, 4
+DEVERR_SELECT_OVERFLOW, DEVERR_BLOCK_TOO_LONG, DEVERR_SYNC_TIMEOUT = 8, 16, 32
 INT32_MAX = 0x7FFFFFFF
 
 
@@ -40,7 +43,7 @@ class Config(ctypes.Structure):
     _fields_ = [("W", ctypes.c_int32), ("R", ctypes.c_int32), ("alpha_pen", ctypes.c_float),
                 ("C", ctypes.c_int32), ("delta", ctypes.c_int32), ("lambda_num", ctypes.c_int32),
                 ("lambda_den", ctypes.c_int32), ("page_size", ctypes.c_int32),
-                ("digest_mode", ctypes.c_int32)]
+                ("digest_mode", ctypes.c_int32), ("page_cap", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -63,11 +66,14 @@ SIGNATURES = {
     "dynsplit_status_string": (ctypes.c_char_p, [_I]),
     "dynsplit_version": (ctypes.c_char_p, []),
     "dynsplit_last_error": (ctypes.c_char_p, []),
+    "dynsplit_read_device_error": (_I, [_P, _P]),
+    "dynsplit_clear_device_error": (_I, [_P, _P]),
+    "dynsplit_stream_fence": (_I, [_P]),
     "dynsplit_score_delimiters": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_weight_table": (_I, [_PS, _P, _P, _I, _P, _P, _P]),
     "dynsplit_segment": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
-    "dynsplit_map_pages": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, _P]),
-    "dynsplit_repack_digest": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "dynsplit_map_pages": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_repack_digest": (_I, [_PS, _PC, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_build_blocks": (_I, [_PS, _PC, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                    _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "dynsplit_score_blocks": (_I, [_PS, _PC, _P, _P, _P, _P, _P]),
@@ -103,6 +109,24 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def read_device_error(ws: torch.Tensor) -> int:
+    """Synchronise the current stream and return the device error word of a
+    workspace (DEVERR_* bits; 0 = no data-dependent error)."""
+    v = lib().dynsplit_read_device_error(_ptr(ws), _stream(ws.device))
+    if v < 0:
+        raise DynsplitError("dynsplit_read_device_error failed")
+    return int(v)
+
+
+def clear_device_error(ws: torch.Tensor) -> None:
+    _check(lib().dynsplit_clear_device_error(_ptr(ws), _stream(ws.device)), "clear_device_error")
+
+
+def stream_fence(device=None) -> None:
+    """dynsplit_stream_fence on the current stream (see include/dynsplit.h)."""
+    _check(lib().dynsplit_stream_fence(_stream(device)), "stream_fence")
 
 
 def _check(st: int, what: str):
@@ -241,8 +265,9 @@ def segment(tokens, delim_ids, w10, cfg: Config):
     return bs, nb
 
 
-def map_pages(block_starts, n_blocks, S: int, cfg: Config):
-    """Row a4 part 1.  -> (page_first, page_block, page_valid, n_pages)."""
+def map_pages(block_starts, n_blocks, S: int, cfg: Config, ws=None):
+    """Row a4 part 1.  -> (page_first, page_block, page_valid, n_pages).
+    ws: optional OP_MAP_PAGES workspace (device error word)."""
     B = block_starts.shape[0]
     shape = make_shape(B, S, 1, 1)
     mb, mp = max_blocks(S, cfg), max_pages(S, cfg)
@@ -253,12 +278,13 @@ def map_pages(block_starts, n_blocks, S: int, cfg: Config):
     npg = torch.empty(B, dtype=torch.int32, device=dev)
     _check(lib().dynsplit_map_pages(ctypes.byref(shape), ctypes.byref(cfg), _ptr(block_starts),
                                     _ptr(n_blocks), _ptr(pf), _ptr(pb), _ptr(pv), _ptr(npg),
-                                    _stream()), "map_pages")
+                                    _ptr(ws), ws.numel() if ws is not None else 0, _stream()), "map_pages")
     return pf, pb, pv, npg
 
 
-def repack_digest(K, V, block_starts, n_blocks, page_first, cfg: Config, out=None):
-    """Row a4 part 2.  K, V [B,S,Hkv,d] -> (Kp, Vp, digests)."""
+def repack_digest(K, V, block_starts, n_blocks, page_first, cfg: Config, out=None, ws=None):
+    """Row a4 part 2.  K, V [B,S,Hkv,d] -> (Kp, Vp, digests).
+    ws: optional OP_REPACK workspace (device error word)."""
     B, S, Hkv, d = K.shape
     shape = make_shape(B, S, Hkv, Hkv, d, 1, _dtype_code(K))
     mb, mp, P = max_blocks(S, cfg), max_pages(S, cfg), cfg.page_size
@@ -270,7 +296,8 @@ def repack_digest(K, V, block_starts, n_blocks, page_first, cfg: Config, out=Non
         Kp, Vp, dig = out
     _check(lib().dynsplit_repack_digest(ctypes.byref(shape), ctypes.byref(cfg), _ptr(K), _ptr(V),
                                         _ptr(block_starts), _ptr(n_blocks), _ptr(page_first),
-                                        _ptr(Kp), _ptr(Vp), _ptr(dig), _stream()), "repack_digest")
+                                        _ptr(Kp), _ptr(Vp), _ptr(dig), _ptr(ws),
+                                        ws.numel() if ws is not None else 0, _stream()), "repack_digest")
     return Kp, Vp, dig
 
 
@@ -403,7 +430,12 @@ class Selection:
 def _decode_shape(q, layer: PagedLayer) -> Shape:
     B, Hq, d = q.shape
     s = layer.shape
-    return make_shape(B, s.S, Hq, s.Hkv, d, 1, _dtype_code(q))
+    code = _dtype_code(q)
+    for name in ("Kp", "Vp", "digests"):
+        t = getattr(layer, name)
+        if t is not None and _dtype_code(t) != code:
+            raise DynsplitError(f"q is {q.dtype} but layer.{name} is {t.dtype}: the KV dtype must match")
+    return make_shape(B, s.S, Hq, s.Hkv, d, 1, code)
 
 
 def score_blocks(q, layer: PagedLayer, out=None):
