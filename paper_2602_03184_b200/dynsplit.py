@@ -532,11 +532,14 @@ def decode_layer(q, layer: PagedLayer, budget: int, scale: float = 0.0, out=None
     return o, lse, Selection(None, ns, mg, kp, wl, None)
 
 
-def merge_partials(o_parts, lse_parts):
-    """Row a8 standalone.  o_parts [n, rows, d], lse_parts [n, rows]."""
+def merge_partials(o_parts, lse_parts, out=None):
+    """Row a8 standalone.  o_parts [n, rows, d], lse_parts [n, rows] -> (o [rows, d], lse [rows])."""
     n, rows, d = o_parts.shape
-    o = torch.empty(rows, d, dtype=torch.float32, device=o_parts.device)
-    lse = torch.empty(rows, dtype=torch.float32, device=o_parts.device)
+    if out is None:
+        o = torch.empty(rows, d, dtype=torch.float32, device=o_parts.device)
+        lse = torch.empty(rows, dtype=torch.float32, device=o_parts.device)
+    else:
+        o, lse = out
     _check(lib().dynsplit_merge_partials(_ptr(o_parts), _ptr(lse_parts), n, rows, d, _ptr(o),
                                          _ptr(lse), _stream()), "merge_partials")
     return o, lse

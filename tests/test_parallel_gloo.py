@@ -114,3 +114,50 @@ def test_seq_split_world2_equals_single_process():
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res), res
     assert res[0][2] == res[1][2]
+
+
+def _worker_index(rank, world, port, out_q):
+    """score_index + gather_global_scores: every rank writes its local block
+    scores with its own row stride into its send buffer; after the gather each
+    global (head, block) must hold exactly that rank's value, blocks past the
+    sequence -inf, identical on every rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        toks = G.tokens(41, 9000)
+        starts = O.segment(toks, G.T7_IDS, G.T7_W10, 32, 14)
+        nb = len(starts) - 1
+        ranges = PAR.seq_split_ranges(starts, nb, world)
+        Hq, mb_glob = 5, nb + 7
+        strides = [max(1, (starts[hi] - starts[lo]) // 18 + 1) for lo, hi in ranges]
+        send_len = Hq * max(strides)
+        idx = PAR.score_index(ranges, strides, Hq, send_len, mb_glob)
+        # the "true" global scores: value = 1000 h + block + 0.25
+        truth = np.full((Hq, mb_glob), -np.inf)
+        for h in range(Hq):
+            truth[h, :nb] = 1000 * h + np.arange(nb) + 0.25
+        lo, hi = ranges[rank]
+        send = torch.full((send_len,), 7.5, dtype=torch.float64)     # junk beyond the rank's blocks
+        for h in range(Hq):
+            send[h * strides[rank]: h * strides[rank] + hi - lo] = torch.from_numpy(truth[h, lo:hi])
+        gathered = torch.full((world * send_len + 1,), float("-inf"), dtype=torch.float64)
+        out = torch.empty(Hq, mb_glob, dtype=torch.float64)
+        PAR.gather_global_scores(send, gathered, idx, out)
+        out_q.put((rank, bool(np.array_equal(out.numpy(), truth))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_score_index_gather(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_index, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res
