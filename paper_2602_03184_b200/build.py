@@ -22,7 +22,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libdynsplit.so")
 SOURCES = ["api.cu", "decode_kernels.cu", "select_kernels.cu", "attn_kernels.cu", "build_kernels.cu",
            "score_kernels.cu", "append_kernels.cu", "fused_kernels.cu"]
-HEADERS = ["common.cuh", "kernels.h"]
+HEADERS = ["common.cuh", "kernels.h", "attn_core.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

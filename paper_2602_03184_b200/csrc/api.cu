@@ -204,9 +204,12 @@ inline WorklistView worklist_view(void* wl, const dynsplit_shape* s) {
 }
 
 // ---- workspace layouts: [kWsHdr header: device error word][body]
+// scores rows padded to 32 floats (the fused decode kernel's row stride)
+inline int score_stride(const dynsplit_shape* s, const dynsplit_config* c) {
+  return (dynsplit_max_blocks(s->S, c) + 31) & ~31;
+}
 size_t select_body(const dynsplit_shape* s, const dynsplit_config* c) {
-  const int maxb = dynsplit_max_blocks(s->S, c);
-  return align_up((size_t)s->B * s->Hq * maxb * 4) + align_up((size_t)s->B * s->Hq * 16);
+  return align_up((size_t)s->B * s->Hq * score_stride(s, c) * 4) + align_up((size_t)s->B * s->Hq * 16);
 }
 size_t select_ws(const dynsplit_shape* s, const dynsplit_config* c) { return kWsHdr + select_body(s, c); }
 // Decode body: [split-merge counters, fixed kMaxCounters ints][part_o][part_lse].
@@ -228,8 +231,10 @@ size_t build_ws(const dynsplit_shape* s) {
   return kWsHdr + score_body(s) + align_up((size_t)s->B * s->S * 4) + segment_body(s);
 }
 // dynsplit_decode_layer: header, decode body (counters at a fixed offset), select body.
+// (+ the fused kernel's moments / selection bitmasks / marginal info)
 size_t layer_ws(const dynsplit_shape* s, const dynsplit_config* c) {
-  return kWsHdr + decode_body(s) + select_body(s, c);
+  return kWsHdr + decode_body(s) + select_body(s, c) +
+         align_up(fused_scratch_bytes(s->B, s->Hq, dynsplit_max_blocks(s->S, c)));
 }
 size_t step_host_extra(const dynsplit_shape* s) {
   return align_up((size_t)s->B * s->Hq * kD * esize(s)) + align_up((size_t)s->B * s->Hq * kD * 4) +
@@ -648,11 +653,14 @@ static dynsplit_status decode_layer_impl(const dynsplit_shape* s, const dynsplit
     float* part_o = reinterpret_cast<float*>(dec_body + kMaxCounters * 4);
     float* part_lse = reinterpret_cast<float*>(dec_body + kMaxCounters * 4 +
                                                align_up((size_t)s->B * s->Hq * kMaxSplit * kD * 4));
+    char* fscratch = body + decode_body(s) + select_body(s, c);
+    const int nb_hint = (int)(((int64_t)s->S * 5 + 4 * c->C - 1) / (4 * c->C));
     const cudaError_t e = launch_decode_fused(
         s->kv_dtype, c->digest_mode, s->Hq / s->Hkv, q, digests, block_starts, n_blocks, page_first, Kp, Vp,
-        s->B, s->Hq, s->Hkv, maxb, dynsplit_max_pages(s->S, c), c->page_size, budget, scale, sc, counters,
-        counters + kMaxCounters / 2, part_o, part_lse, n_sel, marginal_block, marginal_keep, v.hdr, v.count,
-        v.entries, o, lse, err_word(ws), static_cast<cudaStream_t>(stream));
+        s->B, s->Hq, s->Hkv, maxb, dynsplit_max_pages(s->S, c), s->S, c->page_size, budget, nb_hint, scale, sc,
+        score_stride(s, c), fscratch, counters, counters + kMaxCounters / 2, part_o, part_lse, n_sel,
+        marginal_block, marginal_keep, v.count, v.entries, o, lse, err_word(ws),
+        static_cast<cudaStream_t>(stream));
     if (e != cudaErrorNotSupported) return cuda_status(e);
   }
   DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));

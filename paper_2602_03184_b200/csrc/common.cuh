@@ -1,5 +1,6 @@
 // Shared device helpers for the DynSplit-KV sm_100a kernels.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -92,6 +93,11 @@ DSK_DEVICE void split_bf16x2(uint32_t w, unsigned short& lo, unsigned short& hi)
 DSK_DEVICE uint32_t float_key(float f) {
   uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+DSK_DEVICE float key_to_float(uint32_t k) {
+  const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
 }
 
 // ---------------------------------------------------------------- warp utils
@@ -207,6 +213,11 @@ DSK_DEVICE uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+DSK_DEVICE uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 // Programmatic dependent launch: wait until the preceding kernel in the
 // stream has completed (and its writes are visible) / allow the next kernel
 // to be scheduled.  Both are no-ops for a normal launch.
@@ -225,6 +236,16 @@ DSK_DEVICE void mma_rows8(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, 
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// TMA 2-D tensor copy global -> shared (box given by the tensor map),
+// completion signalled on `bar`.
+DSK_DEVICE void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 DSK_DEVICE void named_bar_sync(int id, int nthreads) {

@@ -278,13 +278,6 @@ static volatile bool g_score_cuda_core = getenv("DYNSPLIT_A5_CUDA_CORE") != null
 constexpr int kA5BoxRows = 32;  // rows per TMA box
 constexpr int kA5SlabRowB = 128;  // bytes per row of one 64-dim slab
 
-DSK_DEVICE void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
 
 template <int G>
 __global__ void __launch_bounds__(512, 1) k_score_blocks_tc(const __grid_constant__ CUtensorMap tmD,

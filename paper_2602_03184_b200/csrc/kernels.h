@@ -84,14 +84,17 @@ cudaError_t launch_decode_attn(int dtype, int G, const void* q, const void* Kp, 
 // Fused decode layer (a5 + a6 + a7 + a8 in one kernel, fused_kernels.cu).
 // Returns cudaErrorNotSupported (nothing launched) when the shape or mode is
 // outside what the fused kernel handles; the caller then runs the three
-// kernels.  bar: per-(b, KV head) group-barrier words (zeroed workspace).
+// kernels.  scores: [B][Hq][sstride] fp32 (sstride >= maxb rounded up to 32);
+// fscratch: fused_scratch_bytes(); bar: 4 zero-initialised group-barrier
+// words per (b, KV head); nb_hint: expected blocks per sequence.
+size_t fused_scratch_bytes(int B, int Hq, int maxb);
 cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q, const void* dig,
                                 const int32_t* bs, const int32_t* nb, const int32_t* pf, const void* Kp,
-                                const void* Vp, int B, int Hq, int Hkv, int maxb, int max_pages, int P,
-                                int budget, float scale, float* scores, int* counters, int* bar,
-                                float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
-                                int32_t* wl_hdr, int32_t* wl_count, WLEntry* wl, float* o, float* lse,
-                                int* err, cudaStream_t st);
+                                const void* Vp, int B, int Hq, int Hkv, int maxb, int max_pages, int S, int P,
+                                int budget, int nb_hint, float scale, float* scores, int sstride,
+                                void* fscratch, int* counters, int* bar, float* part_o, float* part_lse,
+                                int32_t* n_sel, int32_t* marg, int32_t* keep, int32_t* wl_count, WLEntry* wl,
+                                float* o, float* lse, int* err, cudaStream_t st);
 cudaError_t launch_merge(const float* o_parts, const float* lse_parts, int n_parts, int rows, int d,
                          float* o, float* lse, cudaStream_t st);
 

@@ -56,10 +56,6 @@ DSK_DEVICE void stamp(int k) {
 #endif
 }
 
-DSK_DEVICE float key_to_float(uint32_t k) {
-  const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-  return __uint_as_float(u);
-}
 DSK_DEVICE int bucket_of(uint32_t k, float mn, float inv) {
   return min(max((int)((key_to_float(k) - mn) * inv), 0), kBkt - 1);
 }
