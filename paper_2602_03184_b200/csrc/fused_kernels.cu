@@ -69,6 +69,7 @@ constexpr int kFSlabRowB = 128;      // bytes per row of one 64-dim digest slab
 constexpr int kFMaxGroups = 1024;    // (b, KV head) groups x NS bound of the moment slots
 constexpr int kBandCap = 256;        // band entries resolved by one warp (8 per lane)
 constexpr int kSlot = 64;            // band entries one CTA publishes per head
+constexpr int kSub = 16;             // sub-bands of [t_lo, t_hi] (per-range token weights)
 
 // Optional phase timestamps (debug builds; dynsplit_debug_fused_timer): the
 // buffer pointer is read once per kernel into dbgp (a global load per stamp
@@ -336,117 +337,171 @@ DSK_DEVICE void f_select_head(const uint32_t (&key)[kFKPT], const int32_t* sbs, 
 template <int G>
 struct SelScratch2 {  // static shared memory of the band selection
   float tlo[G], thi[G];
-  int rwhi[kFNW][G], rwbd[kFNW][G], nsub[kFNW][G];
+  int rwhi[kFNW][G], rwbd[kFNW][G];
   int bcnt[G];
+  int wsub[G * kSub];
   int4 sel[G];  // marginal, keep, threshold key, flags (1 = all fit, 2 = slow path)
 };
 
-// One warp: the marginal block of a head inside its band (cnt <= kBandCap
-// entries (key, block) with key in [t_lo, t_hi]), where `need` tokens of the
-// band are still to be taken in the order (key desc, block asc).  Lane l
-// holds entries l + 32 r.  Weighted MSB radix select on the 32-bit
-// keys, two bits per step from the highest bit in which the band's keys
-// differ (each step: the weights of the entries matching the prefix with the
-// two bits 11, 10 and 01, three warp reductions), then equal keys in block
-// order.  Sets the selection bits of the band's selected blocks (bits: the
-// head's words).
-DSK_DEVICE void f_band_select(const uint2* band, int c, const int32_t* sbs, int need, uint32_t* bits, int& m,
+// One warp: the marginal block of a head inside its band (c <= kBandCap
+// entries (key, block | sub-band << 24) with key in [t_lo, t_hi]), where
+// `need` tokens of the band are still to be taken in the order (key desc,
+// block asc).  Lane l holds entries l + 32 r; lane j < kSub holds wsb, the
+// token weight of sub-band j (summed over the group's ranges).  A suffix scan
+// of the sub-band weights gives the sub-band where `need` is reached (the
+// sub-bands above it are taken whole); its entries stay live.  While more than
+// 32 are live, the live key range [lo, hi] is cut again into 16 sub-bands by
+// a monotone integer map (umulhi(key - lo, scale)) and 16 warp reductions; <=
+// 32 live entries are ranked exactly against each other (all pairs by
+// shuffles, order (key desc, block asc)); equal keys across more than 32
+// entries are taken in block order.  Returns the marginal block m, its kept
+// tokens and its key T, and sets the selection bits of the band's selected
+// blocks (bits: the head's words).
+DSK_DEVICE void f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, int need, uint32_t* bits, int& m,
                               int& keep, uint32_t& T) {
   const int lane = threadIdx.x & 31;
   constexpr int J = kBandCap / 32;
-  uint32_t k[J];
+  uint32_t k[J], sbr[J];
   int ix[J], ln[J];
-  uint32_t valid = 0, orv = 0u, andv = 0xffffffffu;
-  uint2 v[J];
+  uint32_t valid = 0;
+  {
+    uint2 v[J];
 #pragma unroll
-  for (int r = 0; r < J; ++r) {
-    const int e = lane + 32 * r;
-    v[r] = e < c ? band[e] : make_uint2(0u, 0u);
-  }
-#pragma unroll
-  for (int r = 0; r < J; ++r) {
-    const int e = lane + 32 * r;
-    k[r] = v[r].x;
-    ix[r] = (int)v[r].y;
-    const bool ok = e < c;
-    ln[r] = ok ? blen(sbs, ix[r]) : 0;
-    valid |= ok ? 1u << r : 0u;
-    orv |= ok ? k[r] : 0u;
-    andv &= ok ? k[r] : 0xffffffffu;
-  }
-  orv = __reduce_or_sync(0xffffffffu, orv);
-  andv = __reduce_and_sync(0xffffffffu, andv);
-  const uint32_t diff = orv ^ andv;
-  const uint32_t low = diff ? (0xffffffffu >> __clz(diff)) : 0u;  // bits at and below the top differing bit
-  uint32_t prefix = andv & ~low, mask = ~low;
-  int nr = need;
-  int bit = diff ? 31 - __clz(diff) : -1;
-#pragma unroll 1
-  for (; bit >= 1; bit -= 2) {
-    // bits (bit, bit - 1): candidates 11 > 10 > 01 > 00 in key order
-    const uint32_t m2 = mask | (3u << (bit - 1));
-    const uint32_t c3 = prefix | (3u << (bit - 1)), c2 = prefix | (2u << (bit - 1)), c1 = prefix | (1u << (bit - 1));
-    int w3 = 0, w2 = 0, w1 = 0;
+    for (int r = 0; r < J; ++r) v[r] = lane + 32 * r < c ? band[lane + 32 * r] : make_uint2(0u, 0u);
 #pragma unroll
     for (int r = 0; r < J; ++r) {
-      const uint32_t km = k[r] & m2;
-      const int l = ((valid >> r) & 1u) ? ln[r] : 0;
-      w3 += km == c3 ? l : 0;
-      w2 += km == c2 ? l : 0;
-      w1 += km == c1 ? l : 0;
+      const bool ok = lane + 32 * r < c;
+      k[r] = v[r].x;
+      ix[r] = (int)(v[r].y & 0xffffffu);
+      sbr[r] = v[r].y >> 24;
+      ln[r] = ok ? blen(sbs, ix[r]) : 0;
+      valid |= ok ? 1u << r : 0u;
     }
-    w3 = __reduce_add_sync(0xffffffffu, w3);
-    w2 = __reduce_add_sync(0xffffffffu, w2);
-    w1 = __reduce_add_sync(0xffffffffu, w1);
-    if (w3 >= nr) {
-      prefix = c3;
-    } else if (w3 + w2 >= nr) {
-      nr -= w3;
-      prefix = c2;
-    } else if (w3 + w2 + w1 >= nr) {
-      nr -= w3 + w2;
-      prefix = c1;
-    } else {
-      nr -= w3 + w2 + w1;
-    }
-    mask = m2;
   }
-  if (bit == 0) {  // one bit left
-    const uint32_t m2 = mask | 1u, c1 = prefix | 1u;
-    int w = 0;
+  // the published sub-band weights: suffix scan from the top sub-band
+  int nr0 = need;
+  uint32_t live = 0;
+  {
+    int suf = lane < kSub ? wsb : 0;
 #pragma unroll
-    for (int r = 0; r < J; ++r) w += ((valid >> r) & 1u) && (k[r] & m2) == c1 ? ln[r] : 0;
-    w = __reduce_add_sync(0xffffffffu, w);
-    if (w >= nr) prefix = c1;
-    else nr -= w;
+    for (int o = 1; o < kSub; o <<= 1) {
+      const int t = __shfl_down_sync(0xffffffffu, suf, o);
+      if (lane + o < kSub) suf += t;
+    }
+    const uint32_t reach = __ballot_sync(0xffffffffu, lane < kSub && suf >= need);
+    const int sstar = reach ? 31 - __clz(reach) : 0;
+    nr0 = need - __shfl_sync(0xffffffffu, suf - wsb, sstar);
+#pragma unroll
+    for (int r = 0; r < J; ++r)
+      if (((valid >> r) & 1u) && sbr[r] == (uint32_t)sstar) live |= 1u << r;
   }
-  T = prefix;
-  // the entries with key == T, in block order, hold the remaining nr tokens
-  uint32_t taken = 0;
+  int nr = nr0;
   m = -1;
   keep = 0;
+  T = 0;
 #pragma unroll 1
-  for (int it = 0; it < kBandCap; ++it) {
-    uint32_t mi = 0xffffffffu;
+  for (int round = 0; round < 8; ++round) {
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    int nl = 0;
 #pragma unroll
     for (int r = 0; r < J; ++r)
-      if (((valid & ~taken) >> r) & 1u && k[r] == T) mi = min(mi, (uint32_t)ix[r]);
-    mi = __reduce_min_sync(0xffffffffu, mi);
-    if (mi == 0xffffffffu) break;  // cannot happen when the band holds the marginal block
-    int l = 0;
-#pragma unroll
-    for (int r = 0; r < J; ++r)
-      if (((valid & ~taken) >> r) & 1u && k[r] == T && (uint32_t)ix[r] == mi) {
-        l = ln[r];
-        taken |= 1u << r;
+      if ((live >> r) & 1u) {
+        lo = min(lo, k[r]);
+        hi = max(hi, k[r]);
+        ++nl;
       }
-    l = __reduce_add_sync(0xffffffffu, l);
-    if (l >= nr) {
-      m = (int)mi;
-      keep = nr;
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    nl = __reduce_add_sync(0xffffffffu, nl);
+    if (nl <= 32 || lo == hi) {
+      // exact rank of the live entries: compact them to one per lane (through
+      // this head's band list, no longer needed), then all pairs
+      int pos = 0;
+      {
+        int mine = __popc(live);
+        const int incl = warp_incl_scan(mine);
+        pos = incl - mine;
+      }
+      __syncwarp();
+      if (nl <= 32) {
+#pragma unroll
+        for (int r = 0; r < J; ++r)
+          if ((live >> r) & 1u) band[pos++] = make_uint2(k[r], (uint32_t)ix[r]);  // (sub-band bits dropped)
+        __syncwarp();
+        const uint2 e = lane < nl ? band[lane] : make_uint2(0u, 0u);
+        const int el = lane < nl ? blen(sbs, (int)e.y) : 0;
+        int before = 0;
+        for (int j2 = 0; j2 < nl; ++j2) {
+          const uint32_t ok2 = __shfl_sync(0xffffffffu, e.x, j2), oi = __shfl_sync(0xffffffffu, e.y, j2);
+          const int ol = __shfl_sync(0xffffffffu, el, j2);
+          before += (ok2 > e.x || (ok2 == e.x && oi < e.y)) ? ol : 0;
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, lane < nl && before < nr && before + el >= nr);
+        const int src = hit ? __ffs(hit) - 1 : 0;
+        m = (int)__shfl_sync(0xffffffffu, e.y, src);
+        T = __shfl_sync(0xffffffffu, e.x, src);
+        keep = nr - __shfl_sync(0xffffffffu, before, src);
+        if (!hit) m = -1;  // cannot happen when the band holds the marginal block
+      } else {
+        // more than 32 entries with one key: block order
+        T = lo;
+        uint32_t taken = 0;
+#pragma unroll 1
+        for (int it = 0; it < kBandCap; ++it) {
+          uint32_t mi = 0xffffffffu;
+#pragma unroll
+          for (int r = 0; r < J; ++r)
+            if (((live & ~taken) >> r) & 1u) mi = min(mi, (uint32_t)ix[r]);
+          mi = __reduce_min_sync(0xffffffffu, mi);
+          if (mi == 0xffffffffu) break;
+          int l = 0;
+#pragma unroll
+          for (int r = 0; r < J; ++r)
+            if (((live & ~taken) >> r) & 1u && (uint32_t)ix[r] == mi) {
+              l = ln[r];
+              taken |= 1u << r;
+            }
+          l = __reduce_add_sync(0xffffffffu, l);
+          if (l >= nr) {
+            m = (int)mi;
+            keep = nr;
+            break;
+          }
+          nr -= l;
+        }
+      }
       break;
     }
-    nr -= l;
+    // 16 sub-bands of [lo, hi]: sb = floor((key - lo) * scale / 2^32) < 16
+    const uint64_t span = (uint64_t)(hi - lo) + 1u;
+    const uint64_t sc64 = (((uint64_t)16 << 32) / span) - 1u;
+    const uint32_t scale = sc64 > 0xffffffffull ? 0xffffffffu : (uint32_t)sc64;  // (rare path: 64-bit division)
+    uint32_t sbq[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) sbq[r] = __umulhi(k[r] - lo, scale);
+    int wsb = 0;  // lane j < 16: token weight of sub-band j
+#pragma unroll
+    for (int j2 = 0; j2 < 16; ++j2) {
+      int w = 0;
+#pragma unroll
+      for (int r = 0; r < J; ++r) w += (((live >> r) & 1u) && sbq[r] == (uint32_t)j2) ? ln[r] : 0;
+      w = __reduce_add_sync(0xffffffffu, w);
+      if (lane == j2) wsb = w;
+    }
+    // suffix scan from sub-band 15 down: the first sub-band where need is reached
+    int suf = lane < 16 ? wsb : 0;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const int t = __shfl_down_sync(0xffffffffu, suf, o);
+      if (lane + o < 16) suf += t;
+    }
+    const uint32_t reach = __ballot_sync(0xffffffffu, lane < 16 && suf >= nr);
+    const int sstar = 31 - __clz(reach);  // the highest sub-band whose suffix reaches need
+    const int above = __shfl_sync(0xffffffffu, suf - wsb, sstar);
+    nr -= above;
+#pragma unroll
+    for (int r = 0; r < J; ++r)
+      if (sbq[r] != (uint32_t)sstar) live &= ~(1u << r);
   }
   // selection bits of the band's selected blocks (the blocks above t_hi are set already)
 #pragma unroll
@@ -462,7 +517,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     const int32_t* __restrict__ page_first, const bf16* __restrict__ Kp, const bf16* __restrict__ Vp, int Hq,
     int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int cap, int ent_cap, int nwords,
     int sstride, size_t region_a, int per_cap, float scale_log2, float* __restrict__ scores,
-    float4* __restrict__ mom, int4* __restrict__ cls_w, uint2* __restrict__ cls_band, uint32_t* __restrict__ gbits,
+    float4* __restrict__ mom, int4* __restrict__ cls_w, int* __restrict__ cls_sub, uint2* __restrict__ cls_band,
+    uint32_t* __restrict__ gbits,
     int* __restrict__ counters, unsigned* __restrict__ gbar, float* __restrict__ part_o,
     float* __restrict__ part_lse, int32_t* __restrict__ n_sel_out, int32_t* __restrict__ marg_out,
     int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl,
@@ -564,6 +620,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     bad_long |= len > 0xffff || ((len + P - 1) >> Pshift) > 255;
     npg += (len + P - 1) >> Pshift;
   }
+  for (int j = tid; j < G * kSub; j += kFNT) S2.wsub[j] = 0;
   const int any_bad = __syncthreads_or(bad), any_long = __syncthreads_or(bad_long);
   {
     const int c = warp_sum_i(npg);
@@ -606,6 +663,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     reinterpret_cast<uint4*>(s_q)[tid] =
         __ldca(reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD) + tid);
   __syncthreads();
+  fstamp(14);
   {
     const int g = lane >> 2, t = lane & 3;
     uint32_t a0[16], a2[16];
@@ -647,6 +705,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         stage(r0, c_n);
       }
       mbar_wait(&bar, phase);
+      if (r0 == 0) fstamp(15);
       for (int grp = warp; grp * 8 < c_n; grp += kFNW) {
         float c[4] = {0.f, 0.f, 0.f, 0.f};
         const int r = grp * 8 + lr;
@@ -693,8 +752,6 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     }
     mom[((size_t)bh * NS + split) * G + tid] = make_float4((float)n, a, c2, 0.f);
   }
-  // region A is rewritten by TMA (async proxy) in phase 2 after these generic-proxy reads
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();  // every score and moment write of the CTA precedes the arrive
   fstamp(3);
 
@@ -746,10 +803,14 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   }
   __syncthreads();
   // classification of this CTA's range: warp w takes head g = w % G and the
-  // range's words w / G, w / G + 8 / G, ...; lane l is block lo + 32 word + l
+  // range's words w / G, w / G + 8 / G, ...; lane l is block lo + 32 word + l.
+  // A band entry also gets its sub-band sb = floor(16 (x - t_lo) / (t_hi -
+  // t_lo)) clamped to [0, 16) -- monotone in x, the same map in every CTA --
+  // and the range's token weight per (head, sub-band) is published.
   {
     const int g2 = warp % G;
     const float tl = S2.tlo[g2], th = S2.thi[g2];
+    const float sbk = (float)kSub / (th - tl);
     const int nws = (n + 31) >> 5;
     int whi = 0, wbd = 0;
     const uint32_t lt = (1u << lane) - 1u;
@@ -761,8 +822,9 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       const float x = ok ? ssl[g2 * per_cap + il] : -CUDART_INF_F;
       const int len = ok ? blen(sbs, i) : 0;
       const bool above = x > th, atlo = x >= tl;
+      const bool inb = atlo && !above;
       whi += above ? len : 0;
-      wbd += (atlo && !above) ? len : 0;
+      wbd += inb ? len : 0;
       const uint32_t ab = __ballot_sync(0xffffffffu, above);
       const uint32_t bb = __ballot_sync(0xffffffffu, atlo) & ~ab;
       if (lane == 0) gbits[((size_t)bh * G + g2) * nwords + (lo >> 5) + wl] = ab;
@@ -771,7 +833,11 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         if (lane == 0) base = atomicAdd(&S2.bcnt[g2], __popc(bb));
         base = __shfl_sync(0xffffffffu, base, 0);
         const int pos = base + __popc(bb & lt);
-        if (((bb >> lane) & 1u) && pos < kSlot) myband[pos] = make_uint2(float_key(x), (uint32_t)i);
+        if (inb) {
+          const int sb = min(max((int)((x - tl) * sbk), 0), kSub - 1);
+          atomicAdd(&S2.wsub[g2 * kSub + sb], len);
+          if (pos < kSlot) myband[pos] = make_uint2(float_key(x), (uint32_t)i | ((uint32_t)sb << 24));
+        }
       }
     }
     whi = warp_sum_i(whi);
@@ -790,6 +856,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     }
     cls_w[((size_t)bh * NS + split) * G + tid] = make_int4(a, c, S2.bcnt[tid], 0);
   }
+  for (int j = tid; j < G * kSub; j += kFNT) cls_sub[((size_t)bh * NS + split) * G * kSub + j] = S2.wsub[j];
   __syncthreads();  // every published word / entry / weight precedes the arrive
   fstamp(5);
   if (warp == 0) {
@@ -800,8 +867,10 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     if (lane == 0 && split == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(gb), "r"(s_target) : "memory");
   }
   __syncthreads();
-  // gather: the above words of every range, and per head (warp g) the
-  // weights and the band entries of every range into one list
+  fstamp(13);
+  // gather: the above words of every range (all threads), and per head
+  // (warp g) the weights, the sub-band weights and the band entries of every
+  // range; warp g then resolves head g's marginal block (f_band_select)
   for (int t = tid; t < nwu; t += kFNT)
 #pragma unroll
     for (int g2 = 0; g2 < G; ++g2) sbits[g2 * nwords + t] = __ldcg(gbits + ((size_t)bh * G + g2) * nwords + t);
@@ -811,6 +880,23 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     int4 c0 = make_int4(0, 0, 0, 0), c1 = make_int4(0, 0, 0, 0);
     if (lane < NS) c0 = __ldcg(cls_w + ((size_t)bh * NS + lane) * G + g2);
     if (lane + 32 < NS) c1 = __ldcg(cls_w + ((size_t)bh * NS + lane + 32) * G + g2);
+    // the token weight of sub-band j over every range: lane l sums sub-band
+    // l % 16 over the ranges r = l / 16 (mod 2), all loads in flight at once
+    // (NS <= 64: <= 32 per lane), then lanes l and l + 16 are added
+    int wsb = 0;
+    {
+      const int* src = cls_sub + ((size_t)bh * NS * G + g2) * kSub + (lane & (kSub - 1));
+      const size_t rs = (size_t)G * kSub;  // one range further
+      int v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int r = 2 * q + (lane >> 4);
+        v[q] = r < NS ? __ldcg(src + r * rs) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 32; ++q) wsb += v[q];
+      wsb += __shfl_down_sync(0xffffffffu, wsb, 16);
+    }
     const int over = __any_sync(0xffffffffu, c0.z > kSlot || c1.z > kSlot);
     const int n0 = min(c0.z, kSlot), n1 = min(c1.z, kSlot);
     const int i0 = warp_incl_scan(n0);
@@ -818,55 +904,37 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     const int i1 = warp_incl_scan(n1) + t0;
     const int nband = __shfl_sync(0xffffffffu, i1, 31);
     const int W_hi = warp_sum_i(c0.x + c1.x), W_bd = warp_sum_i(c0.y + c1.y);
-    // entry p = lane + 32 j of the concatenated list: range r = the first with
-    // inclusive prefix > p (binary search over the lanes' prefixes), all loads
-    // issued before any store
-    constexpr int J = kBandCap / 32;
-    uint2 ev[J];
+    // copy: lane l moves the entries of ranges l and l + 32 to their place in
+    // the concatenated list (up to 16 + 16 loads in flight before the stores)
+    {
+      const int d0 = i0 - n0, d1 = i1 - n1;
+      const uint2* s0 = cls_band + (((size_t)bh * NS + (lane < NS ? lane : 0)) * G + g2) * kSlot;
+      const uint2* s1 = cls_band + (((size_t)bh * NS + (lane + 32 < NS ? lane + 32 : 0)) * G + g2) * kSlot;
+#pragma unroll 1
+      for (int e0 = 0; e0 < max(n0, n1); e0 += 16) {
+        uint2 ev0[16], ev1[16];
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int pp = lane + 32 * j;
-      // fixed trip count (every lane takes part in every shuffle): 6 halvings cover NS <= 64
-      int lo_r = 0, hi_r = NS - 1;
+        for (int e2 = 0; e2 < 16; ++e2) {
+          ev0[e2] = e0 + e2 < n0 ? __ldcg(s0 + e0 + e2) : make_uint2(0u, 0u);
+          ev1[e2] = e0 + e2 < n1 ? __ldcg(s1 + e0 + e2) : make_uint2(0u, 0u);
+        }
 #pragma unroll
-      for (int it = 0; it < 6; ++it) {
-        const int mid = (lo_r + hi_r) >> 1;
-        const int a0 = __shfl_sync(0xffffffffu, i0, mid & 31), a1 = __shfl_sync(0xffffffffu, i1, mid & 31);
-        if (lo_r < hi_r) {
-          if ((mid < 32 ? a0 : a1) > pp) hi_r = mid;
-          else lo_r = mid + 1;
+        for (int e2 = 0; e2 < 16; ++e2) {
+          if (e0 + e2 < n0 && d0 + e0 + e2 < kBandCap) sband[g2 * kBandCap + d0 + e0 + e2] = ev0[e2];
+          if (e0 + e2 < n1 && d1 + e0 + e2 < kBandCap) sband[g2 * kBandCap + d1 + e0 + e2] = ev1[e2];
         }
       }
-      const int a0 = __shfl_sync(0xffffffffu, i0, lo_r & 31), a1 = __shfl_sync(0xffffffffu, i1, lo_r & 31);
-      const int b0 = __shfl_sync(0xffffffffu, n0, lo_r & 31), b1 = __shfl_sync(0xffffffffu, n1, lo_r & 31);
-      const int excl = (lo_r < 32 ? a0 - b0 : a1 - b1);
-      ev[j] = make_uint2(0u, 0u);
-      if (pp < nband) ev[j] = __ldcg(cls_band + (((size_t)bh * NS + lo_r) * G + g2) * kSlot + (pp - excl));
     }
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-      if (lane + 32 * j < nband) sband[g2 * kBandCap + lane + 32 * j] = ev[j];
-    if (lane == 0) {
-      S2.rwhi[0][g2] = W_hi;
-      S2.rwbd[0][g2] = W_bd;
-      S2.nsub[0][g2] = (over || nband > kBandCap) ? kBandCap + 1 : nband;
-    }
-  }
-  __syncthreads();
-  fstamp(6);
-  // warp g resolves head g's marginal inside the band (weighted radix select)
-  if (warp < G) {
-    const int g2 = warp;
-    const int W_hi = S2.rwhi[0][g2], W_bd = S2.rwbd[0][g2], nband = S2.nsub[0][g2];
-    const int over = nband > kBandCap;
+    __syncwarp();
     int m = -1, keep = 0, all = 0, fb = 0;
     uint32_t T = 0;
     if (total <= budget) {
       all = 1;
-    } else if (W_hi >= budget || W_hi + W_bd < budget || over) {
+    } else if (W_hi >= budget || W_hi + W_bd < budget || over || nband > kBandCap) {
       fb = 1;  // the bounds did not bracket the marginal block: exact slow path below
     } else {
-      f_band_select(sband + (size_t)g2 * kBandCap, nband, sbs, budget - W_hi, sbits + g2 * nwords, m, keep, T);
+      f_band_select(sband + (size_t)g2 * kBandCap, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords, m,
+                    keep, T);
     }
     if (lane == 0) S2.sel[g2] = make_int4(m, keep, (int)T, all | (fb << 1));
   }
@@ -874,6 +942,9 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   fstamp(7);
   // slow path for a head whose bounds failed (rare): CTA-wide exact
   // selection over every key, then its selection words from the keys
+  bool special = false;
+#pragma unroll
+  for (int g2 = 0; g2 < G; ++g2) special |= S2.sel[g2].w != 0;
 #pragma unroll 1
   for (int g2 = 0; g2 < G; ++g2) {
     if (!(S2.sel[g2].w & 2)) continue;
@@ -900,14 +971,16 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     __syncthreads();
   }
   // all-fit heads: every block
+  if (special) {
 #pragma unroll 1
-  for (int g2 = 0; g2 < G; ++g2)
-    if (S2.sel[g2].w & 1)
-      for (int wi = tid; wi < nwu; wi += kFNT) {
-        const int rem = nb - wi * 32;
-        sbits[g2 * nwords + wi] = rem >= 32 ? 0xffffffffu : (1u << rem) - 1u;
-      }
-  __syncthreads();
+    for (int g2 = 0; g2 < G; ++g2)
+      if (S2.sel[g2].w & 1)
+        for (int wi = tid; wi < nwu; wi += kFNT) {
+          const int rem = nb - wi * 32;
+          sbits[g2 * nwords + wi] = rem >= 32 ? 0xffffffffu : (1u << rem) - 1u;
+        }
+    __syncthreads();
+  }
   fstamp(8);
 
   // ---- 3. union worklist.  Thread t owns word t (blocks 32t .. 32t + 31) and
@@ -1070,7 +1143,7 @@ static size_t fs_al(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t fused_scratch_bytes(int B, int Hq, int maxb) {
   const size_t nwords = ((size_t)maxb + 31) / 32;
   return 2 * fs_al((size_t)kFMaxGroups * kMaxG * 16) + fs_al((size_t)kFMaxGroups * kMaxG * kSlot * 8) +
-         fs_al((size_t)B * Hq * nwords * 4);
+         fs_al((size_t)B * Hq * nwords * 4) + fs_al((size_t)kFMaxGroups * kMaxG * kSub * 4);
 }
 
 template <int G>
@@ -1078,15 +1151,16 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
                              const int32_t* bs, const int32_t* nb, const int32_t* pf, const bf16* Kp,
                              const bf16* Vp, int Hq, int Hkv, int maxb, int max_pages, int S, int Pshift,
                              int budget, int cap, int ent_cap, int nwords, int sstride, size_t region_a,
-                             int per_cap, float sl2, float* scores, float4* mom, int4* cls_w, uint2* cls_band,
-                             uint32_t* gbits, int* counters, unsigned* gbar,
+                             int per_cap, float sl2, float* scores, float4* mom, int4* cls_w, int* cls_sub,
+                             uint2* cls_band, uint32_t* gbits, int* counters, unsigned* gbar,
                              float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
                              int32_t* wl_count, WLEntry* wl, float* o, float* lse, int* err) {
   allow_max_dyn_smem(k_decode_fused<G>);
   if (occupancy_of(k_decode_fused<G>, kFNT, smem) < 1) return cudaErrorNotSupported;
   launch_ex(k_decode_fused<G>, grid, dim3(kFNT), smem, st, 1, tm, q, bs, nb, pf, Kp, Vp, Hq, Hkv, maxb,
             max_pages, S, Pshift, budget, cap, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores, mom,
-            cls_w, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep, wl_count, wl, o, lse, err);
+            cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep, wl_count, wl, o,
+            lse, err);
   g_fused_launches.fetch_add(1);
   return post_launch("k_decode_fused", st);
 }
@@ -1145,6 +1219,7 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   uint2* cls_band = reinterpret_cast<uint2*>(fs + 2 * fs_al((size_t)kFMaxGroups * kMaxG * 16));
   uint32_t* gbits = reinterpret_cast<uint32_t*>(fs + 2 * fs_al((size_t)kFMaxGroups * kMaxG * 16) +
                                                 fs_al((size_t)kFMaxGroups * kMaxG * kSlot * 8));
+  int* cls_sub = reinterpret_cast<int*>(reinterpret_cast<char*>(gbits) + fs_al((size_t)B * Hq * nwords * 4));
   unsigned* gbar = reinterpret_cast<unsigned*>(bar);
   const float sl2 = scale * 1.4426950408889634f;
   const dim3 grid(NS, Hkv, B);
@@ -1152,7 +1227,8 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   return run_fused<GG>(tm, grid, smem, st, static_cast<const bf16*>(q), bs, nb, pf,                       \
                        static_cast<const bf16*>(Kp), static_cast<const bf16*>(Vp), Hq, Hkv, maxb, max_pages, \
                        S, Pshift, budget, cap, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores,    \
-                       mom, cls_w, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep,    \
+                       mom, cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, \
+                       keep,                                                                                \
                        wl_count, wl, o, lse, err)
   switch (G) {
     case 1: DSK_FU(1);

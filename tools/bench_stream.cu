@@ -138,7 +138,7 @@ int main() {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  auto run = [&](int mode, int ctas_per_sm, int nw, int depth, const int64_t* o, const char* tag) {
+  auto run = [&](int mode, int ctas_per_sm, int nw, int depth, const int64_t* o, const char* tag, int grid = 0) {
     size_t smem = (size_t)nw * depth * CHUNK + nw * depth * 8;
     void (*k)(const unsigned char*, const int64_t*, int, int, unsigned*) =
         mode == 0 ? k_stream<0> : mode == 1 ? k_stream<1> : k_stream<2>;
@@ -148,7 +148,7 @@ int main() {
     for (int rep = 0; rep < 5; ++rep) {
       CK(cudaMemsetAsync(flush, rep, 256 << 20));
       CK(cudaEventRecord(a));
-      k<<<sms * ctas_per_sm, nw * 32, smem>>>(buf, o, n_chunks, depth, sink);
+      k<<<grid ? grid : sms * ctas_per_sm, nw * 32, smem>>>(buf, o, n_chunks, depth, sink);
       CK(cudaEventRecord(b));
       CK(cudaEventSynchronize(b));
       CK(cudaGetLastError());
@@ -156,8 +156,9 @@ int main() {
       CK(cudaEventElapsedTime(&ms, a, b));
       best = std::min(best, ms);
     }
-    printf("%-4s mode %d  ctas/sm %d  warps %2d  depth %d  smem %6zu : %7.2f us  %7.0f GB/s\n", tag, mode,
-           ctas_per_sm, nw, depth, smem, best * 1e3, (double)n_chunks * CHUNK / (best * 1e-3) / 1e9);
+    printf("%-4s mode %d  ctas/sm %d  grid %4d  warps %2d  depth %d  smem %6zu : %7.2f us  %7.0f GB/s\n", tag, mode,
+           ctas_per_sm, grid ? grid : sms * ctas_per_sm, nw, depth, smem, best * 1e3,
+           (double)n_chunks * CHUNK / (best * 1e-3) / 1e9);
   };
   // empty-kernel reference
   {
@@ -173,6 +174,12 @@ int main() {
     }
     printf("empty kernel: %.2f us\n", best * 1e3);
   }
+  // fewer SMs streaming (one 8- or 16-warp CTA per SM on a subset of the SMs)
+  n_chunks = 12288;
+  printf("--- 12288 chunks (48 MiB), SM subsets\n");
+  for (int grid : {64, 72, 96, 128, 144})
+    for (int depth : {2, 3}) run(0, 1, 8, depth, offs, "rand", grid);
+  for (int grid : {72, 144}) run(0, 1, 16, 3, offs, "rand", grid);
   for (int n : {12288, 49152, 196608}) {
     n_chunks = n;
     printf("--- %d chunks (%d MiB)\n", n, n * 4 / 1024);

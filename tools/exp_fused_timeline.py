@@ -37,7 +37,7 @@ outs = [(torch.empty(B, Hq, d, device=dev), torch.empty(B, Hq, device=dev)) for 
 ws = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer")
 lib = D.lib()
 NAMES = ["start", "plan", "pdl_wait", "scored+arrive A", "A passed", "range classified", "B passed+gathered",
-         "band selected", "bits final", "union counted", "dealt", "pages done", "merged"]
+         "band selected", "bits final", "union counted", "dealt", "pages done", "merged", "B passed", "q loaded", "digests in smem"]
 
 
 def step():
@@ -72,7 +72,7 @@ t = tc[used, :16]
 clk = tc[used, 16:]
 t0 = t[:, 0].min()
 print(f"CTAs stamped: {used.sum()}  budget {budget}  B {B}")
-ORDER = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12]
+ORDER = [0, 1, 2, 14, 15, 3, 4, 5, 13, 7, 8, 9, 10, 11, 12]
 prev = None
 for k in ORDER:
     name = NAMES[k]
