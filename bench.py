@@ -1,22 +1,34 @@
 """Benchmark of the DynSplit-KV decode hot path on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode batch|seqsplit]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
 
-Workload (config.workload): BASELINE.json config 3's per-GPU shard -- a
-Llama-3-8B-shaped decode step (32 layers, 32 Q / 8 KV heads, d = 128, bf16 KV)
-at 128K context, token budget 4096, `--batch-per-gpu` sequences per GPU
-(default 1, so N = 8 is config 3's batch 8 sharded by batch).  A step = one
-decode token through all 32 layers: per layer dynsplit_decode_layer = a5 block
-scoring + a6 budgeted selection + a7/a8 split-K sparse attention with LSE
-merge, all in libdynsplit.so kernels, replayed as one CUDA graph.  Sequences are independent
-(no data-path collective); scaling is weak (fixed work per GPU).
+--mode batch (default; the headline).  Workload (config.workload): BASELINE.json
+config 3's per-GPU shard -- a Llama-3-8B-shaped decode step (32 layers, 32 Q /
+8 KV heads, d = 128, bf16 KV) at 128K context, token budget 4096,
+`--batch-per-gpu` sequences per GPU (default 1, so N = 8 is config 3's batch 8
+sharded by batch).  A step = one decode token through all 32 layers: per
+layer one dynsplit_decode_layer call = one k_decode_fused launch (a5 block
+scoring + a6 budgeted selection + a7/a8 split-K sparse attention with the LSE
+merge), replayed as one CUDA graph.  Sequences are independent (no data-path
+collective); scaling is weak (fixed work per GPU).  At N = 1 the line also
+carries two more configurations of the metric, each with its roofline, e2e
+and dense baseline: "c3_b8" (config 3 unsharded: all 8 sequences on one GPU)
+and "c4" (config 4 on one GPU: Llama2-13B shape, 40 MHA heads, 40 layers).
+
+--mode seqsplit.  Config 4 (Llama2-13B: 40 layers, 40 MHA heads, 128K,
+budget 4096) sequence-split across the N ranks (parallel.SeqSplitDecoder:
+local a5 -> NCCL all-gather of the block scores -> global a6 -> local a7 ->
+all-gather of (o, lse) -> rank-ordered a8 merge); strong scaling.
 
 value = aggregate algorithmic HBM bytes per step (digests + GQA-union of the
 selected K/V rows + block starts + q + o/lse) over all
-ranks / max-over-ranks step time, in GB/s.  ms_per_step is the decode step
+ranks / max-over-ranks step time, in GB/s; ms_per_step is the decode-step
 latency.  The per-layer working set (~65 MiB x 32 layers ~ 2 GiB per step) is
-far larger than the 126 MB L2, so no flush is needed between steps.
+far larger than the 126 MB L2, so no flush is needed between steps; blocks
+that cycle fewer distinct layer caches than layers still stream every layer's
+bytes from HBM (each cache is >> L2) and say so in their config.
 """
 from __future__ import annotations
 
@@ -36,14 +48,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sparse decode-attn µs/step & HBM GB/s vs peak at 128K ctx, 1/2/4/8 B200"
 WORKLOAD = "C3 per-GPU shard: Llama-3-8B decode (32 layers, 32Q/8KV, d=128, bf16) at 128K ctx, budget 4K"
+WORKLOAD_C4 = "C4: Llama2-13B decode (40 layers, 40 MHA heads, d=128, bf16) at 128K ctx, budget 4K, sequence split"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="batch", choices=["batch", "seqsplit"])
     ap.add_argument("--seq", type=int, default=131072)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--batch-per-gpu", type=int, default=1)
@@ -55,8 +69,9 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c3_b8 / c4 blocks")
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
 
@@ -77,6 +92,23 @@ def measured_peak_hbm():
         return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 class ClockSampler:
@@ -160,17 +192,39 @@ def oracle_layer_bytes(q, K, starts, budget, Hkv, g, e=2):
     return nb * Hkv * 2 * d * e + union * 2 * d * e + 2 * (nb + 1) * 4 + q.size * e + q.shape[0] * (d + 1) * 4
 
 
-def time_oracle(q, K, V, starts, budget, heads):
-    """Oracle decode step over the sampled heads; returns seconds."""
+_POOL_ARGS = None  # (q, K, V, starts, budget) shared with forked workers
+
+
+def _oracle_heads(hs):
     from oracle import dynsplit_oracle as O
-    t0 = time.perf_counter()
-    O.decode_step(q[:heads], K, V, starts, budget)
-    return time.perf_counter() - t0
+    q, K, V, starts, budget = _POOL_ARGS
+    g = q.shape[0] // K.shape[1]
+    # the oracle's decode step over a contiguous group of query heads (whole KV groups)
+    return O.decode_step(q[hs[0]:hs[1]], K[:, hs[0] // g: (hs[1] - 1) // g + 1], V[:, hs[0] // g: (hs[1] - 1) // g + 1],
+                         starts, budget)["lse"].shape
 
 
-def host_layer(seed, S, Hq, Hkv, d, rho):
-    from synth import generators as G
-    return G.decode_qkv(seed, S, Hq, Hkv, d, rho=rho)
+def time_oracle(q, K, V, starts, budget, heads, workers=1):
+    """Oracle decode step over the first `heads` query heads; returns seconds.
+    workers > 1: whole KV groups of heads spread over forked processes."""
+    global _POOL_ARGS
+    from oracle import dynsplit_oracle as O
+    if workers <= 1:
+        t0 = time.perf_counter()
+        O.decode_step(q[:heads], K, V, starts, budget)
+        return time.perf_counter() - t0
+    import multiprocessing as mp
+    g = q.shape[0] // K.shape[1]
+    groups = heads // g
+    n = max(1, min(workers, groups))
+    cuts = [round(i * groups / n) * g for i in range(n + 1)]
+    _POOL_ARGS = (q, K, V, starts, budget)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(n) as pool:
+        t0 = time.perf_counter()
+        pool.map(_oracle_heads, [(cuts[i], cuts[i + 1]) for i in range(n) if cuts[i + 1] > cuts[i]])
+        dt = time.perf_counter() - t0
+    return dt
 
 
 def cpu_threads_limit():
@@ -182,7 +236,19 @@ def cpu_threads_limit():
         return contextlib.nullcontext()
 
 
+def host_layer(seed, S, Hq, Hkv, d, rho):
+    from synth import generators as G
+    return G.decode_qkv(seed, S, Hq, Hkv, d, rho=rho)
+
+
 def run_reference(args, world, rank):
+    """The reference arm: the fp64 oracle (no reference implementation exists,
+    the reference is a paper) on the host cores, one thread, on a bounded
+    sample of the workload: each timed step is the oracle's decode step of
+    `--cpu-sample-heads` query heads of ONE layer of one sequence.  The line's
+    ms_per_step is that sample step as timed (steps x ms_per_step is the wall
+    time of the timed region); the full-step time it extrapolates to (x layers
+    x heads) is reported beside it, marked as such."""
     if rank != 0:
         return
     from oracle import dynsplit_oracle as O
@@ -202,19 +268,20 @@ def run_reference(args, world, rank):
             if i >= args.warmup:
                 times.append(dt)
     sec = float(np.mean(times))
-    # one oracle step = `heads` of the 32 heads of one layer of one sequence;
-    # scaled to the metric: bytes that fraction of a layer touches per second
     gbs = layer_bytes * frac / sec / 1e9
-    step_ms = sec / frac * args.layers * args.batch_per_gpu * 1e3
-    sample = f"oracle decode step, {heads}/{Hq} heads of 1 layer of 1 seq at S={S}, budget {args.budget}"
+    sample = (f"oracle decode step, {heads}/{Hq} heads of 1 of {args.layers} layers of 1 sequence at S={S}, "
+              f"budget {args.budget}, 1 thread")
     line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "seq_len": S, "layers": args.layers,
                        "batch_per_gpu": args.batch_per_gpu, "budget": args.budget},
-            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "sample_step": {"layers": 1, "heads": heads, "sequences": 1,
+                            "extrapolated_full_step_ms": sec / frac * args.layers * args.batch_per_gpu * 1e3,
+                            "note": "ms_per_step is the timed sample step; the full step is extrapolated"},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model()},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -279,8 +346,286 @@ def prefill_c5(args, D, G, cfg, ids, dev, cur):
 
 
 # ---------------------------------------------------------------------------
-# GPU arm
+# GPU arm: one decode workload (B sequences, L layers over Ld distinct caches)
 # ---------------------------------------------------------------------------
+class Workload:
+    """Synthetic decode workload: B sequences of S tokens, the static-T7
+    DD-Select plan, Ld distinct layer caches (pages sized tightly to the
+    plan's page count), one query per layer cache."""
+
+    def __init__(self, D, G, B, S, Hq, Hkv, Ld, rho, seed, dev, tok_seed0):
+        import torch
+        self.D, self.B, self.S, self.Hq, self.Hkv, self.Ld = D, B, S, Hq, Hkv, Ld
+        d = 128
+        self.d = d
+        ids = torch.from_numpy(G.T7_IDS).to(dev)
+        self.toks = torch.from_numpy(np.stack([G.tokens(tok_seed0 + b, S) for b in range(B)])).to(dev)
+        cfg0 = D.default_config()
+        plan = D.build_blocks(self.toks, ids, None, None, cfg0, static_w10=G.T7_W10, Hq=Hq, Hkv=Hkv)
+        cap = int(plan.n_pages.max().item()) + 8                     # setup-time read of the plan
+        self.cfg = D.default_config(page_cap=cap)
+        self.nblk = [int(x) for x in plan.n_blocks.cpu()]
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        self.layers, self.qs = [], []
+        self.host_keep = None
+        for l in range(Ld):
+            q, K, V = G.torch_decode_layer(gen, S, Hq, Hkv, d, B, dev, rho=rho)
+            self.layers.append(D.build_blocks(self.toks, ids, K, V, self.cfg, static_w10=G.T7_W10, Hq=Hq))
+            self.qs.append(q.contiguous())
+            if l == 0:
+                self.K0 = K[0].float().cpu().numpy()
+                self.V0 = V[0].float().cpu().numpy()
+                self.q0 = q[0].float().cpu().numpy()
+            del K, V
+        torch.cuda.synchronize()
+        self.shape = D.make_shape(B, S, Hq, Hkv, d)
+
+
+def time_graph(torch, fn, steps, warmup, cur, dev, world, barrier):
+    """Capture fn() (one step) in a CUDA graph, replay `warmup` times, then time
+    `steps` replays with events around each; returns (mean ms, per-step ms)."""
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream(dev).wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(warmup):
+        g.replay()
+    barrier()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    for i in range(steps):
+        evs[i].record(cur)
+        g.replay()
+    evs[-1].record(cur)
+    barrier()
+    per = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(steps)])
+    return float(evs[0].elapsed_time(evs[-1]) / steps), per, g
+
+
+def decode_block(args, torch, D, wl: Workload, L, budget, dev, cur, world, barrier, peak, with_e2e=True,
+                 with_dense=True, with_three_kernel=False):
+    """Time one decode workload: the step graph (L dynsplit_decode_layer calls
+    = L k_decode_fused launches), its algorithmic bytes, the fused kernel's
+    roofline, e2e through dynsplit_decode_step_host, the dense baseline."""
+    B, Hq, Hkv, d = wl.B, wl.Hq, wl.Hkv, wl.d
+    g = Hq // Hkv
+    shape, cfg = wl.shape, wl.cfg
+    Ld = wl.Ld
+    outs = [(torch.empty(B, Hq, d, device=dev), torch.empty(B, Hq, device=dev)) for _ in range(L)]
+    sel = [D._sel_outputs(shape, cfg, budget, dev, want_blocks=False) for _ in range(Ld)]
+    ws = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer_step")
+
+    def step():
+        for l in range(L):
+            j = l % Ld
+            _, ns, mg, kp, w = sel[j]
+            D.decode_layer(wl.qs[j], wl.layers[j], budget, out=(ns, mg, kp, w, outs[l][0], outs[l][1]), ws=ws)
+
+    lib = D.lib()
+    lib.dynsplit_debug_fused_launches.restype = __import__("ctypes").c_longlong
+    n0 = lib.dynsplit_debug_fused_launches()
+    step()
+    torch.cuda.synchronize()
+    fused_per_step = lib.dynsplit_debug_fused_launches() - n0
+    # algorithmic bytes (digests + union rows + block starts + q + o/lse) from the worklists
+    union_rows = []
+    for j in range(Ld):
+        _, streamed = D.worklist_rows(sel[j][4], shape, g)
+        union_rows.append(int(streamed.sum()))
+    e = 2
+    per_layer = [sum(wl.nblk) * Hkv * 2 * d * e + union_rows[l % Ld] * 2 * d * e
+                 + 2 * sum(n + 1 for n in wl.nblk) * 4 + B * Hq * d * e + B * Hq * (d + 1) * 4 for l in range(L)]
+    step_bytes = float(sum(per_layer))
+    ms, per, gstep = time_graph(torch, step, args.steps, args.warmup, cur, dev, world, barrier)
+    res = {"ms_per_step": ms, "us_per_layer": ms * 1e3 / L, "bytes_per_step": step_bytes,
+           "GB_s": step_bytes / (ms * 1e-3) / 1e9,
+           "step_ms_p10_p50_p90": [float(np.percentile(per, p)) for p in (10, 50, 90)],
+           "union_factor": sum(union_rows[l % Ld] for l in range(L)) / (L * B * Hkv * budget),
+           "fused_launches_per_step": fused_per_step}
+    # the dominant (only) kernel: k_decode_fused, one launch per layer
+    res["roofline"] = {"bound": "hbm", "kernel": "k_decode_fused (a5+a6+a7+a8)",
+                       "achieved": step_bytes / L / (ms * 1e-3 / L) / 1e9, "peak": peak[0], "unit": "GB/s",
+                       "frac": step_bytes / (ms * 1e-3) / 1e9 / peak[0],
+                       "traffic": ncu_traffic("k_decode_fused"), "peak_source": peak[1],
+                       "algorithmic_bytes_per_launch": step_bytes / L, "avg_launch_us": ms * 1e3 / L,
+                       "timing": "CUDA events around the step graph of L back-to-back (PDL-chained) launches, "
+                                 "per launch"}
+    if with_three_kernel:
+        # context: the same step through the three-kernel path (a5 -> a6 -> a7), and
+        # k_decode_attn alone (its old roofline)
+        lib.dynsplit_debug_fused(0)
+        try:
+            ms3, _, _ = time_graph(torch, step, args.steps, args.warmup, cur, dev, world, barrier)
+            wsd = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "decode")
+
+            def attn_only():
+                for l in range(L):
+                    j = l % Ld
+                    D.decode_attn(wl.qs[j], wl.layers[j], sel[j][4], out=outs[l], ws=wsd)
+            msa, _, _ = time_graph(torch, attn_only, args.steps, args.warmup, cur, dev, world, barrier)
+        finally:
+            lib.dynsplit_debug_fused(1)
+        attn_bytes = sum(union_rows[l % Ld] * 2 * d * e + B * Hq * d * e + B * Hq * (d + 1) * 4
+                         for l in range(L)) / L
+        res["three_kernel_path"] = {"ms_per_step": ms3, "k_decode_attn_us": msa * 1e3 / L,
+                                    "k_decode_attn_frac": attn_bytes / (msa * 1e-3 / L) / 1e9 / peak[0],
+                                    "note": "k_score_blocks_tc -> k_select_reg -> k_decode_attn per layer "
+                                            "(DYNSPLIT_NO_FUSED), context"}
+    if with_e2e:
+        # e2e through the exported host-buffer call dynsplit_decode_step_host:
+        # per layer the H2D copy of q from pinned memory, the decode, the D2H
+        # copies of o and lse; the host reads the step's result (synchronise)
+        q_h = [wl.qs[l % Ld].cpu().pin_memory() for l in range(L)]
+        o_h = [torch.empty(B, Hq, d).pin_memory() for _ in range(L)]
+        l_h = [torch.empty(B, Hq).pin_memory() for _ in range(L)]
+        wsh = D.workspace(D.step_host_workspace_bytes(shape, cfg, budget), dev, "step_host")
+        wlh = D._sel_outputs(shape, cfg, budget, dev, want_blocks=False)[4]
+
+        def host_step():
+            for l in range(L):
+                D.decode_step_host(q_h[l], wl.layers[l % Ld], budget, o_h[l], l_h[l], wlh, wsh)
+
+        for _ in range(args.warmup):
+            host_step()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(cur)
+        for _ in range(args.steps):
+            host_step()
+            cur.synchronize()                      # the step's result is read on the host
+        ev1.record(cur)
+        barrier()
+        e2e_ms = ev0.elapsed_time(ev1) / args.steps
+        h2d = sum(x.numel() * x.element_size() for x in q_h)
+        d2h = sum(x.numel() * 4 for x in o_h) + sum(x.numel() * 4 for x in l_h)
+        res["e2e"] = {"value": step_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                      "api": "dynsplit_decode_step_host (host q/o/lse, pinned), one call per layer"}
+    if with_dense:
+        wsd = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "decode")
+
+        def dense_step():
+            for l in range(L):
+                j = l % Ld
+                D.decode_attn(wl.qs[j], wl.layers[j], None, out=outs[l], ws=wsd)
+        dms, _, _ = time_graph(torch, dense_step, max(2, min(args.steps, 5)), 1, cur, dev, world, barrier)
+        dense_bytes = L * B * Hkv * wl.S * 2 * d * e
+        res["dense"] = {"ms_per_step": dms, "GB_s": dense_bytes / (dms * 1e-3) / 1e9,
+                        "frac_of_peak": dense_bytes / (dms * 1e-3) / 1e9 / peak[0], "sparse_speedup": dms / ms}
+    del gstep
+    return res
+
+
+def cpu_baseline_leg(args, wl: Workload, budget):
+    """The oracle on this host's cores: 1 thread, and all cores (forked
+    workers over whole KV groups of heads), on a bounded sample (heads of
+    layer 0 of sequence 0)."""
+    from oracle import dynsplit_oracle as O
+    from synth import generators as G
+    starts = O.segment(G.tokens(args.seed * 7919 + 0, wl.S), G.T7_IDS, G.T7_W10, 32, 14)
+    g = wl.Hq // wl.Hkv
+    heads = min(args.cpu_sample_heads, wl.Hq)
+    lb = oracle_layer_bytes(wl.q0, wl.K0, starts, budget, wl.Hkv, g)
+    out = {}
+    cores = cpu_cores()
+    groups = heads // g
+    with cpu_threads_limit():
+        for tag, workers in (("1_thread", 1), ("all_cores", min(cores, groups))):
+            ts = []
+            t_start = time.perf_counter()
+            while not ts or (time.perf_counter() - t_start < args.cpu_seconds / 2 and len(ts) < 20):
+                ts.append(time_oracle(wl.q0, wl.K0, wl.V0, starts, budget, heads, workers))
+            sec = float(np.mean(ts))
+            out[tag] = {"value": lb * heads / wl.Hq / sec / 1e9, "seconds_per_sample": sec, "samples": len(ts),
+                        "workers": workers}
+    one, allc = out["1_thread"], out["all_cores"]
+    return {"value": allc["value"], "unit": "GB/s", "cores": allc["workers"], "kind": "oracle",
+            "sample": f"oracle decode step of {heads}/{wl.Hq} heads of layer 0 of sequence 0 at S={wl.S}, "
+                      f"budget {budget}; value = {allc['workers']} forked single-thread workers (one per KV "
+                      f"group, the parallelism the sample has; the host has {cores} cores), "
+                      f"{allc['seconds_per_sample']:.2f} s per sample; 1 thread: {one['value']:.4f} GB/s "
+                      f"({one['seconds_per_sample']:.2f} s per sample)",
+            "one_thread_value": one["value"], "host_cores": cores, "cpu": cpu_model()}
+
+
+def run_seqsplit(args, world, rank, local):
+    """Config 4 sequence-split across the ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_03184_b200 import dynsplit as D
+    from paper_2602_03184_b200 import parallel as PAR
+    from synth import generators as G
+    dev = torch.device("cuda", local)
+    S, Hq, Hkv, d, L, budget = args.seq, 40, 40, 128, 40, args.budget
+    Ld = min(L, 10)
+    cfg = D.default_config()
+    toks = torch.from_numpy(G.tokens(args.seed * 7919, S)[None]).to(dev)
+    ids = torch.from_numpy(G.T7_IDS).to(dev)
+    glob, ranges = PAR.global_plan(toks, ids, cfg, G.T7_W10, Hq, Hkv, world)
+    t_lo, t_hi = PAR.shard_token_range(glob.block_starts[0].tolist(), ranges, rank)
+    gen = torch.Generator(device=dev)
+    layers, qs = [], []
+    for l in range(Ld):
+        gen.manual_seed(1000003 * (args.seed + 1) + 7 * l + 1)          # q: identical on every rank
+        q = torch.randn(1, Hq, d, generator=gen, device=dev).to(torch.bfloat16)
+        gen.manual_seed(1000003 * (args.seed + 1) + 7 * l + 2 + 1000 * rank)  # K/V: this rank's tokens
+        n_loc = max(t_hi - t_lo, 1)
+        K = (1.5 * torch.randn(1, n_loc, Hkv, d, generator=gen, device=dev)).to(torch.bfloat16)
+        V = torch.randn(1, n_loc, Hkv, d, generator=gen, device=dev).to(torch.bfloat16)
+        layers.append(PAR.local_layer(glob, ranges, rank, K, V, cfg, Hq))
+        qs.append(q)
+        del K, V
+    dec = PAR.SeqSplitDecoder(glob, ranges, rank, Hq, budget, dev)
+    o = torch.empty(Hq, d, device=dev)
+    lse = torch.empty(Hq, device=dev)
+
+    def step():
+        for l in range(L):
+            dec.step(qs[l % Ld], layers[l % Ld], o=o, lse=lse)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    step()
+    torch.cuda.synchronize()
+    # algorithmic bytes of this rank: local digests + local union rows + q + o/lse (+ the exchange)
+    nloc = int(layers[0].n_blocks[0])
+    _, streamed = D.worklist_rows(dec.sel_out[4], dec.gshape, 1)
+    rank_bytes = L * (nloc * Hkv * 2 * d * 2 + int(streamed.sum()) * 2 * d * 2 + Hq * d * 2 + Hq * (d + 1) * 4)
+    cur = torch.cuda.current_stream(dev)
+    clk = ClockSampler(local)
+    clk.__enter__()
+    ms, per, _ = time_graph(torch, step, args.steps, args.warmup, cur, dev, world, barrier)
+    clk.__exit__(None, None, None)
+    vals = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(rank_bytes)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms = vals.item()
+    if rank == 0:
+        peak = measured_peak_hbm()
+        line = {"metric": METRIC, "value": tot.item() / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": WORKLOAD_C4, "seq_len": S, "layers": L, "distinct_layer_caches": Ld,
+                           "heads_q": Hq, "heads_kv": Hkv, "head_dim": d, "budget": budget,
+                           "parallelism": f"sequence-split x{world}", "ranges": ranges,
+                           "l2": "no flush: every layer cache >> 126 MB L2"},
+                "us_per_layer": ms * 1e3 / L,
+                "step_frac_of_peak_aggregate": tot.item() / (ms * 1e-3) / 1e9 / (peak[0] * world),
+                "gpu_launches": None, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -299,241 +644,67 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     D.lib()
+    if args.mode == "seqsplit":
+        return run_seqsplit(args, world, rank, local)
 
     B, S, Hq, Hkv, d, L = args.batch_per_gpu, args.seq, args.hq, args.hkv, 128, args.layers
-    g = Hq // Hkv
     budget = args.budget
-    cfg = D.default_config()
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000003 * (args.seed + 1) + rank)
-
-    # ---- prefill (untimed setup): tokens -> static-T7 DD-Select plan, pages, digests
-    toks = torch.from_numpy(np.stack([G.tokens(args.seed * 7919 + rank * B + b, S) for b in range(B)])).to(dev)
-    ids = torch.from_numpy(G.T7_IDS).to(dev)
-    layers, qs = [], []
-    host_keep = None
-    for l in range(L):
-        q, K, V = G.torch_decode_layer(gen, S, Hq, Hkv, d, B, dev, rho=args.rho)
-        layers.append(D.build_blocks(toks, ids, K, V, cfg, static_w10=G.T7_W10, Hq=Hq))
-        qs.append(q.contiguous())
-        if l == 0 and rank == 0 and not args.no_cpu_baseline:
-            host_keep = (q[0].float().cpu().numpy(), K[0].float().cpu().numpy(), V[0].float().cpu().numpy())
-        del K, V
-    torch.cuda.synchronize()
-
-    # ---- per-layer preallocated outputs; shared workspaces / worklist
-    shape = D.make_shape(B, S, Hq, Hkv, d)
-    sel_out = [D._sel_outputs(shape, cfg, budget, dev, want_blocks=False) for _ in range(L)]
-    attn_out = [(torch.empty(B, Hq, d, device=dev), torch.empty(B, Hq, device=dev)) for _ in range(L)]
-    ws_sel = D.workspace(D.workspace_bytes(D.OP_SELECT, shape, cfg, budget), dev, "select")
-    ws_dec = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "decode")
-
-    def sel_layer(l):
-        sb, ns, mg, kp, wl = sel_out[l]
-        return D.select(qs[l], layers[l], budget, out=(sb, ns, mg, kp, wl, None), ws=ws_sel)
-
-    def attn_layer(l):
-        return D.decode_attn(qs[l], layers[l], sel_out[l][4], out=attn_out[l], ws=ws_dec)
-
-    ws_step = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer_step")
-
-    def step():
-        # the public per-layer call (a5 -> a6 -> a7+a8, PDL-ordered)
-        for l in range(L):
-            _, ns, mg, kp, wl = sel_out[l]
-            D.decode_layer(qs[l], layers[l], budget, out=(ns, mg, kp, wl, attn_out[l][0], attn_out[l][1]),
-                           ws=ws_step)
-
-    def dense_step():
-        for l in range(L):
-            D.decode_attn(qs[l], layers[l], None, out=attn_out[l], ws=ws_dec)
-
-    # eager warm-up call (sets kernel attributes before capture), metrics
-    step()
-    torch.cuda.synchronize()
-    e = 2
-    nblk = [int(x) for x in layers[0].n_blocks.cpu()]
-    union_rows = 0
-    for l in range(L):
-        _, streamed = D.worklist_rows(sel_out[l][4], shape, g)
-        union_rows += int(streamed.sum())
-    n_entries_total = 0
-    digest_bytes = L * sum(nblk) * Hkv * 2 * d * e
-    kv_bytes = union_rows * 2 * d * e
-    small = L * (2 * sum(n + 1 for n in nblk) * 4 + B * Hq * d * e + B * Hq * (d + 1) * 4)
-    step_bytes = digest_bytes + kv_bytes + small
-    attn_bytes_per_launch = (kv_bytes + L * (B * Hq * d * e + B * Hq * (d + 1) * 4)) / L
-    score_bytes_per_launch = digest_bytes / L + B * Hq * d * e
-
-    # ---- CUDA graphs: whole step; per-layer select / attn (kernel timing)
-    s = torch.cuda.Stream(dev)
-    s.wait_stream(torch.cuda.current_stream(dev))
-    with torch.cuda.stream(s):
-        step()
-    torch.cuda.current_stream(dev).wait_stream(s)
-    g_step = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_step):
-        step()
-    # per-kernel-group timing: all L layers' a5+a6 (resp. a7+a8) launches in one
-    # graph, back to back as in the step (PDL-chained), averaged per launch
-    g_sel_all, g_attn_all = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_sel_all):
-        for l in range(L):
-            sel_layer(l)
-    # a5 alone (block scores into the select workspace), for the a5 / a6 split
-    mb_ = D.max_blocks(S, cfg)
-    score_buf = torch.empty(B, Hq, mb_, dtype=torch.float32, device=dev)
-    g_score_all = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_score_all):
-        for l in range(L):
-            D.score_blocks(qs[l], layers[l], out=score_buf)
-    with torch.cuda.graph(g_attn_all):
-        for l in range(L):
-            attn_layer(l)
+    cur = torch.cuda.current_stream(dev)
+    peak = measured_peak_hbm()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        g_step.replay()
-    barrier()
-
-    # ---- timed region 1: whole-step graph
-    cur = torch.cuda.current_stream(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step_evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    # clocks are sampled over timed regions 1 and 2 (the step graph, then the
-    # per-kernel-group graphs): region 1 alone is only ~50 ms at the defaults
+    # ---- the headline block: config 3's per-GPU shard, every layer its own cache
+    wl = Workload(D, G, B, S, Hq, Hkv, L, args.rho, 1000003 * (args.seed + 1) + rank, dev,
+                  args.seed * 7919 + rank * B)
     clk = ClockSampler(local)
     clk.__enter__()
-    barrier()
-    ev0.record(cur)
-    for i in range(args.steps):
-        step_evs[i].record(cur)
-        g_step.replay()
-    step_evs[-1].record(cur)
-    ev1.record(cur)
-    barrier()
-    step_ms = ev0.elapsed_time(ev1) / args.steps
-    per_step = np.array([step_evs[i].elapsed_time(step_evs[i + 1]) for i in range(args.steps)])
-
-    # ---- timed region 2: the step's kernel groups, each as an L-layer graph
-    barrier()
-    t0, t1, t2, t3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-    t0.record(cur)
-    for _ in range(args.steps):
-        g_sel_all.replay()
-    t1.record(cur)
-    for _ in range(args.steps):
-        g_attn_all.replay()
-    t2.record(cur)
-    for _ in range(args.steps):
-        g_score_all.replay()
-    t3.record(cur)
-    barrier()
+    main_res = decode_block(args, torch, D, wl, L, budget, dev, cur, world, barrier, peak,
+                            with_three_kernel=(world == 1))
     clk.__exit__(None, None, None)
-    sel_ms = t0.elapsed_time(t1) / (args.steps * L)
-    attn_ms = t1.elapsed_time(t2) / (args.steps * L)
-    score_ms = t2.elapsed_time(t3) / (args.steps * L)
-    split_step_ms = t0.elapsed_time(t2) / args.steps
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(args, wl, budget)
+    del wl
+    torch.cuda.empty_cache()
 
-    # ---- e2e: the step's inputs from pinned HOST memory (every layer's q, one
-    #      H2D copy), the public per-layer call dynsplit_decode_layer, and the
-    #      step's result (every layer's o and lse) read back to pinned host
-    #      memory (one D2H copy) and synchronised on, every step
-    q_all_h = torch.stack([q.cpu() for q in qs]).pin_memory()            # [L, B, Hq, d] bf16
-    # every layer's o and lse in one buffer, read back with one D2H copy
-    res_h = torch.empty(L * B * Hq * (d + 1)).pin_memory()
-    q_all_d = torch.empty(q_all_h.shape, dtype=q_all_h.dtype, device=dev)
-    res_d = torch.empty(L * B * Hq * (d + 1), device=dev)
-    o_all_d = res_d[: L * B * Hq * d].view(L, B, Hq, d)
-    l_all_d = res_d[L * B * Hq * d:].view(L, B, Hq)
-    ws_layer = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, cfg, budget), dev, "layer_e2e")
-    sel_e2e = D._sel_outputs(shape, cfg, budget, dev, want_blocks=False)
-
-    def host_step():
-        q_all_d.copy_(q_all_h, non_blocking=True)
-        for l in range(L):
-            _, ns, mg, kp, wl = sel_e2e
-            D.decode_layer(q_all_d[l], layers[l], budget, out=(ns, mg, kp, wl, o_all_d[l], l_all_d[l]),
-                           ws=ws_layer)
-        res_h.copy_(res_d, non_blocking=True)
-
-    host_step()
-    torch.cuda.synchronize()
-    g_host = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_host):
-        host_step()
-    for _ in range(args.warmup):
-        g_host.replay()
-    barrier()
-    ev0.record(cur)
-    for _ in range(args.steps):
-        g_host.replay()
-        cur.synchronize()                     # the step's result is read on the host
-    ev1.record(cur)
-    barrier()
-    e2e_ms = ev0.elapsed_time(ev1) / args.steps
-    h2d = q_all_h.numel() * q_all_h.element_size()
-    d2h = res_h.numel() * 4
-
-    # ---- prefill row a1 (context, not the headline): Alg. 1 delimiter scoring
-    #      of one sequence-layer at S_pf (C5 shape: 32Q/8KV, bf16), one launch pair
-    prefill = None
-    if rank == 0 and not args.no_prefill:
-        prefill = prefill_c5(args, D, G, cfg, ids, dev, cur)
-
-    # ---- dense baseline (row a9): every page, every head
-    dense_ms = None
-    if not args.no_dense:
-        g_dense = torch.cuda.CUDAGraph()
-        dense_step()
-        torch.cuda.synchronize()
-        with torch.cuda.graph(g_dense):
-            dense_step()
-        g_dense.replay()
-        barrier()
-        nd = max(2, min(args.steps, 5))
-        ev0.record(cur)
-        for _ in range(nd):
-            g_dense.replay()
-        ev1.record(cur)
-        barrier()
-        dense_ms = ev0.elapsed_time(ev1) / nd
-
-    # ---- max over ranks
-    vals = torch.tensor([step_ms, attn_ms, sel_ms, e2e_ms, split_step_ms, dense_ms or 0.0, score_ms],
-                        dtype=torch.float64, device=dev)
-    tot_bytes = torch.tensor([float(step_bytes)], dtype=torch.float64, device=dev)
+    # ---- max over ranks of the headline
+    vals = torch.tensor([main_res["ms_per_step"], main_res["e2e"]["ms_per_step"]], dtype=torch.float64, device=dev)
+    tot = torch.tensor([main_res["bytes_per_step"]], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot_bytes, op=dist.ReduceOp.SUM)
-    step_ms, attn_ms, sel_ms, e2e_ms, split_step_ms, dense_ms_v, score_ms = vals.tolist()
-    all_bytes = tot_bytes.item()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    step_ms, e2e_ms = vals.tolist()
+    all_bytes = tot.item()
 
-    cpu = None
-    if rank == 0 and host_keep is not None:
-        from oracle import dynsplit_oracle as O
-        qh, Kh, Vh = host_keep
-        starts = O.segment(G.tokens(args.seed * 7919 + 0, S), G.T7_IDS, G.T7_W10, 32, 14)
-        heads = min(args.cpu_sample_heads, Hq)
-        lb = oracle_layer_bytes(qh, Kh, starts, budget, Hkv, g)
-        ts = []
-        with cpu_threads_limit():
-            t_start = time.perf_counter()
-            while not ts or (time.perf_counter() - t_start < args.cpu_seconds and len(ts) < 50):
-                ts.append(time_oracle(qh, Kh, Vh, starts, budget, heads))
-        sec = float(np.mean(ts))
-        cpu = {"value": lb * heads / Hq / sec / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"{len(ts)} oracle decode steps of layer 0, sequence 0 ({heads}/{Hq} heads) "
-                         f"at S={S}, budget {budget}; mean {sec:.2f} s each, "
-                         f"{sum(ts):.1f} s total, 1 thread"}
+    # ---- more configurations of the metric on one GPU (N = 1 only)
+    extra = {}
+    if world == 1 and not args.no_extra:
+        wl8 = Workload(D, G, 8, S, Hq, Hkv, 8, args.rho, 77 + args.seed, dev, args.seed * 7919 + 100)
+        r8 = decode_block(args, torch, D, wl8, L, budget, dev, cur, world, barrier, peak)
+        r8["config"] = {"workload": "C3 unsharded: Llama-3-8B decode, 8 sequences on 1 GPU, 128K, budget 4K",
+                        "batch": 8, "layers": L, "distinct_layer_caches": 8,
+                        "note": "32 layers of work over 8 distinct layer caches (each 5.2 GB >> L2)"}
+        extra["c3_b8"] = r8
+        del wl8
+        torch.cuda.empty_cache()
+        wl4 = Workload(D, G, 1, S, 40, 40, 10, args.rho, 99 + args.seed, dev, args.seed * 7919 + 200)
+        r4 = decode_block(args, torch, D, wl4, 40, budget, dev, cur, world, barrier, peak)
+        r4["config"] = {"workload": "C4 on 1 GPU: Llama2-13B decode (40 layers, 40 MHA heads), 128K, budget 4K",
+                        "layers": 40, "distinct_layer_caches": 10,
+                        "note": "40 layers of work over 10 distinct layer caches (each 3.4 GB >> L2)"}
+        extra["c4"] = r4
+        del wl4
+        torch.cuda.empty_cache()
+
+    prefill = None
+    if rank == 0 and not args.no_prefill:
+        prefill = prefill_c5(args, D, G, D.default_config(), torch.from_numpy(G.T7_IDS).to(dev), dev, cur)
 
     if rank == 0:
-        peak, peak_src = measured_peak_hbm()
-        achieved = attn_bytes_per_launch / (attn_ms * 1e-3) / 1e9
         line = {
             "metric": METRIC,
             "value": all_bytes / (step_ms * 1e-3) / 1e9,
@@ -549,38 +720,28 @@ def main():
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
                        "seq_len": S, "layers": L, "heads_q": Hq, "heads_kv": Hkv, "head_dim": d,
-                       "budget": budget, "rho": args.rho, "C": cfg.C, "delta": cfg.delta,
-                       "page_size": cfg.page_size, "parallelism": f"batch-shard x{world}",
-                       "l2": "no flush: ~%.0f MiB touched per step >> 126 MB L2" % (step_bytes / 2**20)},
+                       "budget": budget, "rho": args.rho, "C": 32, "delta": 14, "page_size": 16,
+                       "parallelism": f"batch-shard x{world}",
+                       "l2": "no flush: ~%.0f MiB touched per step >> 126 MB L2" %
+                             (main_res["bytes_per_step"] / 2 ** 20)},
             "us_per_step": step_ms * 1e3,
-            "step_ms_p10_p50_p90": [float(np.percentile(per_step, p)) for p in (10, 50, 90)],
             "us_per_layer": step_ms * 1e3 / L,
-            "bytes_per_step": step_bytes,
-            "union_factor": union_rows / (L * B * Hkv * budget),
-            "roofline": {"bound": "hbm", "kernel": "k_decode_attn (a7+a8)", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("k_decode_attn"),
-                         "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": attn_bytes_per_launch,
-                         "avg_launch_us": attn_ms * 1e3,
-                         "timing": "CUDA events around an L-layer graph of the kernel's launches (back to back, "
-                                   "PDL-chained), per launch",
-                         "select_us_per_layer": sel_ms * 1e3,
-                         "score_us_per_layer": score_ms * 1e3,
-                         "score_frac_of_peak": score_bytes_per_launch / (score_ms * 1e-3) / 1e9 / peak,
-                         "select_bytes_per_launch": score_bytes_per_launch,
-                         "step_frac_of_peak": (step_bytes / (step_ms * 1e-3) / 1e9) / peak},
-            "e2e": {"value": all_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "gpu_launches": 3 * L * args.steps,   # k_score_blocks_tc, k_select_reg, k_decode_attn per layer
+            "step_ms_p10_p50_p90": main_res["step_ms_p10_p50_p90"],
+            "bytes_per_step": main_res["bytes_per_step"],
+            "union_factor": main_res["union_factor"],
+            "roofline": main_res["roofline"],
+            "e2e": dict(main_res["e2e"], value=all_bytes / (e2e_ms * 1e-3) / 1e9, ms_per_step=e2e_ms),
+            "gpu_launches": main_res["fused_launches_per_step"] * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        if "dense" in main_res:
+            line["dense"] = main_res["dense"]
+        if "three_kernel_path" in main_res:
+            line["three_kernel_path"] = main_res["three_kernel_path"]
+        line.update(extra)
         if prefill:
             line["prefill"] = prefill
-        if dense_ms:
-            dense_bytes = L * B * Hkv * S * 2 * d * e
-            line["dense"] = {"ms_per_step": dense_ms_v, "GB_s": dense_bytes / (dense_ms_v * 1e-3) / 1e9,
-                             "sparse_speedup": dense_ms_v / step_ms}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
