@@ -476,18 +476,20 @@ def decode_block(args, torch, D, wl: Workload, L, budget, dev, cur, world, barri
                                     "note": "k_score_blocks_tc -> k_select_reg -> k_decode_attn per layer "
                                             "(DYNSPLIT_NO_FUSED), context"}
     if with_e2e:
-        # e2e through the exported host-buffer call dynsplit_decode_step_host:
-        # per layer the H2D copy of q from pinned memory, the decode, the D2H
-        # copies of o and lse; the host reads the step's result (synchronise)
-        q_h = [wl.qs[l % Ld].cpu().pin_memory() for l in range(L)]
-        o_h = [torch.empty(B, Hq, d).pin_memory() for _ in range(L)]
-        l_h = [torch.empty(B, Hq).pin_memory() for _ in range(L)]
-        wsh = D.workspace(D.step_host_workspace_bytes(shape, cfg, budget), dev, "step_host")
+        # e2e through the exported whole-step host-buffer call
+        # dynsplit_decode_step_host_layers: every step ONE copy of every
+        # layer's q from pinned host memory, the L decode layers, ONE copy
+        # each of every layer's o and lse back to pinned host memory; the host
+        # reads the step's result (synchronise)
+        q_h = torch.stack([wl.qs[l % Ld].cpu() for l in range(L)]).pin_memory()
+        o_h = torch.empty(L, B, Hq, d).pin_memory()
+        l_h = torch.empty(L, B, Hq).pin_memory()
+        lays = [wl.layers[l % Ld] for l in range(L)]
+        wsh = D.workspace(D.step_host_layers_workspace_bytes(shape, cfg, budget, L), dev, "step_host_layers")
         wlh = D._sel_outputs(shape, cfg, budget, dev, want_blocks=False)[4]
 
         def host_step():
-            for l in range(L):
-                D.decode_step_host(q_h[l], wl.layers[l % Ld], budget, o_h[l], l_h[l], wlh, wsh)
+            D.decode_step_host_layers(q_h, lays, budget, o_h, l_h, wlh, wsh)
 
         for _ in range(args.warmup):
             host_step()
@@ -500,11 +502,11 @@ def decode_block(args, torch, D, wl: Workload, L, budget, dev, cur, world, barri
         ev1.record(cur)
         barrier()
         e2e_ms = ev0.elapsed_time(ev1) / args.steps
-        h2d = sum(x.numel() * x.element_size() for x in q_h)
-        d2h = sum(x.numel() * 4 for x in o_h) + sum(x.numel() * 4 for x in l_h)
+        h2d = q_h.numel() * q_h.element_size()
+        d2h = o_h.numel() * 4 + l_h.numel() * 4
         res["e2e"] = {"value": step_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                      "api": "dynsplit_decode_step_host (host q/o/lse, pinned), one call per layer"}
+                      "api": "dynsplit_decode_step_host_layers (pinned host q/o/lse, one call per step)"}
     if with_dense:
         wsd = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "decode")
 

@@ -404,6 +404,28 @@ dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* shape, const dyn
                                           float* lse_host, void* worklist, void* ws,
                                           size_t ws_bytes, void* stream);
 
+/* One decode token through n_layers layers of one model with HOST queries
+ * and outputs -- the whole-step form of dynsplit_decode_step_host (KV
+ * selection Steps 1-3 per layer): ONE copy of every layer's query
+ * q_host (pinned, kv dtype [n_layers, B, Hq, d]) to the device, the
+ * n_layers decode layers back to back (dynsplit_decode_layer on layer l's
+ * digests[l], Kp[l], Vp[l]; the plan -- block_starts, n_blocks, page_first --
+ * is per sequence and shared by every layer), then ONE copy each of all o
+ * (fp32 [n_layers, B, Hq, d]) and all lse (fp32 [n_layers, B, Hq]) back to
+ * o_host / lse_host (pinned).  digests / Kp / Vp are HOST arrays of n_layers
+ * device pointers.  Asynchronous: synchronise `stream` before reading the
+ * outputs.  Workspace: dynsplit_step_host_layers_workspace_bytes.  Errors
+ * as dynsplit_decode_layer (n_layers < 1: INVALID_ARGUMENT). */
+size_t dynsplit_step_host_layers_workspace_bytes(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                                 int32_t budget, int32_t n_layers);
+dynsplit_status dynsplit_decode_step_host_layers(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                                 int32_t budget, int32_t n_layers, const void* q_host,
+                                                 const void* const* digests, const int32_t* block_starts,
+                                                 const int32_t* n_blocks, const int32_t* page_first,
+                                                 const void* const* Kp, const void* const* Vp, float scale,
+                                                 float* o_host, float* lse_host, void* worklist, void* ws,
+                                                 size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

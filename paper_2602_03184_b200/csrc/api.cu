@@ -800,4 +800,58 @@ dynsplit_status dynsplit_decode_step_host(const dynsplit_shape* s, const dynspli
   return DYNSPLIT_OK;
 }
 
+// ---- the whole-step host-buffer form
+static size_t host_layers_extra(const dynsplit_shape* s, int32_t n_layers) {
+  const size_t L = (size_t)(n_layers > 0 ? n_layers : 0);
+  return align_up(L * s->B * s->Hq * kD * esize(s)) + align_up(L * s->B * s->Hq * kD * 4) +
+         align_up(L * s->B * s->Hq * 4) + 3 * align_up((size_t)s->B * s->Hq * 4);
+}
+
+size_t dynsplit_step_host_layers_workspace_bytes(const dynsplit_shape* s, const dynsplit_config* c,
+                                                 int32_t budget, int32_t n_layers) {
+  (void)budget;
+  if (check_shape(s) != DYNSPLIT_OK || check_cfg(c) != DYNSPLIT_OK || n_layers < 1) return 0;
+  return layer_ws(s, c) + host_layers_extra(s, n_layers);
+}
+
+dynsplit_status dynsplit_decode_step_host_layers(const dynsplit_shape* s, const dynsplit_config* c,
+                                                 int32_t budget, int32_t n_layers, const void* q_host,
+                                                 const void* const* digests, const int32_t* block_starts,
+                                                 const int32_t* n_blocks, const int32_t* page_first,
+                                                 const void* const* Kp, const void* const* Vp, float scale,
+                                                 float* o_host, float* lse_host, void* worklist, void* ws,
+                                                 size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (n_layers < 1 || !q_host || !digests || !Kp || !Vp || !o_host || !lse_host || !ws || !worklist)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < dynsplit_step_host_layers_workspace_bytes(s, c, budget, n_layers))
+    return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t L = (size_t)n_layers, rows = (size_t)s->B * s->Hq;
+  const size_t qbytes = rows * kD * esize(s);
+  char* extra = static_cast<char*>(ws) + layer_ws(s, c);
+  char* q_dev = extra;
+  float* o_dev = reinterpret_cast<float*>(extra + align_up(L * qbytes));
+  float* lse_dev = reinterpret_cast<float*>(reinterpret_cast<char*>(o_dev) + align_up(L * rows * kD * 4));
+  int32_t* nsel = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(lse_dev) + align_up(L * rows * 4));
+  int32_t* marg = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(nsel) + align_up(rows * 4));
+  int32_t* keep = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(marg) + align_up(rows * 4));
+  if (cudaMemcpyAsync(q_dev, q_host, L * qbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return DYNSPLIT_ERR_CUDA;
+  // the copy is not a PDL primary: the first layer's pre-wait prologue reads
+  // only resident inputs, and q after its wait
+  for (size_t l = 0; l < L; ++l) {
+    if (!digests[l] || !Kp[l] || !Vp[l]) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+    DSK_TRY(decode_layer_impl(s, c, budget, q_dev + l * qbytes, digests[l], block_starts, n_blocks, page_first,
+                              Kp[l], Vp[l], scale, nsel, marg, keep, worklist, o_dev + l * rows * kD,
+                              lse_dev + l * rows, ws, stream));
+  }
+  if (cudaMemcpyAsync(o_host, o_dev, L * rows * kD * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(lse_host, lse_dev, L * rows * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return DYNSPLIT_ERR_CUDA;
+  return DYNSPLIT_OK;
+}
+
 }  // extern "C"

@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     const __grid_constant__ CUtensorMap tmD, const bf16* __restrict__ q,
     const int32_t* __restrict__ block_starts, const int32_t* __restrict__ n_blocks,
     const int32_t* __restrict__ page_first, const bf16* __restrict__ Kp, const bf16* __restrict__ Vp, int Hq,
-    int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int cap, int ent_cap, int nwords,
+    int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int cap, int cap2, int ent_cap, int nwords,
     int sstride, size_t region_a, int per_cap, float scale_log2, float* __restrict__ scores,
     float4* __restrict__ mom, int4* __restrict__ cls_w, int* __restrict__ cls_sub, uint2* __restrict__ cls_band,
     uint32_t* __restrict__ gbits,
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     int32_t* __restrict__ keep_out, int32_t* __restrict__ wl_count, WLEntry* __restrict__ wl,
     float* __restrict__ o, float* __restrict__ lse, int* __restrict__ err) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar, bar2, bar_plan;
+  __shared__ __align__(8) uint64_t barD[2], bar2, bar_plan;
   __shared__ FusedScratch F;
   __shared__ SelScratch2<G> S2;
   __shared__ float2 red_m[kFNW][8];
@@ -560,17 +560,22 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   //      digests into smem by TMA
   const int per = (((nb + NS - 1) / NS) + kFBox - 1) & ~(kFBox - 1);
   const int lo = min(nb, split * per), hi = min(nb, lo + per), n = hi - lo;
-  const size_t slab = (size_t)cap * kFSlabRowB;
+  // digest staging: one buffer of `cap` rows when the range fits it, else two
+  // buffers of `cap2` rows (the next round loads while this one is scored)
+  const bool dbl = n > cap;
+  const int rows = dbl ? cap2 : cap;
+  const size_t slab = (size_t)rows * kFSlabRowB;
   const int row0 = bh * maxb + lo;
-  auto stage = [&](int r0, int cnt) {  // rows r0 .. r0 + cnt of the range -> smem rows 0 ..
+  auto stage = [&](int r0, int cnt, int buf) {  // rows r0 .. r0 + cnt of the range -> buffer buf
     if (tid == 0) {
       const int nbox = (cnt + kFBox - 1) / kFBox;
-      mbar_arrive_expect_tx(&bar, (uint32_t)(nbox * 4 * kFBox * kFSlabRowB));
+      unsigned char* base = smA + (size_t)buf * 4 * slab;
+      mbar_arrive_expect_tx(&barD[buf], (uint32_t)(nbox * 4 * kFBox * kFSlabRowB));
       for (int j = 0; j < nbox; ++j)
 #pragma unroll
         for (int sl = 0; sl < 4; ++sl)
-          tma_load_2d(smA + sl * slab + (size_t)j * kFBox * kFSlabRowB, &tmD, sl * 64, row0 + r0 + j * kFBox,
-                      &bar);
+          tma_load_2d(base + sl * slab + (size_t)j * kFBox * kFSlabRowB, &tmD, sl * 64, row0 + r0 + j * kFBox,
+                      &barD[buf]);
     }
   };
   // a plan row is copied from its 16-byte aligned-down start (skip ints),
@@ -591,7 +596,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   const uint32_t bs_bytes = row_bytes(bs_row, skip_bs, nb + 1, arr_end_bs);
   const uint32_t pf_bytes = row_bytes(pf_row, skip_pf, nb, arr_end_pf);
   if (tid == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&barD[0], 1);
+    mbar_init(&barD[1], 1);
     mbar_init(&bar2, 1);
     mbar_init(&bar_plan, 1);
     fence_mbar_init();
@@ -599,7 +605,10 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     if (bs_bytes) bulk_g2s(sbs_st, bs_row - skip_bs, bs_bytes, &bar_plan, policy_evict_last());
     if (pf_bytes) bulk_g2s(spf_st, pf_row - skip_pf, pf_bytes, &bar_plan, policy_evict_last());
   }
-  if (n > 0) stage(0, min(cap, n));
+  if (n > 0) {
+    stage(0, min(rows, n), 0);
+    if (dbl) stage(rows, min(rows, n - rows), 1);
+  }
   int32_t* sbs = sbs_st + skip_bs;
   int32_t* spf = spf_st + skip_pf;
   mbar_wait(&bar_plan, 0);
@@ -648,7 +657,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       }
       wl_count[bh] = 0;
     }
-    if (n > 0) mbar_wait(&bar, 0);  // the staging must land before region A is reused
+    if (n > 0) mbar_wait(&barD[0], 0);  // the staging must land before region A is reused
+    if (dbl) mbar_wait(&barD[1], 0);
     if (split != 0) return;
     // no pages: o = 0 and lse = -inf for the G heads (as the unfused path)
     attn_bf16_pipeline<G, kFNW, kFD>(smA, s_rows, s_q, 1, P, 0, [](int, int&, uint32_t&, uint32_t&) {}, Kp, Vp,
@@ -696,20 +706,17 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     float* srow_g = scores + ((size_t)b * Hq + hk * G + g) * sstride + lo;
     const int lr = lane & 7, lc = lane >> 3;
     const uint32_t sbase_u = smem_u32(smA);
-    uint32_t phase = 0;
-    for (int r0 = 0; r0 < n; r0 += cap, phase ^= 1u) {
-      const int c_n = min(cap, n - r0);
-      if (r0) {
-        __syncthreads();  // the previous round's rows are consumed
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        stage(r0, c_n);
-      }
-      mbar_wait(&bar, phase);
+    int rd = 0;
+    for (int r0 = 0; r0 < n; r0 += rows, ++rd) {
+      const int c_n = min(rows, n - r0);
+      const int buf = dbl ? (rd & 1) : 0;
+      mbar_wait(&barD[buf], dbl ? ((rd >> 1) & 1u) : (rd & 1u));
       if (r0 == 0) fstamp(15);
+      const uint32_t sbuf_u = sbase_u + (uint32_t)((size_t)buf * 4 * slab);
       for (int grp = warp; grp * 8 < c_n; grp += kFNW) {
         float c[4] = {0.f, 0.f, 0.f, 0.f};
         const int r = grp * 8 + lr;
-        const uint32_t rowa = sbase_u + (uint32_t)(r * kFSlabRowB);
+        const uint32_t rowa = sbuf_u + (uint32_t)(r * kFSlabRowB);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // two k-steps (32 dims) per ldmatrix.x4
           const uint32_t chunk = (uint32_t)((((kk & 1) << 2) | lc) ^ (r & 7));
@@ -734,6 +741,13 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
             s2 = fmaf(c[1], c[1], s2);
           }
         }
+      }
+      // this buffer takes the round after next (two buffers) or the next one (one)
+      const int nxt = r0 + (dbl ? 2 : 1) * rows;
+      if (nxt < n) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async-proxy writes
+        __syncthreads();                                                // every warp is done with the buffer
+        stage(nxt, min(rows, n - nxt), buf);
       }
     }
     // the range's moments per head (fixed order: lanes, then warps)
@@ -1150,7 +1164,7 @@ template <int G>
 static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cudaStream_t st, const bf16* q,
                              const int32_t* bs, const int32_t* nb, const int32_t* pf, const bf16* Kp,
                              const bf16* Vp, int Hq, int Hkv, int maxb, int max_pages, int S, int Pshift,
-                             int budget, int cap, int ent_cap, int nwords, int sstride, size_t region_a,
+                             int budget, int cap, int cap2, int ent_cap, int nwords, int sstride, size_t region_a,
                              int per_cap, float sl2, float* scores, float4* mom, int4* cls_w, int* cls_sub,
                              uint2* cls_band, uint32_t* gbits, int* counters, unsigned* gbar,
                              float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
@@ -1158,7 +1172,7 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
   allow_max_dyn_smem(k_decode_fused<G>);
   if (occupancy_of(k_decode_fused<G>, kFNT, smem) < 1) return cudaErrorNotSupported;
   launch_ex(k_decode_fused<G>, grid, dim3(kFNT), smem, st, 1, tm, q, bs, nb, pf, Kp, Vp, Hq, Hkv, maxb,
-            max_pages, S, Pshift, budget, cap, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores, mom,
+            max_pages, S, Pshift, budget, cap, cap2, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores, mom,
             cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep, wl_count, wl, o,
             lse, err);
   g_fused_launches.fetch_add(1);
@@ -1196,6 +1210,7 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   region_a = max(region_a, (size_t)cap * 4 * kFSlabRowB);
   region_a = max(region_a, (size_t)kFNW * G * kScStride * 4);
   region_a = (region_a + 1023) & ~(size_t)1023;
+  const int cap2 = max(kFBox, (int)(region_a / (2 * 4 * kFSlabRowB)) / kFBox * kFBox);  // two staging buffers
   const int ent_cap = min(512, (max_pages + NS - 1) / NS + 1);
   const int per_cap = (((maxb + NS - 1) / NS) + kFBox - 1) & ~(kFBox - 1);  // >= any range
   const size_t smem = 1024 + region_a + (size_t)2 * (nwords * 32 + 8) * 4 + (size_t)ent_cap * 16 +
@@ -1226,7 +1241,7 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
 #define DSK_FU(GG)                                                                                        \
   return run_fused<GG>(tm, grid, smem, st, static_cast<const bf16*>(q), bs, nb, pf,                       \
                        static_cast<const bf16*>(Kp), static_cast<const bf16*>(Vp), Hq, Hkv, maxb, max_pages, \
-                       S, Pshift, budget, cap, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores,    \
+                       S, Pshift, budget, cap, cap2, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores, \
                        mom, cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, \
                        keep,                                                                                \
                        wl_count, wl, o, lse, err)

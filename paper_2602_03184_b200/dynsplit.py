@@ -91,6 +91,9 @@ SIGNATURES = {
     "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
     "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
                                        ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_step_host_layers_workspace_bytes": (_SZ, [_PS, _PC, _I, _I]),
+    "dynsplit_decode_step_host_layers": (_I, [_PS, _PC, _I, _I, _P, _P, _P, _P, _P, _P, _P,
+                                              ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
 }
 
 _lib = None
@@ -560,6 +563,33 @@ def decode_step_host(q_host, layer: PagedLayer, budget: int, o_host, lse_host, w
         _ptr(layer.Kp), _ptr(layer.Vp), _ptr(layer.page_valid), ctypes.c_float(scale),
         ctypes.c_void_p(o_host.data_ptr()), ctypes.c_void_p(lse_host.data_ptr()), _ptr(worklist),
         _ptr(ws), ws.numel(), _stream()), "decode_step_host")
+
+
+def decode_step_host_layers(q_host, layers, budget: int, o_host, lse_host, worklist, ws, scale: float = 0.0):
+    """One token through len(layers) layers with pinned HOST q [L, B, Hq, d]
+    and o [L, B, Hq, d] / lse [L, B, Hq] through dynsplit_decode_step_host_layers
+    (the layers share one plan)."""
+    L, B, Hq, d = q_host.shape
+    s = layers[0].shape
+    shape = make_shape(B, s.S, Hq, s.Hkv, d, 1, _dtype_code(q_host))
+    for t in (q_host, o_host, lse_host):
+        if t.is_cuda or not t.is_pinned():
+            raise DynsplitError("decode_step_host_layers expects pinned host tensors")
+    arr = ctypes.c_void_p * L
+    dig = arr(*[lay.digests.data_ptr() for lay in layers])
+    kp = arr(*[lay.Kp.data_ptr() for lay in layers])
+    vp = arr(*[lay.Vp.data_ptr() for lay in layers])
+    lay0 = layers[0]
+    _check(lib().dynsplit_decode_step_host_layers(
+        ctypes.byref(shape), ctypes.byref(lay0.cfg), budget, L, ctypes.c_void_p(q_host.data_ptr()),
+        ctypes.cast(dig, ctypes.c_void_p), _ptr(lay0.block_starts), _ptr(lay0.n_blocks), _ptr(lay0.page_first),
+        ctypes.cast(kp, ctypes.c_void_p), ctypes.cast(vp, ctypes.c_void_p), ctypes.c_float(scale),
+        ctypes.c_void_p(o_host.data_ptr()), ctypes.c_void_p(lse_host.data_ptr()), _ptr(worklist), _ptr(ws),
+        ws.numel(), _stream()), "decode_step_host_layers")
+
+
+def step_host_layers_workspace_bytes(shape: Shape, cfg: Config, budget: int, n_layers: int) -> int:
+    return lib().dynsplit_step_host_layers_workspace_bytes(ctypes.byref(shape), ctypes.byref(cfg), budget, n_layers)
 
 
 def step_host_workspace_bytes(shape: Shape, cfg: Config, budget: int) -> int:

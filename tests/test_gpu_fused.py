@@ -204,3 +204,27 @@ def test_fused_layers_graph_replay(D):
         for (o, l), (ro, rl) in zip(outs, ref):
             assert torch.equal(o, ro) and torch.equal(l, rl)
     assert D.read_device_error(ws) == 0
+
+
+def test_step_host_layers_equals_device_layers(D):
+    """dynsplit_decode_step_host_layers (one H2D of every layer's q, the
+    layers back to back, one D2H each of o and lse) equals dynsplit_decode_layer
+    per layer bit for bit."""
+    B, S, Hq, Hkv, d, budget, L = 2, 6000, 32, 8, 128, 500, 3
+    toks = np.stack([G.tokens(3500 + b, S) for b in range(B)])
+    layers, qs = [], []
+    for l in range(L):
+        q, K, V = zip(*[G.decode_qkv(3510 + 10 * l + b, S, Hq, Hkv, d) for b in range(B)])
+        layers.append(build(D, toks, np.stack(K), np.stack(V), Hq))
+        qs.append(t(np.stack(q), torch.bfloat16))
+    ref = [D.decode_layer(qs[l], layers[l], budget)[:2] for l in range(L)]
+    q_h = torch.stack([x.cpu() for x in qs]).pin_memory()
+    o_h = torch.empty(L, B, Hq, d).pin_memory()
+    l_h = torch.empty(L, B, Hq).pin_memory()
+    shape = D.make_shape(B, S, Hq, Hkv, d)
+    ws = D.workspace(D.step_host_layers_workspace_bytes(shape, layers[0].cfg, budget, L), DEV, "shl_test")
+    wl = D._sel_outputs(shape, layers[0].cfg, budget, DEV, want_blocks=False)[4]
+    D.decode_step_host_layers(q_h, layers, budget, o_h, l_h, wl, ws)
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert torch.equal(o_h[l], ref[l][0].cpu()) and torch.equal(l_h[l], ref[l][1].cpu())
