@@ -86,3 +86,38 @@ def test_prefill_scoring_64k_sampled():
     for i in sample:
         assert abs(s[i] - ref[i]) <= 2e-4, (i, s[i], ref[i])
     assert np.isnan(s[S - 1]) and np.sum(~np.isnan(s)) == len(cands)
+
+
+def test_decode_128k_batch8():
+    """Config 3 unsharded (all 8 sequences of 128K on one GPU, the bench's
+    c3_b8 block): dynsplit_decode_layer (one k_decode_fused launch, 2 splits
+    per (sequence, KV head), double-buffered digest staging) against the
+    three-kernel path bit for bit and every head of every sequence against
+    the oracle."""
+    from paper_2602_03184_b200 import dynsplit as D
+    B, S, Hq, Hkv, d, budget = 8, 131072, 32, 8, 128, 4096
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(2200 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, cfg.C, cfg.delta) for b in range(B)]
+    qs, Ks, Vs = zip(*[G.decode_qkv(2300 + b, S, Hq, Hkv, d) for b in range(B)])
+    q = np.stack(qs)
+    q = H.certify_queries(2300, q, np.stack(Ks), starts, budget)
+    layer = D.build_blocks(t(toks), t(G.T7_IDS), t(np.stack(Ks), torch.bfloat16), t(np.stack(Vs), torch.bfloat16),
+                           cfg, static_w10=G.T7_W10, Hq=Hq)
+    qt = t(q, torch.bfloat16)
+    o_l, lse_l, sel_l = D.decode_layer(qt, layer, budget)
+    sel = D.select(qt, layer, budget)
+    o, lse = D.decode_attn(qt, layer, sel.worklist)
+    torch.cuda.synchronize()
+    assert torch.equal(o_l, o) and torch.equal(lse_l, lse)
+    for name in ("n_sel", "marginal_block", "marginal_keep"):
+        assert torch.equal(getattr(sel_l, name), getattr(sel, name)), name
+    o_np, lse_np = o_l.cpu().numpy(), lse_l.cpu().numpy()
+    mg, kp, ns = sel_l.marginal_block.cpu().numpy(), sel_l.marginal_keep.cpu().numpy(), sel_l.n_sel.cpu().numpy()
+    for b in range(B):
+        res = O.decode_step(q[b], Ks[b], Vs[b], starts[b], budget)
+        for h in range(Hq):
+            assert ns[b, h] == len(res["sel_blocks"][h]) and mg[b, h] == res["marginal"][h] \
+                and kp[b, h] == res["keep"][h], (b, h)
+        assert np.all(H.row_rel_err(o_np[b], res["o"]) <= 2e-3)
+        assert np.all(np.abs(lse_np[b] - res["lse"]) <= 1e-4 * np.maximum(1, np.abs(res["lse"])))
