@@ -481,6 +481,39 @@ def select_blocks_direct(scores, block_starts, budget):
     return sorted(chosen), marginal, keep, np.array(sorted(toks), np.int64)
 
 
+def group_block_scores(q_group, kmax_h, kmin_h):
+    """NEXT-2 group-shared GQA selection (DESIGN R23): one score per block for
+    the g query heads of a KV head, the sum of the heads' V2F scores,
+    sum_{h in group} sum_j max(q_hj kmax_j, q_hj kmin_j), so the group takes
+    ONE selection (the paper runs GQA models; its shapes are per query
+    head, P:749).  q_group [g, d]."""
+    return np.sum([block_scores(qh, kmax_h, kmin_h) for qh in _f64(q_group)], axis=0)
+
+
+def select_whole_blocks(scores, block_starts, budget):
+    """NEXT-2 whole-block budget (DESIGN R24; "select the top-k highest-scoring
+    blocks"): blocks in (score desc, index asc) order are taken whole
+    until their lengths reach the budget -- the block that reaches it is taken
+    whole as well (k = the fewest top blocks covering the budget).  Returns
+    (ascending blocks, marginal block, its length, ascending tokens); (all,
+    -1, 0, all) when every token fits."""
+    bs = [int(x) for x in block_starts]
+    nb = len(bs) - 1
+    if bs[-1] - bs[0] <= int(budget):
+        return list(range(nb)), -1, 0, np.arange(bs[0], bs[-1], dtype=np.int64)
+    order = sorted(range(nb), key=lambda b: (-float(scores[b]), b))
+    total = 0
+    chosen = []
+    for b in order:
+        chosen.append(b)
+        total += bs[b + 1] - bs[b]
+        if total >= int(budget):
+            break
+    m = chosen[-1]
+    toks = np.concatenate([np.arange(bs[b], bs[b + 1]) for b in sorted(chosen)]).astype(np.int64)
+    return sorted(chosen), m, bs[m + 1] - bs[m], toks
+
+
 # ---------------------------------------------------------------------------
 # O8  Attention over the selected set (Step 3, P:753; S:359-372, Q20):
 #     z = q.k * scale, p = softmax(z), o = sum p v, lse = log sum exp z.
@@ -523,10 +556,15 @@ def merge_partials(o_parts, lse_parts):
 # ---------------------------------------------------------------------------
 # One decode step for one sequence and one layer (Steps 1-3).
 # ---------------------------------------------------------------------------
-def decode_step(q, K, V, block_starts, budget, scale=None, digest_mode="minmax"):
+def decode_step(q, K, V, block_starts, budget, scale=None, digest_mode="minmax", gqa_mode="head",
+                budget_mode="token"):
     """q [Hq, d]; K, V [S, Hkv, d].  Per query head (Q18): O5 digests, O6
     scores, O7 selection, O8 attention.  digest_mode "mean" uses the
-    mean-pooling variant.  Returns a dict of per-head results."""
+    mean-pooling variant.  NEXT-2 variants: gqa_mode "group"
+    scores every block once per KV head with group_block_scores and the g
+    query heads share that selection (R23); budget_mode "whole" takes the
+    budget-reaching block whole (select_whole_blocks, R24).  Returns a dict of
+    per-head results ("scores" are the scores the selection used)."""
     q = _f64(q)
     Hq, d = q.shape
     Hkv = np.asarray(K).shape[1]
@@ -543,9 +581,17 @@ def decode_step(q, K, V, block_starts, budget, scale=None, digest_mode="minmax")
     Vf = _f64(V)
     for h in range(Hq):
         hk = h // g
-        sc = block_scores_mean(q[h], kmean[hk]) if digest_mode == "mean" else block_scores(q[h], kmax[hk], kmin[hk])
-        toks = select_tokens(sc, block_starts, budget)
-        sb, m, keep = selection_from_tokens(toks, sc, block_starts, budget)
+        if gqa_mode == "group":
+            sc = group_block_scores(q[hk * g:(hk + 1) * g], kmax[hk], kmin[hk])
+        elif digest_mode == "mean":
+            sc = block_scores_mean(q[h], kmean[hk])
+        else:
+            sc = block_scores(q[h], kmax[hk], kmin[hk])
+        if budget_mode == "whole":
+            sb, m, keep, toks = select_whole_blocks(sc, block_starts, budget)
+        else:
+            toks = select_tokens(sc, block_starts, budget)
+            sb, m, keep = selection_from_tokens(toks, sc, block_starts, budget)
         o, lse = sparse_attention(q[h], Kf[:, hk, :], Vf[:, hk, :], toks, scale)
         res["scores"].append(sc)
         res["tokens"].append(toks)

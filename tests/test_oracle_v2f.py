@@ -185,3 +185,93 @@ def test_mean_mode_full_budget_equals_dense():
     for h in range(4):
         o, lse = O.dense_attention(q[h], K[:, h // 2], V[:, h // 2], 1 / math.sqrt(16))
         assert np.allclose(res["o"][h], o, rtol=0, atol=1e-12) and abs(res["lse"][h] - lse) < 1e-12
+
+
+# ---------------------------------------------------------------- NEXT-2 variants (DESIGN R23, R24)
+def _rand_plan(r, S, lo=18, hi=46):
+    bs = [0]
+    while bs[-1] < S:
+        bs.append(min(S, bs[-1] + int(r.integers(lo, hi + 1))))
+    return bs
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_group_scores_bound_the_group_logits(seed):
+    """Sum of the heads' Quest bounds >= sum over heads of each head's best
+    logit in the block >= the best summed logit of one token (an upper bound
+    of the group's attention logits, brute force over tokens)."""
+    r = G.rng(seed, 41)
+    S, g, d = 300, 4, 16
+    K = r.standard_normal((S, 1, d))
+    q = r.standard_normal((g, d))
+    bs = _rand_plan(r, S, 3, 12)
+    kmax, kmin = O.digests(K, bs)
+    sc = O.group_block_scores(q, kmax[0], kmin[0])
+    for b in range(len(bs) - 1):
+        logits = q @ K[bs[b]:bs[b + 1], 0].T          # [g, len]
+        assert sc[b] >= logits.max(axis=1).sum() - 1e-9
+        assert logits.max(axis=1).sum() >= logits.sum(axis=0).max() - 1e-9
+
+
+def test_group_mode_reduces_to_per_head():
+    """g = 1 (MHA): group mode is the per-head method; identical queries in a
+    group: the group score is g x each head's score, so every head selects
+    what per-head selection selects."""
+    r = G.rng(3, 42)
+    S, d = 400, 16
+    bs = _rand_plan(r, S)
+    K, V = r.standard_normal((S, 2, d)), r.standard_normal((S, 2, d))
+    q1 = r.standard_normal((2, d))
+    a = O.decode_step(q1, K, V, bs, 90, gqa_mode="group")
+    b = O.decode_step(q1, K, V, bs, 90)
+    assert a["sel_blocks"] == b["sel_blocks"] and a["marginal"] == b["marginal"] and a["keep"] == b["keep"]
+    assert np.array_equal(a["o"], b["o"])
+    q4 = np.repeat(r.standard_normal((2, 1, d)), 4, axis=1).reshape(8, d)   # Hq = 8, Hkv = 2, identical in-group
+    a = O.decode_step(q4, K, V, bs, 90, gqa_mode="group")
+    b = O.decode_step(q4, K, V, bs, 90)
+    assert a["sel_blocks"] == b["sel_blocks"] and a["marginal"] == b["marginal"]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_group_mode_shares_one_selection_of_exactly_budget(seed):
+    """Every head of a KV group takes the same tokens, exactly `budget` of
+    them, so the union over the group is 1x the budget."""
+    r = G.rng(seed, 43)
+    S, Hq, Hkv, d, budget = 600, 8, 2, 16, 150
+    bs = _rand_plan(r, S)
+    K, V = r.standard_normal((S, Hkv, d)), r.standard_normal((S, Hkv, d))
+    q = r.standard_normal((Hq, d))
+    res = O.decode_step(q, K, V, bs, budget, gqa_mode="group")
+    for hk in range(Hkv):
+        toks = [res["tokens"][h].tolist() for h in range(hk * 4, hk * 4 + 4)]
+        assert all(t == toks[0] for t in toks) and len(toks[0]) == budget
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_whole_blocks_extend_the_token_selection(seed):
+    """Whole-block budget = the token-exact selection plus the rest of its
+    marginal block: >= budget tokens, fewer than budget + the marginal
+    block's length, every selected block whole; a budget ending on a block
+    boundary selects the same tokens in both modes; budget >= S takes all."""
+    r = G.rng(seed, 44)
+    S = 500
+    bs = _rand_plan(r, S)
+    sc = r.standard_normal(len(bs) - 1)
+    sc[r.integers(0, len(sc), 5)] = sc[0]                      # ties
+    for budget in (1, 37, 120, 499, 500, 900):
+        blocks, m, ln, toks = O.select_whole_blocks(sc, bs, budget)
+        exact = O.select_tokens(sc, bs, budget)
+        if budget >= S:
+            assert m == -1 and len(toks) == S
+            continue
+        sb, m2, keep = O.selection_from_tokens(exact, sc, bs, budget)
+        assert blocks == sb and m == m2 and ln == bs[m + 1] - bs[m]
+        assert set(exact.tolist()) <= set(toks.tolist())
+        assert budget <= len(toks) < budget + ln
+        assert len(toks) - len(exact) == ln - keep
+        for b in blocks:
+            assert set(range(bs[b], bs[b + 1])) <= set(toks.tolist())
+    # the budget exactly at a block boundary of the score order
+    order = sorted(range(len(sc)), key=lambda b: (-sc[b], b))
+    budget = sum(bs[b + 1] - bs[b] for b in order[:5])
+    assert np.array_equal(O.select_whole_blocks(sc, bs, budget)[3], O.select_tokens(sc, bs, budget))
