@@ -670,6 +670,30 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline_leg(args, wl, budget)
+    # NEXT-2 variants on the same workload (paper variants, DESIGN R23 / R24):
+    # group-shared GQA selection and the whole-block budget (context keys)
+    variants = {}
+    if world == 1 and not args.no_extra:
+        import copy
+        for name, fields in (("gqa_group_shared", {"gqa_mode": 1}), ("whole_block_budget", {"budget_mode": 1})):
+            saved = [lay.cfg for lay in wl.layers]
+            cfg_v = copy.copy(wl.cfg)
+            for k2, v2 in fields.items():
+                setattr(cfg_v, k2, v2)
+            for lay in wl.layers:
+                lay.cfg = cfg_v
+            wl_cfg = wl.cfg
+            wl.cfg = cfg_v
+            try:
+                rv = decode_block(args, torch, D, wl, L, budget, dev, cur, world, barrier, peak, with_e2e=False,
+                                  with_dense=False)
+            finally:
+                wl.cfg = wl_cfg
+                for lay, c0 in zip(wl.layers, saved):
+                    lay.cfg = c0
+            variants[name] = {"ms_per_step": rv["ms_per_step"], "GB_s": rv["GB_s"],
+                              "frac_of_peak": rv["roofline"]["frac"], "union_factor": rv["union_factor"],
+                              "bytes_per_step": rv["bytes_per_step"], "config": fields}
     del wl
     torch.cuda.empty_cache()
 
@@ -742,6 +766,8 @@ def main():
         if "three_kernel_path" in main_res:
             line["three_kernel_path"] = main_res["three_kernel_path"]
         line.update(extra)
+        if variants:
+            line["variants"] = variants
         if prefill:
             line["prefill"] = prefill
         print(json.dumps(line), flush=True)

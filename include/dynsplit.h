@@ -125,6 +125,14 @@ typedef struct {
                               bound dynsplit_max_pages() derives from S.  A plan needing more sets
                               DYNSPLIT_DEVERR_PAGE_CAPACITY.  (The bound is ~1.9x what DD-Select
                               plans use at C = 32; a caller that knows n_pages can allocate tightly.) */
+  int32_t gqa_mode;        /* NEXT-2 (DESIGN R23): 0 = every query head selects on its own scores (the
+                              paper's per-head shapes; default); 1 = group-shared: the g heads of a
+                              KV head take ONE selection on the sum of their block scores (GQA).
+                              Fused decode layer only (dynsplit_decode_layer*): elsewhere UNSUPPORTED. */
+  int32_t budget_mode;     /* NEXT-2 (DESIGN R24): 0 = token-exact budget through the block-to-token
+                              mapping (default); 1 = whole blocks: "the top-k highest-scoring
+                              blocks" -- the block that reaches the budget is taken whole.
+                              Fused decode layer only, as gqa_mode. */
 } dynsplit_config;
 
 /* Fills the defaults above. */

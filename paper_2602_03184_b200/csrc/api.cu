@@ -165,6 +165,8 @@ dynsplit_status check_cfg(const dynsplit_config* c) {
   if (c->W < 1 || c->R < 1 || !(c->alpha_pen >= 0.f)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (c->digest_mode != 0 && c->digest_mode != 1) return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (c->page_cap < 0) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if ((c->gqa_mode != 0 && c->gqa_mode != 1) || (c->budget_mode != 0 && c->budget_mode != 1))
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
   return DYNSPLIT_OK;
 }
 
@@ -266,6 +268,8 @@ void dynsplit_default_config(dynsplit_config* c) {
   c->page_size = 16;
   c->digest_mode = 0;
   c->page_cap = 0;
+  c->gqa_mode = 0;
+  c->budget_mode = 0;
 }
 
 int32_t dynsplit_max_blocks(int32_t S, const dynsplit_config* c) {
@@ -533,6 +537,7 @@ static dynsplit_status select_impl(const dynsplit_shape* s, const dynsplit_confi
       !marginal_keep || !worklist)
     return DYNSPLIT_ERR_INVALID_ARGUMENT;
   if (blk_lo < 0 || blk_hi < blk_lo) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->gqa_mode || c->budget_mode) return DYNSPLIT_ERR_UNSUPPORTED;  // NEXT-2 variants: fused layer only
   const int maxb = dynsplit_max_blocks(s->S, c);
   // smem-resident keys (S up to ~300K), 8-bit page counts per block, 16-bit block lengths
   if (select_smem_needed(maxb, s->Hq / s->Hkv) == (size_t)-1) return DYNSPLIT_ERR_UNSUPPORTED;
@@ -657,11 +662,13 @@ static dynsplit_status decode_layer_impl(const dynsplit_shape* s, const dynsplit
     const int nb_hint = (int)(((int64_t)s->S * 5 + 4 * c->C - 1) / (4 * c->C));
     const cudaError_t e = launch_decode_fused(
         s->kv_dtype, c->digest_mode, s->Hq / s->Hkv, q, digests, block_starts, n_blocks, page_first, Kp, Vp,
-        s->B, s->Hq, s->Hkv, maxb, dynsplit_max_pages(s->S, c), s->S, c->page_size, budget, nb_hint, scale, sc,
+        s->B, s->Hq, s->Hkv, maxb, dynsplit_max_pages(s->S, c), s->S, c->page_size, budget, c->gqa_mode,
+        c->budget_mode, nb_hint, scale, sc,
         score_stride(s, c), fscratch, counters, counters + kMaxCounters / 2, part_o, part_lse, n_sel,
         marginal_block, marginal_keep, v.count, v.entries, o, lse, err_word(ws),
         static_cast<cudaStream_t>(stream));
     if (e != cudaErrorNotSupported) return cuda_status(e);
+    if (c->gqa_mode || c->budget_mode) return DYNSPLIT_ERR_UNSUPPORTED;  // NEXT-2 variants: fused layer only
   }
   DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
   DSK_TRY(select_impl(s, c, budget, sc, block_starts, n_blocks, page_first, 0, 0x7fffffff, nullptr, n_sel,

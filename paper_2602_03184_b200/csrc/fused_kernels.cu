@@ -515,7 +515,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     const __grid_constant__ CUtensorMap tmD, const bf16* __restrict__ q,
     const int32_t* __restrict__ block_starts, const int32_t* __restrict__ n_blocks,
     const int32_t* __restrict__ page_first, const bf16* __restrict__ Kp, const bf16* __restrict__ Vp, int Hq,
-    int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int cap, int cap2, int ent_cap, int nwords,
+    int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int gqa_mode, int budget_mode, int cap, int cap2,
+    int ent_cap, int nwords,
     int sstride, size_t region_a, int per_cap, float scale_log2, float* __restrict__ scores,
     float4* __restrict__ mom, int4* __restrict__ cls_w, int* __restrict__ cls_sub, uint2* __restrict__ cls_band,
     uint32_t* __restrict__ gbits,
@@ -726,6 +727,16 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
           mma_rows8(c, a0[2 * kk + 1], a2[2 * kk + 1], bk[2], bk[3]);
         }
         // c0, c1: head g, blocks grp * 8 + 2t, + 1 (rows 8..15 are zero)
+        if (gqa_mode) {
+          // group-shared selection (R23): every head of the group gets the sum
+          // of the G heads' scores (lanes 4g + t; rows >= G are zero), a fixed
+          // butterfly, so every CTA and every head holds the same fp32 value
+#pragma unroll
+          for (int o2 = 4; o2 < 32; o2 <<= 1) {
+            c[0] += __shfl_xor_sync(0xffffffffu, c[0], o2);
+            c[1] += __shfl_xor_sync(0xffffffffu, c[1], o2);
+          }
+        }
         const int i0 = r0 + grp * 8 + 2 * t;
         if (g < G) {
           if (i0 < n) {
@@ -950,6 +961,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       f_band_select(sband + (size_t)g2 * kBandCap, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords, m,
                     keep, T);
     }
+    if (budget_mode && m >= 0) keep = blen(sbs, m);  // whole blocks (R24): the marginal block whole
     if (lane == 0) S2.sel[g2] = make_int4(m, keep, (int)T, all | (fb << 1));
   }
   __syncthreads();
@@ -981,7 +993,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       const int wi = k * kFNW + warp;
       if (lane == 0 && wi < nwords) sbits[g2 * nwords + wi] = word;
     }
-    if (tid == 0) S2.sel[g2] = make_int4(m_c, F.info[1], (int)T_c, all_c);
+    if (tid == 0) S2.sel[g2] = make_int4(m_c, (budget_mode && m_c >= 0 && !all_c) ? blen(sbs, m_c) : F.info[1],
+                                         (int)T_c, all_c);
     __syncthreads();
   }
   // all-fit heads: every block
@@ -1164,7 +1177,8 @@ template <int G>
 static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cudaStream_t st, const bf16* q,
                              const int32_t* bs, const int32_t* nb, const int32_t* pf, const bf16* Kp,
                              const bf16* Vp, int Hq, int Hkv, int maxb, int max_pages, int S, int Pshift,
-                             int budget, int cap, int cap2, int ent_cap, int nwords, int sstride, size_t region_a,
+                             int budget, int gqa_mode, int budget_mode, int cap, int cap2, int ent_cap, int nwords,
+                             int sstride, size_t region_a,
                              int per_cap, float sl2, float* scores, float4* mom, int4* cls_w, int* cls_sub,
                              uint2* cls_band, uint32_t* gbits, int* counters, unsigned* gbar,
                              float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
@@ -1172,7 +1186,8 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
   allow_max_dyn_smem(k_decode_fused<G>);
   if (occupancy_of(k_decode_fused<G>, kFNT, smem) < 1) return cudaErrorNotSupported;
   launch_ex(k_decode_fused<G>, grid, dim3(kFNT), smem, st, 1, tm, q, bs, nb, pf, Kp, Vp, Hq, Hkv, maxb,
-            max_pages, S, Pshift, budget, cap, cap2, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores, mom,
+            max_pages, S, Pshift, budget, gqa_mode, budget_mode, cap, cap2, ent_cap, nwords, sstride, region_a,
+            per_cap, sl2, scores, mom,
             cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep, wl_count, wl, o,
             lse, err);
   g_fused_launches.fetch_add(1);
@@ -1182,7 +1197,8 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
 cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q, const void* dig,
                                 const int32_t* bs, const int32_t* nb, const int32_t* pf, const void* Kp,
                                 const void* Vp, int B, int Hq, int Hkv, int maxb, int max_pages, int S, int P,
-                                int budget, int nb_hint, float scale, float* scores, int sstride,
+                                int budget, int gqa_mode, int budget_mode, int nb_hint, float scale, float* scores,
+                                int sstride,
                                 void* fscratch, int* counters, int* bar, float* part_o, float* part_lse,
                                 int32_t* n_sel, int32_t* marg, int32_t* keep, int32_t* wl_count, WLEntry* wl,
                                 float* o, float* lse, int* err, cudaStream_t st) {
@@ -1241,7 +1257,8 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
 #define DSK_FU(GG)                                                                                        \
   return run_fused<GG>(tm, grid, smem, st, static_cast<const bf16*>(q), bs, nb, pf,                       \
                        static_cast<const bf16*>(Kp), static_cast<const bf16*>(Vp), Hq, Hkv, maxb, max_pages, \
-                       S, Pshift, budget, cap, cap2, ent_cap, nwords, sstride, region_a, per_cap, sl2, scores, \
+                       S, Pshift, budget, gqa_mode, budget_mode, cap, cap2, ent_cap, nwords, sstride,       \
+                       region_a, per_cap, sl2, scores,                                                      \
                        mom, cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, \
                        keep,                                                                                \
                        wl_count, wl, o, lse, err)

@@ -91,7 +91,8 @@ size_t fused_scratch_bytes(int B, int Hq, int maxb);
 cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q, const void* dig,
                                 const int32_t* bs, const int32_t* nb, const int32_t* pf, const void* Kp,
                                 const void* Vp, int B, int Hq, int Hkv, int maxb, int max_pages, int S, int P,
-                                int budget, int nb_hint, float scale, float* scores, int sstride,
+                                int budget, int gqa_mode, int budget_mode, int nb_hint, float scale, float* scores,
+                                int sstride,
                                 void* fscratch, int* counters, int* bar, float* part_o, float* part_lse,
                                 int32_t* n_sel, int32_t* marg, int32_t* keep, int32_t* wl_count, WLEntry* wl,
                                 float* o, float* lse, int* err, cudaStream_t st);

@@ -43,7 +43,8 @@ class Config(ctypes.Structure):
     _fields_ = [("W", ctypes.c_int32), ("R", ctypes.c_int32), ("alpha_pen", ctypes.c_float),
                 ("C", ctypes.c_int32), ("delta", ctypes.c_int32), ("lambda_num", ctypes.c_int32),
                 ("lambda_den", ctypes.c_int32), ("page_size", ctypes.c_int32),
-                ("digest_mode", ctypes.c_int32), ("page_cap", ctypes.c_int32)]
+                ("digest_mode", ctypes.c_int32), ("page_cap", ctypes.c_int32),
+                ("gqa_mode", ctypes.c_int32), ("budget_mode", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -156,3 +156,43 @@ def certify_queries_mean(seed, q, K, starts_list, budget, dtype="bf16", max_retr
                     raise RuntimeError("could not certify a query")
                 q[b, h] = G.query_resample(seed, b, h, r, d, dtype)
     return q
+
+
+def certify_queries_group(seed, q, K, starts_list, budget, max_retry=40):
+    """Group-shared selection (DESIGN R23): the score the GPU selects on is the
+    fp32 sum of the g heads' fp32 block scores.  Its error is at most the sum
+    of the heads' bounds plus the g - 1 additions' rounding (2^-24 relative
+    each, at most (g-1) 2^-23 sum_h |s_h|); resample the whole group (derived
+    sub-seeds) until the gaps around the group's marginal block exceed the
+    bounds.  q [B,Hq,d], K [B,S,Hkv,d] float32 arrays.  Returns q."""
+    q = q.copy()
+    B, Hq, d = q.shape
+    Hkv = K.shape[2]
+    g = Hq // Hkv
+    for b in range(B):
+        kmax, kmin = O.digests(K[b], starts_list[b])
+        st = starts_list[b]
+        for hk in range(Hkv):
+            r = 0
+            while True:
+                heads = range(hk * g, (hk + 1) * g)
+                s_h = [O.block_scores(q[b, h], kmax[hk], kmin[hk]) for h in heads]
+                sc = np.sum(s_h, axis=0)
+                eps = np.sum([score_error_bound(q[b, h], kmax[hk], kmin[hk], True) for h in heads], axis=0)
+                eps = eps + (g - 1) * 2.0 ** -23 * np.sum(np.abs(s_h), axis=0)
+                ok = True
+                if int(st[-1] - st[0]) > budget:
+                    order, rk = marginal_rank(sc, st, budget)
+                    m = order[rk]
+                    if rk > 0 and not sc[order[rk - 1]] - sc[m] > eps[order[rk - 1]] + eps[m]:
+                        ok = False
+                    if rk + 1 < len(order) and not sc[m] - sc[order[rk + 1]] > eps[m] + eps[order[rk + 1]]:
+                        ok = False
+                if ok:
+                    break
+                r += 1
+                if r > max_retry:
+                    raise RuntimeError("could not certify a query group")
+                for h in heads:
+                    q[b, h] = G.query_resample(seed + 7919, b, h, r, d, "bf16")
+    return q

@@ -228,3 +228,48 @@ def test_step_host_layers_equals_device_layers(D):
     torch.cuda.synchronize()
     for l in range(L):
         assert torch.equal(o_h[l], ref[l][0].cpu()) and torch.equal(l_h[l], ref[l][1].cpu())
+
+
+# ---------------------------------------------------------------- NEXT-2 variants (DESIGN R23, R24)
+@pytest.mark.parametrize("gqa,whole,kind", [(1, 0, "int"), (1, 0, "cont"), (0, 1, "cont"), (0, 1, "int"),
+                                            (1, 1, "cont")])
+def test_fused_variants_against_oracle(D, gqa, whole, kind):
+    """Group-shared GQA selection and the whole-block budget through
+    dynsplit_decode_layer (fused), against oracle.decode_step(gqa_mode,
+    budget_mode): selections exact, attention within R17; group mode streams
+    exactly the budget per (sequence, KV head) (the union is 1x)."""
+    B, S, Hq, Hkv, d, budget = 2, 9000, 32, 8, 128, 700
+    toks = np.stack([G.tokens(3600 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    gen = G.decode_qkv_integer if kind == "int" else G.decode_qkv
+    qs, Ks, Vs = zip(*[gen(3700 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    if kind == "cont":
+        q = (H.certify_queries_group(3700, q, K, starts, budget) if gqa
+             else H.certify_queries(3700, q, K, starts, budget, "bf16"))
+    cfg = D.default_config(gqa_mode=gqa, budget_mode=whole)
+    layer = D.build_blocks(t(toks), t(G.T7_IDS), t(K, torch.bfloat16), t(V, torch.bfloat16), cfg,
+                           static_w10=G.T7_W10, Hq=Hq)
+    qt = t(q, torch.bfloat16)
+    o, lse, sel = D.decode_layer(qt, layer, budget)
+    torch.cuda.synchronize()
+    res = [O.decode_step(q[b], K[b], V[b], starts[b], budget, gqa_mode="group" if gqa else "head",
+                         budget_mode="whole" if whole else "token") for b in range(B)]
+    check_oracle(sel, o, lse, res, B, Hq)
+    if gqa and not whole:
+        shape = D.make_shape(B, S, Hq, Hkv, d)
+        _, streamed = D.worklist_rows(sel.worklist, shape, Hq // Hkv)
+        assert np.all(streamed == budget), streamed
+
+
+def test_variants_unsupported_outside_the_fused_layer(D):
+    """The NEXT-2 variants exist only in the fused layer: dynsplit_select
+    refuses them (UNSUPPORTED) instead of silently selecting per head."""
+    S, Hq, Hkv, d = 3000, 8, 2, 128
+    toks = G.tokens(3800, S)[None]
+    q, K, V = G.decode_qkv(3801, S, Hq, Hkv, d)
+    cfg = D.default_config(gqa_mode=1)
+    layer = D.build_blocks(t(toks), t(G.T7_IDS), t(K[None], torch.bfloat16), t(V[None], torch.bfloat16), cfg,
+                           static_w10=G.T7_W10, Hq=Hq)
+    with pytest.raises(D.DynsplitError):
+        D.select(t(q[None], torch.bfloat16), layer, 300)
