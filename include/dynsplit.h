@@ -387,6 +387,25 @@ dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* shape, const dyn
                                           const int32_t* page_first, const void* ws, void* const* Kp,
                                           void* const* Vp, void* const* digests, void* stream);
 
+/* The same two calls with the prefix length in DEVICE memory, for decode
+ * loops captured once as a CUDA graph and replayed per token: L_prev =
+ * *L_prev_dev (read by the kernels; >= 1, a planned prefix), L = L_prev +
+ * n_new.  A length outside [1, S - n_new] sets DYNSPLIT_DEVERR_PLAN_MISMATCH
+ * and leaves the sequence untouched.  The caller advances *L_prev_dev after
+ * the step (e.g. with its own kernel). */
+dynsplit_status dynsplit_append_plan_dev(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                         const int32_t* L_prev_dev, int32_t n_new, const int32_t* tokens,
+                                         const int32_t* delim_ids, int32_t n_ids, const uint8_t* w10,
+                                         int32_t* block_starts, int32_t* n_blocks, int32_t* page_first,
+                                         int32_t* page_block, int16_t* page_valid, int32_t* n_pages,
+                                         void* ws, size_t ws_bytes, void* stream);
+dynsplit_status dynsplit_append_kv_layers_dev(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                              const int32_t* L_prev_dev, int32_t n_new, int32_t n_layers,
+                                              const void* const* K_new, const void* const* V_new,
+                                              const int32_t* block_starts, const int32_t* n_blocks,
+                                              const int32_t* page_first, const void* ws, void* const* Kp,
+                                              void* const* Vp, void* const* digests, void* stream);
+
 /* Row a8 standalone (cross-GPU merge of sequence-split shards):
  *   o_parts fp32 [n_parts, rows, d], lse_parts fp32 [n_parts, rows] ->
  *   lse = log sum_s exp(lse_s), o = sum_s exp(lse_s - lse) o_s, fixed part order. */

@@ -748,6 +748,57 @@ dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynspli
   return cuda_status(launch_fence(st));
 }
 
+dynsplit_status dynsplit_append_plan_dev(const dynsplit_shape* s, const dynsplit_config* c,
+                                         const int32_t* L_prev_dev, int32_t n_new, const int32_t* tokens,
+                                         const int32_t* delim_ids, int32_t n_ids, const uint8_t* w10,
+                                         int32_t* block_starts, int32_t* n_blocks, int32_t* page_first,
+                                         int32_t* page_block, int16_t* page_valid, int32_t* n_pages, void* ws,
+                                         size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!L_prev_dev || !tokens || !delim_ids || !w10 || !block_starts || !n_blocks || !page_first ||
+      !page_block || !page_valid || !n_pages || !ws)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_ids < 1 || n_ids > 64 || n_new < 1 || n_new > s->S) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
+  if (ws_bytes < kWsHdr + append_ws_bytes(s->B)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // L_prev = 1, L = 1 + n_new are placeholders the kernel replaces by *L_prev_dev
+  DSK_TRY(cuda_status(launch_plan_append(
+      tokens, delim_ids, n_ids, w10, s->B, s->S, dynsplit_max_blocks(s->S, c), dynsplit_max_pages(s->S, c),
+      c->C, c->delta, c->lambda_num, c->lambda_den, c->page_size, 1, 1 + n_new, block_starts, n_blocks,
+      page_first, page_block, page_valid, n_pages, reinterpret_cast<int32_t*>(ws_body(ws)), err_word(ws), st,
+      L_prev_dev)));
+  return cuda_status(launch_fence(st));
+}
+
+dynsplit_status dynsplit_append_kv_layers_dev(const dynsplit_shape* s, const dynsplit_config* c,
+                                              const int32_t* L_prev_dev, int32_t n_new, int32_t n_layers,
+                                              const void* const* K_new, const void* const* V_new,
+                                              const int32_t* block_starts, const int32_t* n_blocks,
+                                              const int32_t* page_first, const void* ws, void* const* Kp,
+                                              void* const* Vp, void* const* digests, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  if (!L_prev_dev || !block_starts || !n_blocks || !page_first || !ws || !Kp || !Vp || !digests || !K_new ||
+      !V_new)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (n_layers < 1 || n_layers > kAppendMaxLayers || n_new < 1 || n_new > s->S)
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  for (int l = 0; l < n_layers; ++l)
+    if (!Kp[l] || !Vp[l] || !digests[l] || !K_new[l] || !V_new[l]) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (c->C + c->delta > append_max_tail(s->kv_dtype)) return DYNSPLIT_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DSK_TRY(cuda_status(launch_kv_append(
+      s->kv_dtype, n_layers, K_new, V_new, n_new, s->B, s->Hkv, dynsplit_max_blocks(s->S, c),
+      dynsplit_max_pages(s->S, c), c->page_size, 1, c->C + c->delta, block_starts, n_blocks, page_first,
+      reinterpret_cast<const int32_t*>(static_cast<const char*>(ws) + kWsHdr), Kp, Vp, digests, c->digest_mode,
+      st, L_prev_dev)));
+  return cuda_status(launch_fence(st));
+}
+
 dynsplit_status dynsplit_append_kv(const dynsplit_shape* s, const dynsplit_config* c, int32_t L_prev,
                                    int32_t L, const void* K_new, const void* V_new,
                                    const int32_t* block_starts, const int32_t* n_blocks,

@@ -46,9 +46,24 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
                                                     int32_t* __restrict__ page_block,
                                                     int16_t* __restrict__ page_valid,
                                                     int32_t* __restrict__ n_pages,
-                                                    int32_t* __restrict__ ws, int* __restrict__ err) {
+                                                    int32_t* __restrict__ ws, int* __restrict__ err,
+                                                    const int32_t* __restrict__ Lp_dev) {
   __shared__ int s_ids[64], s_w[64];
   const int b = blockIdx.x, lane = threadIdx.x;
+  if (Lp_dev) {  // device-side length (graph-captured decode loops): L_prev from memory, L = L_prev + n_new
+    const int n_new = L - L_prev;
+    L_prev = *Lp_dev;
+    L = L_prev + n_new;
+    if (L_prev < 1 || L > S) {  // a decode step needs a planned prefix and room for the new tokens
+      if (lane == 0) {
+        int32_t* w0 = ws + (size_t)b * kAppendWs;
+        w0[0] = -1;
+        w0[1] = w0[2] = 0;
+        raise_err(err, kErrPlanMismatch);
+      }
+      return;
+    }
+  }
   for (int j = lane; j < n_ids; j += 32) {
     s_ids[j] = delim_ids[j];
     s_w[j] = w10[(size_t)b * n_ids + j];
@@ -194,8 +209,10 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
                                                    const int32_t* __restrict__ block_starts,
                                                    const int32_t* __restrict__ n_blocks,
                                                    const int32_t* __restrict__ page_first,
-                                                   const int32_t* __restrict__ ws, int mean_mode) {
+                                                   const int32_t* __restrict__ ws, int mean_mode,
+                                                   const int32_t* __restrict__ Lp_dev) {
   constexpr int LE = kD / 32;  // elements per lane
+  if (Lp_dev) L_prev = *Lp_dev;  // device-side length (k_plan_append validated it)
   extern __shared__ __align__(16) unsigned char smem[];
   T* sK = reinterpret_cast<T*>(smem);  // [max_tail][kD]
   T* sV = sK + (size_t)max_tail * kD;
@@ -309,10 +326,10 @@ cudaError_t launch_plan_append(const int32_t* tokens, const int32_t* delim_ids, 
                                int B, int S, int maxb, int maxp, int C, int delta, int lam_num, int lam_den,
                                int P, int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
                                int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                               int32_t* n_pages, int32_t* ws, int* err, cudaStream_t st) {
+                               int32_t* n_pages, int32_t* ws, int* err, cudaStream_t st, const int32_t* Lp_dev) {
   k_plan_append<<<B, 32, 0, st>>>(tokens, delim_ids, n_ids, w10, S, maxb, maxp, C, delta, lam_num, lam_den, P,
                                    L_prev, L, block_starts, n_blocks, page_first, page_block, page_valid,
-                                   n_pages, ws, err);
+                                   n_pages, ws, err, Lp_dev);
   cudaError_t e = post_launch(__func__, st);
   if (e != cudaSuccess || L_prev > 0) return e;
   return launch_map_pages(block_starts, n_blocks, B, maxb, maxp, P, L, page_first, page_block, page_valid,
@@ -323,7 +340,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
-                             int mean_mode, cudaStream_t st) {
+                             int mean_mode, cudaStream_t st, const int32_t* Lp_dev) {
   if (n_layers < 1 || n_layers > kAppendMaxLayers) return cudaErrorInvalidValue;
   AppendLayers lays = {};
   for (int l = 0; l < n_layers; ++l) {
@@ -339,11 +356,11 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
   if (dtype == 0) {
     allow_max_dyn_smem(k_kv_append<bf16>);
     k_kv_append<bf16><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
-                                               block_starts, n_blocks, page_first, ws, mean_mode);
+                                               block_starts, n_blocks, page_first, ws, mean_mode, Lp_dev);
   } else {
     allow_max_dyn_smem(k_kv_append<float>);
     k_kv_append<float><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
-                                                block_starts, n_blocks, page_first, ws, mean_mode);
+                                                block_starts, n_blocks, page_first, ws, mean_mode, Lp_dev);
   }
   return post_launch(__func__, st);
 }

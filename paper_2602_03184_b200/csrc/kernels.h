@@ -123,12 +123,13 @@ cudaError_t launch_plan_append(const int32_t* tokens, const int32_t* delim_ids, 
                                int B, int S, int maxb, int maxp, int C, int delta, int lam_num, int lam_den,
                                int P, int L_prev, int L, int32_t* block_starts, int32_t* n_blocks,
                                int32_t* page_first, int32_t* page_block, int16_t* page_valid,
-                               int32_t* n_pages, int32_t* ws, int* err, cudaStream_t st);
+                               int32_t* n_pages, int32_t* ws, int* err, cudaStream_t st,
+                               const int32_t* Lp_dev = nullptr);  // Lp_dev: device-side L_prev (decode loops)
 cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, const void* const* V_new,
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
-                             int mean_mode, cudaStream_t st);
+                             int mean_mode, cudaStream_t st, const int32_t* Lp_dev = nullptr);
 
 // prefill scoring (score_kernels.cu)
 size_t score_ws_bytes(int Ls, int B, int S, int Hq);

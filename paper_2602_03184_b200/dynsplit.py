@@ -89,6 +89,8 @@ SIGNATURES = {
     "dynsplit_append_kv": (_I, [_PS, _PC, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dynsplit_append_kv_layers": (_I, [_PS, _PC, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dynsplit_merge_partials": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
+    "dynsplit_append_plan_dev": (_I, [_PS, _PC, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_append_kv_layers_dev": (_I, [_PS, _PC, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
     "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
                                        ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
@@ -419,6 +421,28 @@ def append_kv_layers(layers, K_new, V_new, L_prev: int, L: int, ws) -> None:
         _ptr(lay.block_starts), _ptr(lay.n_blocks), _ptr(lay.page_first), _ptr(ws),
         arr([x.Kp for x in layers]), arr([x.Vp for x in layers]), arr([x.digests for x in layers]),
         _stream()), "append_kv_layers")
+
+
+def append_plan_dev(tokens, delim_ids, layer: PagedLayer, L_prev_dev, n_new: int, ws) -> None:
+    """dynsplit_append_plan_dev: as append_plan with L_prev read from the
+    device int32 tensor L_prev_dev (graph-capturable decode loops)."""
+    _check(lib().dynsplit_append_plan_dev(
+        ctypes.byref(layer.shape), ctypes.byref(layer.cfg), _ptr(L_prev_dev), n_new, _ptr(tokens), _ptr(delim_ids),
+        delim_ids.numel(), _ptr(layer.w10), _ptr(layer.block_starts), _ptr(layer.n_blocks),
+        _ptr(layer.page_first), _ptr(layer.page_block), _ptr(layer.page_valid), _ptr(layer.n_pages),
+        _ptr(ws), ws.numel(), _stream()), "append_plan_dev")
+
+
+def append_kv_layers_dev(layers, K_new, V_new, L_prev_dev, n_new: int, ws) -> None:
+    """dynsplit_append_kv_layers_dev: as append_kv_layers with L_prev on the device."""
+    n = len(layers)
+    arr = lambda xs: (ctypes.c_void_p * n)(*[ctypes.c_void_p(x.data_ptr()) for x in xs])
+    lay = layers[0]
+    _check(lib().dynsplit_append_kv_layers_dev(
+        ctypes.byref(lay.shape), ctypes.byref(lay.cfg), _ptr(L_prev_dev), n_new, n, arr(K_new), arr(V_new),
+        _ptr(lay.block_starts), _ptr(lay.n_blocks), _ptr(lay.page_first), _ptr(ws),
+        arr([x.Kp for x in layers]), arr([x.Vp for x in layers]), arr([x.digests for x in layers]),
+        _stream()), "append_kv_layers_dev")
 
 
 @dataclass
