@@ -744,7 +744,7 @@ dynsplit_status dynsplit_append_kv_layers(const dynsplit_shape* s, const dynspli
       s->kv_dtype, n_layers, K_new, V_new, L - L_prev, s->B, s->Hkv, dynsplit_max_blocks(s->S, c),
       dynsplit_max_pages(s->S, c), c->page_size, L_prev, c->C + c->delta, block_starts, n_blocks, page_first,
       reinterpret_cast<const int32_t*>(static_cast<const char*>(ws) + kWsHdr), Kp, Vp, digests, c->digest_mode,
-      st)));
+      st, nullptr, err_word(const_cast<void*>(ws)))));
   return cuda_status(launch_fence(st));
 }
 
@@ -795,7 +795,7 @@ dynsplit_status dynsplit_append_kv_layers_dev(const dynsplit_shape* s, const dyn
       s->kv_dtype, n_layers, K_new, V_new, n_new, s->B, s->Hkv, dynsplit_max_blocks(s->S, c),
       dynsplit_max_pages(s->S, c), c->page_size, 1, c->C + c->delta, block_starts, n_blocks, page_first,
       reinterpret_cast<const int32_t*>(static_cast<const char*>(ws) + kWsHdr), Kp, Vp, digests, c->digest_mode,
-      st, L_prev_dev)));
+      st, L_prev_dev, err_word(const_cast<void*>(ws)))));
   return cuda_status(launch_fence(st));
 }
 

@@ -34,7 +34,7 @@ struct AppendLayers {
   void* vp[kAppendMaxLayers];
   void* dg[kAppendMaxLayers];
 };
-constexpr int kAppendWs = 4 + kAppendMaxTail;  // int32 per sequence: f, start_f, n_old, pad, loc[]
+constexpr int kAppendWs = 4 + kAppendMaxTail;  // int32 per sequence: f, start_f, n_old, L, loc[]
 
 __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ tokens,
                                                     const int32_t* __restrict__ delim_ids, int n_ids,
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
         int32_t* w0 = ws + (size_t)b * kAppendWs;
         w0[0] = -1;
         w0[1] = w0[2] = 0;
+        w0[3] = -1;
         raise_err(err, kErrPlanMismatch);
       }
       return;
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
       if (lane == 0) {
         w[0] = -1;
         w[1] = w[2] = 0;
+        w[3] = -1;
         raise_err(err, kErrPlanMismatch);
       }
       return;
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(32) k_plan_append(const int32_t* __restrict__ 
     w[0] = f;
     w[1] = s0;
     w[2] = n_old;
+    w[3] = L;  // the planned length k_kv_append must be called for
   }
   __syncwarp();
 
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
                                                    const int32_t* __restrict__ n_blocks,
                                                    const int32_t* __restrict__ page_first,
                                                    const int32_t* __restrict__ ws, int mean_mode,
-                                                   const int32_t* __restrict__ Lp_dev) {
+                                                   const int32_t* __restrict__ Lp_dev, int* __restrict__ err) {
   constexpr int LE = kD / 32;  // elements per lane
   if (Lp_dev) L_prev = *Lp_dev;  // device-side length (k_plan_append validated it)
   extern __shared__ __align__(16) unsigned char smem[];
@@ -226,6 +229,12 @@ __global__ void __launch_bounds__(256) k_kv_append(AppendLayers lays, int n_new,
   const int32_t* w = ws + (size_t)b * kAppendWs;
   const int f = w[0], s0 = w[1], n_old = w[2];
   if (f < 0) return;  // k_plan_append flagged this sequence (plan mismatch / capacity)
+  // the workspace must describe this append (the plan was advanced to
+  // L_prev + n_new by k_plan_append); a stale one is a caller error
+  if (w[3] != L_prev + n_new || s0 < 0 || n_old != L_prev - s0 || n_old > max_tail) {
+    if (threadIdx.x == 0) raise_err(err, kErrPlanMismatch);
+    return;
+  }
   const int32_t* bs = block_starts + (size_t)b * (maxb + 1);
   const int32_t* pf = page_first + (size_t)b * (maxb + 1);
   const size_t page_base = ((size_t)b * Hkv + hk) * maxp;
@@ -340,7 +349,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
-                             int mean_mode, cudaStream_t st, const int32_t* Lp_dev) {
+                             int mean_mode, cudaStream_t st, const int32_t* Lp_dev, int* err) {
   if (n_layers < 1 || n_layers > kAppendMaxLayers) return cudaErrorInvalidValue;
   AppendLayers lays = {};
   for (int l = 0; l < n_layers; ++l) {
@@ -356,11 +365,11 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
   if (dtype == 0) {
     allow_max_dyn_smem(k_kv_append<bf16>);
     k_kv_append<bf16><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
-                                               block_starts, n_blocks, page_first, ws, mean_mode, Lp_dev);
+                                               block_starts, n_blocks, page_first, ws, mean_mode, Lp_dev, err);
   } else {
     allow_max_dyn_smem(k_kv_append<float>);
     k_kv_append<float><<<grid, 256, smem, st>>>(lays, n_new, Hkv, maxb, maxp, P, L_prev, max_tail,
-                                                block_starts, n_blocks, page_first, ws, mean_mode, Lp_dev);
+                                                block_starts, n_blocks, page_first, ws, mean_mode, Lp_dev, err);
   }
   return post_launch(__func__, st);
 }

@@ -612,6 +612,10 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   }
   int32_t* sbs = sbs_st + skip_bs;
   int32_t* spf = spf_st + skip_pf;
+  // the barriers' initialisation must be visible before any thread polls one:
+  // a stale word left in this smem by an earlier kernel can otherwise read as
+  // a completed phase (the plan is then read before it lands)
+  __syncthreads();
   mbar_wait(&bar_plan, 0);
   // entries past the bulk copies (the last row near the array end): direct loads
   for (int i = (int)(bs_bytes >> 2) - skip_bs + tid; i <= nb; i += kFNT) sbs[i] = bs_row[i];

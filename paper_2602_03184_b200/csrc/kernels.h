@@ -129,7 +129,7 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
                              int n_new, int B, int Hkv, int maxb, int maxp, int P, int L_prev, int max_tail,
                              const int32_t* block_starts, const int32_t* n_blocks, const int32_t* page_first,
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
-                             int mean_mode, cudaStream_t st, const int32_t* Lp_dev = nullptr);
+                             int mean_mode, cudaStream_t st, const int32_t* Lp_dev, int* err);
 
 // prefill scoring (score_kernels.cu)
 size_t score_ws_bytes(int Ls, int B, int S, int Hq);

@@ -151,3 +151,41 @@ class RandomLlama:
         logits = torch.nn.functional.rms_norm(x, (sh.d_model,), self.nf, sh.eps) @ self.emb.t()
         self.pos.add_(1)
         return logits.argmax(dim=-1).to(torch.int32)
+
+
+def time_decode(model: RandomLlama, first_tok: torch.Tensor, checkpoints, warmup: int = 3):
+    """Generate tokens with one decode step captured as a CUDA graph (the
+    step's argmax feeds the next replay on the device) and return, for every
+    checkpoint n in `checkpoints` (ascending), the mean ms per token of the
+    tokens generated up to n (CUDA events).  The first `warmup` steps run
+    eagerly (kernel attributes, cuBLAS heuristics) and count as generated."""
+    dev = first_tok.device
+    tok = first_tok.clone()
+    for _ in range(warmup):
+        tok = model.step(tok)
+    tok_in = tok.clone()
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        out = model.step(tok_in)
+        tok_in.copy_(out)
+    cur = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(checkpoints) + 1)]
+    ev[0].record(cur)
+    done = warmup
+    res = {}
+    for i, n in enumerate(checkpoints):
+        while done < n:
+            g.replay()
+            done += 1
+        ev[i + 1].record(cur)
+    torch.cuda.synchronize()
+    prev = warmup
+    tot = 0.0
+    for i, n in enumerate(checkpoints):
+        tot += ev[i].elapsed_time(ev[i + 1])
+        res[n] = tot / max(n - warmup, 1)
+    del g
+    return res

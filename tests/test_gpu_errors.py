@@ -249,3 +249,40 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=ROOT)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+def test_append_kv_without_plan_append(D):
+    """append_kv for [L, L + 1) without the matching append_plan: the
+    workspace still describes the previous append, so the kernel reports a
+    PlanMismatch and writes nothing (the staged tail would not match)."""
+    cfg = D.default_config()
+    B, Hq, Hkv, S_cap = 1, 4, 2, 800
+    toks = G.tokens(8, S_cap)
+    w10 = t(G.T7_W10[None], torch.uint8)
+    lay = D.alloc_paged(B, S_cap, Hq, Hkv, cfg, w10, torch.bfloat16, DEV)
+    ws = D.append_workspace(lay)
+    _, K, V = G.decode_qkv(8, S_cap, Hq, Hkv)
+    Kd, Vd = t(K[None], torch.bfloat16), t(V[None], torch.bfloat16)
+    D.append_plan(t(toks[None]), t(G.T7_IDS), lay, 0, 500, ws)
+    D.append_kv(lay, Kd[:, :500].contiguous(), Vd[:, :500].contiguous(), 0, 500, ws)
+    assert D.read_device_error(ws) == 0
+    kp, vp, dg = lay.Kp.clone(), lay.Vp.clone(), lay.digests.clone()
+    D.append_kv(lay, Kd[:, 500:501].contiguous(), Vd[:, 500:501].contiguous(), 500, 501, ws)
+    assert D.read_device_error(ws) & D.DEVERR_PLAN_MISMATCH
+    assert torch.equal(lay.Kp, kp) and torch.equal(lay.Vp, vp) and torch.equal(lay.digests, dg)
+
+
+def test_fused_synccheck_subprocess():
+    """compute-sanitizer synccheck + memcheck over the decode-model flow
+    (append kernels, then the fused layer reusing their shared memory): every
+    mbarrier is initialised before any thread polls it (a stale word once read
+    as a completed phase) and no access is out of bounds."""
+    import shutil
+    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not available")
+    for tool in ("synccheck", "memcheck"):
+        r = subprocess.run([san, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                            os.path.join(ROOT, "tests", "_san_append_decode.py")],
+                           capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0 and "ok" in r.stdout, (tool, r.stdout[-3000:], r.stderr[-3000:])
