@@ -70,11 +70,15 @@ constexpr int kFMaxGroups = 1024;    // (b, KV head) groups x NS bound of the mo
 constexpr int kBandCap = 256;        // band entries resolved by one warp (8 per lane)
 constexpr int kSlot = 64;            // band entries one CTA publishes per head
 constexpr int kSub = 16;             // sub-bands of [t_lo, t_hi] (per-range token weights)
+constexpr int kH = 256;              // bins of a head's score histogram (the fallback of R25)
 
 // Optional phase timestamps (debug builds; dynsplit_debug_fused_timer): the
 // buffer pointer is read once per kernel into dbgp (a global load per stamp
 // would add its latency to every phase).
 __device__ unsigned long long* g_fused_dbg = nullptr;
+// test switch (dynsplit_debug_fused_force): 1 = every head takes the
+// histogram fallback, 2 = every head takes the CTA-wide slow path
+__device__ int g_fused_force = 0;
 #ifdef DSK_DEBUG
 #define fstamp(k)                                                                                    \
   do {                                                                                               \
@@ -83,14 +87,38 @@ __device__ unsigned long long* g_fused_dbg = nullptr;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                         \
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_));                                             \
       const size_t cta_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;    \
-      dbgp[cta_ * 32 + (k)] = t_;                                                                    \
-      dbgp[cta_ * 32 + 16 + (k)] = c_;                                                               \
+      dbgp[cta_ * 64 + (k)] = t_;                                                                    \
+      dbgp[cta_ * 64 + 16 + (k)] = c_;                                                               \
+    }                                                                                                \
+  } while (0)
+// a %globaltimer stamp into debug slot 56 + k (thread 0 or lane 0 of a warp: any thread)
+#define fstampx(k)                                                                                   \
+  do {                                                                                               \
+    if (dbgp) {                                                                                      \
+      unsigned long long t_;                                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                         \
+      const size_t cta_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;    \
+      dbgp[cta_ * 64 + 56 + (k)] = t_;                                                               \
+    }                                                                                                \
+  } while (0)
+// a value into debug slot 32 + k of this CTA (any thread)
+#define fdbg(k, v)                                                                                   \
+  do {                                                                                               \
+    if (dbgp) {                                                                                      \
+      const size_t cta_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;    \
+      dbgp[cta_ * 64 + 32 + (k)] = (unsigned long long)(v);                                          \
     }                                                                                                \
   } while (0)
 #define FSTAMP_INIT unsigned long long* const dbgp = g_fused_dbg
 #else
 #define fstamp(k) \
   do {            \
+  } while (0)
+#define fdbg(k, v) \
+  do {             \
+  } while (0)
+#define fstampx(k) \
+  do {             \
   } while (0)
 #define FSTAMP_INIT
 #endif
@@ -341,6 +369,7 @@ struct SelScratch2 {  // static shared memory of the band selection
   int bcnt[G];
   int wsub[G * kSub];
   int4 sel[G];  // marginal, keep, threshold key, flags (1 = all fit, 2 = slow path)
+  float gmn[G], kb[G];  // bin map of the fallback: bin(x) = min(floor((x - gmn) kb), kH - 1)
 };
 
 // One warp: the marginal block of a head inside its band (c <= kBandCap
@@ -357,9 +386,13 @@ struct SelScratch2 {  // static shared memory of the band selection
 // entries are taken in block order.  Returns the marginal block m, its kept
 // tokens and its key T, and sets the selection bits of the band's selected
 // blocks (bits: the head's words).
-DSK_DEVICE void f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, int need, uint32_t* bits, int& m,
-                              int& keep, uint32_t& T) {
+// Returns (m, keep, T).  (Inlined: a noinline copy measured 0.6 us slower per
+// layer.)
+DSK_DEVICE int4 f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, int need,
+                                           uint32_t* bits) {
   const int lane = threadIdx.x & 31;
+  int m, keep;
+  uint32_t T;
   constexpr int J = kBandCap / 32;
   uint32_t k[J], sbr[J];
   int ix[J], ln[J];
@@ -480,7 +513,7 @@ DSK_DEVICE void f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, i
 #pragma unroll
     for (int r = 0; r < J; ++r) sbq[r] = __umulhi(k[r] - lo, scale);
     int wsb = 0;  // lane j < 16: token weight of sub-band j
-#pragma unroll
+#pragma unroll 1
     for (int j2 = 0; j2 < 16; ++j2) {
       int w = 0;
 #pragma unroll
@@ -508,6 +541,7 @@ DSK_DEVICE void f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, i
   for (int r = 0; r < J; ++r)
     if (((valid >> r) & 1u) && (k[r] > T || (k[r] == T && ix[r] <= m)))
       atomicOr(&bits[ix[r] >> 5], 1u << (ix[r] & 31));
+  return make_int4(m, keep, (int)T, 0);
 }
 
 template <int G>
@@ -528,7 +562,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   __shared__ __align__(8) uint64_t barD[2], bar2, bar_plan;
   __shared__ FusedScratch F;
   __shared__ SelScratch2<G> S2;
-  __shared__ float2 red_m[kFNW][8];
+  __shared__ float4 red_m[kFNW][8];
   __shared__ unsigned s_target;
   __shared__ int s_last;
 
@@ -554,6 +588,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   const int nb = min(max(nb_raw, 0), min(maxb, nw32));
   const int nwu = (nb + 31) >> 5;  // selection words in use
   FSTAMP_INIT;
+  const int force = g_fused_force;
   fstamp(0);
 
   // ---- prologue (resident inputs; overlaps the preceding kernel under PDL):
@@ -708,6 +743,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       }
     }
     float s1 = 0.f, s2 = 0.f;  // this lane's sum / sum of squares of head g's scores
+    float mn = CUDART_INF_F, mx = -CUDART_INF_F;  // and their range
     float* srow_g = scores + ((size_t)b * Hq + hk * G + g) * sstride + lo;
     const int lr = lane & 7, lc = lane >> 3;
     const uint32_t sbase_u = smem_u32(smA);
@@ -748,12 +784,16 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
             ssl[g * per_cap + i0] = c[0];
             s1 += c[0];
             s2 = fmaf(c[0], c[0], s2);
+            mn = fminf(mn, c[0]);
+            mx = fmaxf(mx, c[0]);
           }
           if (i0 + 1 < n) {
             srow_g[i0 + 1] = c[1];
             ssl[g * per_cap + i0 + 1] = c[1];
             s1 += c[1];
             s2 = fmaf(c[1], c[1], s2);
+            mn = fminf(mn, c[1]);
+            mx = fmaxf(mx, c[1]);
           }
         }
       }
@@ -766,20 +806,26 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       }
     }
     // the range's moments per head (fixed order: lanes, then warps)
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
-    if (t == 0 && g < G) red_m[warp][g] = make_float2(s1, s2);
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (t == 0 && g < G) red_m[warp][g] = make_float4(s1, s2, mn, mx);
   }
   __syncthreads();
   if (tid < G) {
-    float a = 0.f, c2 = 0.f;
+    float a = 0.f, c2 = 0.f, mn = CUDART_INF_F, mx = -CUDART_INF_F;
     for (int w = 0; w < kFNW; ++w) {
-      a += red_m[w][tid].x;
-      c2 += red_m[w][tid].y;
+      const float4 r = red_m[w][tid];
+      a += r.x;
+      c2 += r.y;
+      mn = fminf(mn, r.z);
+      mx = fmaxf(mx, r.w);
     }
-    mom[((size_t)bh * NS + split) * G + tid] = make_float4((float)n, a, c2, 0.f);
+    mom[((size_t)bh * NS + split) * G + tid] = make_float4(a, c2, mn, mx);
   }
   __syncthreads();  // every score and moment write of the CTA precedes the arrive
   fstamp(3);
@@ -805,17 +851,24 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   // published weights verify it
   if (warp < G) {
     const int g2 = warp;
-    float cn = 0.f, c1 = 0.f, c2 = 0.f;
+    float c1 = 0.f, c2 = 0.f, gmn = CUDART_INF_F, gmx = -CUDART_INF_F;
     for (int r = lane; r < NS; r += 32) {
       const float4 mm = __ldcg(mom + ((size_t)bh * NS + r) * G + g2);
-      cn += mm.x;
-      c1 += mm.y;
-      c2 += mm.z;
+      c1 += mm.x;
+      c2 += mm.y;
+      gmn = fminf(gmn, mm.z);
+      gmx = fmaxf(gmx, mm.w);
     }
-    cn = warp_sum(cn);
     c1 = warp_sum(c1);
     c2 = warp_sum(c2);
+    gmn = -warp_max(-gmn);
+    gmx = warp_max(gmx);
     if (lane == 0) {
+      const float cn = (float)nb;
+      float kb = (float)kH / (gmx - gmn);  // the fallback's bin map over [gmin, gmax]
+      if (!(kb < 3.0e38f)) kb = 0.f;       // equal scores (or an overflowing span): one bin
+      S2.gmn[g2] = gmn;
+      S2.kb[g2] = kb;
       float tl = -CUDART_INF_F, th = CUDART_INF_F;
       const float pb = (float)budget / (float)max(total, 1);
       if (cn > 1.f && pb < 0.25f) {
@@ -959,17 +1012,158 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     uint32_t T = 0;
     if (total <= budget) {
       all = 1;
-    } else if (W_hi >= budget || W_hi + W_bd < budget || over || nband > kBandCap) {
+    } else if (W_hi >= budget || W_hi + W_bd < budget || over || nband > kBandCap || force) {
       fb = 1;  // the bounds did not bracket the marginal block: exact slow path below
     } else {
-      f_band_select(sband + (size_t)g2 * kBandCap, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords, m,
-                    keep, T);
+      const int4 r = f_band_select(sband + (size_t)g2 * kBandCap, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
+      m = r.x;
+      keep = r.y;
+      T = (uint32_t)r.z;
     }
     if (budget_mode && m >= 0) keep = blen(sbs, m);  // whole blocks (R24): the marginal block whole
     if (lane == 0) S2.sel[g2] = make_int4(m, keep, (int)T, all | (fb << 1));
+    if (lane == 0 && g2 < 4) {
+      fdbg(4 * g2 + 0, nband);
+      fdbg(4 * g2 + 1, over);
+      fdbg(4 * g2 + 2, W_hi);
+      fdbg(4 * g2 + 3, W_bd);
+    }
   }
   __syncthreads();
   fstamp(7);
+  // fallback for a head whose Gaussian bounds did not bracket its marginal
+  // block (a skewed score distribution, R25): its warp reads every score of
+  // the head (all written before barrier A) and selects exactly on its own --
+  // the same data and arithmetic in every CTA of the group, so the same
+  // result, with no further barrier.  A kH-bin token-weight histogram over
+  // [gmin, gmax] (a monotone bin map) gives the crossing bin j*, the highest
+  // bin whose suffix weight reaches the budget: bins above j* are selected
+  // (W_hi < budget by construction) and the blocks of bin j* are ranked by
+  // f_band_select (sub-band = the fraction of the bin x 16, also monotone).
+  // A crossing bin of more than kBandCap blocks (massive ties) leaves the
+  // head to the CTA-wide slow path below.
+  uint32_t fbm = 0;  // heads to the fallback (the same in every CTA of the group)
+#pragma unroll
+  for (int g2 = 0; g2 < G; ++g2) fbm |= (uint32_t)((S2.sel[g2].w >> 1) & 1) << g2;
+  if (force & 2) fbm = 0;
+  if (fbm) {
+    // the heads' scores are copied into the free tail of region A (past the
+    // selection scratch), as many heads per round as fit
+    const int nb4 = (nb + 3) & ~3;
+    const size_t sel_b = ((size_t)kFBkt * 4 + (size_t)G * kBandCap * 8 + (size_t)G * nwords * 4 + 15) & ~(size_t)15;
+    float* sx = reinterpret_cast<float*>(smA + sel_b);
+    const int hpp = max(1, (int)((region_a - sel_b) / ((size_t)nb4 * 4)));
+    uint32_t ph = 0;
+#pragma unroll 1
+    for (int h0 = 0; h0 < G; h0 += hpp) {
+      const int hn = min(hpp, G - h0);
+      const uint32_t cm = fbm & (((1u << hn) - 1u) << h0);
+      if (!cm) continue;
+      if (tid == 0) {  // one bulk copy (TMA) per head row, completion on bar2
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the space
+        mbar_arrive_expect_tx(&bar2, (uint32_t)(__popc(cm) * nb4 * 4));
+        for (int k = h0; k < h0 + hn; ++k)
+          if ((cm >> k) & 1u)
+            bulk_g2s(sx + (size_t)(k - h0) * nb4, scores + ((size_t)b * Hq + hk * G + k) * sstride,
+                     (uint32_t)(nb4 * 4), &bar2, policy_evict_last());
+      }
+      mbar_wait(&bar2, ph);
+      ph ^= 1u;
+      if (tid == 0) fstampx(0);
+      if (warp < G && ((cm >> warp) & 1u)) {
+        const int g2 = warp;
+        const float* xs = sx + (size_t)(g2 - h0) * nb4;
+        const float gmn = S2.gmn[g2], kb = S2.kb[g2];
+        uint2* lst = sband + (size_t)g2 * kBandCap;
+        uint32_t* h = reinterpret_cast<uint32_t*>(lst);  // [kH] histogram, then the band list (kBandCap x 8 B >= kH x 4 B)
+        for (int j = lane; j < kH; j += 32) h[j] = 0u;
+        if (lane < kSub) S2.wsub[g2 * kSub + lane] = 0;
+        __syncwarp();
+        for (int i0 = 0; i0 < nb; i0 += 8 * 32) {  // 8 elements per lane in flight
+          float x8[8];
+          int l8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * 32 + lane;
+            x8[u] = i < nb ? xs[i] : 0.f;
+            l8[u] = i < nb ? blen(sbs, i) : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (l8[u]) atomicAdd(&h[min((int)((x8[u] - gmn) * kb), kH - 1)], (uint32_t)l8[u]);
+        }
+        __syncwarp();
+        if (lane == 0 && g2 == 0) fstampx(1);
+        int hv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hv[k] = (int)h[8 * lane + k];
+        int suf = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) suf += hv[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // suffix weight of bins >= 8 lane
+          const int t2 = __shfl_down_sync(0xffffffffu, suf, o);
+          if (lane + o < 32) suf += t2;
+        }
+        int kst = -1, cur = suf, wabove = 0;  // the lane's highest bin whose suffix reaches the budget
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (cur >= budget) {
+            kst = k;
+            wabove = cur - hv[k];
+          }
+          cur -= hv[k];
+        }
+        const uint32_t anyb = __ballot_sync(0xffffffffu, kst >= 0);  // total > budget: never empty
+        const int ls = 31 - __clz(anyb);
+        const int js = 8 * ls + __shfl_sync(0xffffffffu, kst, ls);
+        const int W_hi = __shfl_sync(0xffffffffu, wabove, ls);
+        __syncwarp();  // the histogram is read: its space takes the band list
+        const uint32_t lt = (1u << lane) - 1u;
+        int nband = 0;
+        for (int w0 = 0; w0 < nwu; w0 += 4) {  // 4 words per step, loads first
+          float x4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = (w0 + u) * 32 + lane;
+            x4[u] = i < nb ? xs[i] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = (w0 + u) * 32 + lane;
+            const float tb = (x4[u] - gmn) * kb;
+            const int bn = i < nb ? min((int)tb, kH - 1) : -1;
+            const uint32_t ab = __ballot_sync(0xffffffffu, bn > js);
+            const uint32_t bb = __ballot_sync(0xffffffffu, bn == js);
+            if (lane == 0 && w0 + u < nwu) sbits[g2 * nwords + w0 + u] = ab;
+            if (bn == js) {
+              const int pos = nband + __popc(bb & lt);
+              const int sb = min((int)((tb - (float)bn) * (float)kSub), kSub - 1);
+              atomicAdd(&S2.wsub[g2 * kSub + sb], blen(sbs, i));
+              if (pos < kBandCap) lst[pos] = make_uint2(float_key(x4[u]), (uint32_t)i | ((uint32_t)sb << 24));
+            }
+            nband += __popc(bb);
+          }
+        }
+        __syncwarp();
+        if (lane == 0 && g2 == 0) fstampx(2);
+        if (lane == 0 && g2 < 4) fdbg(16 + g2, 1 + nband);
+        if (nband <= kBandCap) {
+          const int wsb = lane < kSub ? S2.wsub[g2 * kSub + lane] : 0;
+          int m = -1, keep = 0;
+          uint32_t T = 0;
+          const int4 r = f_band_select(lst, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
+          m = r.x;
+          keep = r.y;
+          T = (uint32_t)r.z;
+          if (budget_mode && m >= 0) keep = blen(sbs, m);  // whole blocks (R24)
+          if (lane == 0) S2.sel[g2] = make_int4(m, keep, (int)T, 0);
+        }  // else flag 2 stays: the slow path below
+        if (lane == 0 && g2 == 0) fstampx(3);
+      }
+      __syncthreads();
+    }
+  }
   // slow path for a head whose bounds failed (rare): CTA-wide exact
   // selection over every key, then its selection words from the keys
   bool special = false;
@@ -1161,6 +1355,9 @@ extern "C" long long dynsplit_debug_fused_launches(void) { return dsk::g_fused_l
 extern "C" int dynsplit_debug_fused(int on) {
   dsk::g_fused_off = on == 0;
   return 0;
+}
+extern "C" int dynsplit_debug_fused_force(int mode) {
+  return (int)cudaMemcpyToSymbol(dsk::g_fused_force, &mode, sizeof(int));
 }
 extern "C" int dynsplit_debug_fused_timer(void* dev_ptr) {
   return (int)cudaMemcpyToSymbol(dsk::g_fused_dbg, &dev_ptr, sizeof(void*));

@@ -18,6 +18,8 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libdynsplit_debug.so" if os.environ.get("DYNSPLIT_DEBUG_BUILD")
                         else "libdynsplit.so")
+if os.environ.get("DYNSPLIT_LIB_AB"):  # A/B timing of another in-tree build (tools/); never set by the tests
+    LIB_PATH = os.path.join(_PKG, "lib", os.environ["DYNSPLIT_LIB_AB"])
 
 OK = 0
 BF16, FP32 = 0, 1

@@ -7,7 +7,9 @@ switches between them and dynsplit_debug_fused_launches() proves the fused
 kernel actually ran.  The fused kernel must give bit-identical selections,
 worklists, o and lse (same page assignment, same arithmetic), so every case
 compares with torch.equal, then with the oracle (selection exact, attention
-within DESIGN R17).  Cases cover the band fast path (continuous scores), the
+within DESIGN R17).  Cases cover the band fast path (continuous scores, also
+skewed by outlier tails and at budget / total = 1/3: the local brackets of
+R25 hold for any distribution), the
 exact slow path (integer scores: massive ties; all-zero scores), all-fit
 budgets, budget 1, G = 1 / 2 / 4 / 8, several sequences per launch, a plan
 whose blocks are shorter than any DD-Select plan, and the digest staging in
@@ -114,6 +116,9 @@ def build(D, toks, K, V, Hq, cfg=None):
     (2, 3000, 32, 8, 5000, "cont"),      # budget >= S: everything fits
     (1, 3000, 32, 8, 400, "zero"),       # q = 0: all scores equal (index order)
     (4, 2500, 32, 8, 256, "cont"),       # several sequences, few splits each
+    (1, 20000, 32, 8, 1024, "lowtail"),  # a tail of low-score outlier blocks (skewed distribution)
+    (1, 20000, 32, 8, 1024, "hightail"),  # a tail of high-score blocks, all in the last ranges
+    (1, 12000, 32, 8, 4000, "cont"),     # budget / total = 1/3 (a wide crossing band)
 ])
 def test_fused_equals_three_kernels_and_oracle(D, B, S, Hq, Hkv, budget, kind):
     d = 128
@@ -122,7 +127,11 @@ def test_fused_equals_three_kernels_and_oracle(D, B, S, Hq, Hkv, budget, kind):
     gen = G.decode_qkv_integer if kind == "int" else G.decode_qkv
     qs, Ks, Vs = zip(*[gen(3200 + b, S, Hq, Hkv, d) for b in range(B)])
     q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
-    if kind == "cont":
+    if kind == "lowtail":   # x 1/16 and x 4 keep the keys bf16-exact
+        K[:, S - 1500:] *= 0.0625
+    if kind == "hightail":
+        K[:, S - 600:] *= 4.0
+    if kind in ("cont", "lowtail", "hightail"):
         q = H.certify_queries(3200, q, K, starts, budget, "bf16")
     if kind == "zero":
         q = np.zeros_like(q)
@@ -134,6 +143,44 @@ def test_fused_equals_three_kernels_and_oracle(D, B, S, Hq, Hkv, budget, kind):
     if kind != "zero":
         res = H.oracle_decode(q, K, V, starts, budget)
         check_oracle(a[2], a[0], a[1], res, B, Hq)
+
+
+@pytest.mark.parametrize("force", [1, 2])
+@pytest.mark.parametrize("B,S,Hq,Hkv,budget,kind", [
+    (1, 20000, 32, 8, 1024, "cont"),
+    (1, 8000, 32, 4, 500, "lowtail"),    # G = 8
+    (2, 9000, 16, 8, 700, "hightail"),
+    (1, 6000, 8, 8, 300, "cont"),        # G = 1
+    (1, 5000, 32, 8, 600, "int"),        # ties: the fallback's crossing bin overflows -> slow path
+])
+def test_fused_selection_paths(D, force, B, S, Hq, Hkv, budget, kind):
+    """Every head forced through the histogram fallback (force = 1: the
+    crossing bin of a kH-bin histogram over [gmin, gmax], R25) or through the
+    CTA-wide slow path (force = 2): the same selections, worklists, o and lse
+    as the three-kernel path, and the oracle's."""
+    lib = D.lib()
+    d = 128
+    toks = np.stack([G.tokens(3500 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    gen = G.decode_qkv_integer if kind == "int" else G.decode_qkv
+    qs, Ks, Vs = zip(*[gen(3600 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    if kind == "lowtail":
+        K[:, S - 1500:] *= 0.0625
+    if kind == "hightail":
+        K[:, S - 600:] *= 4.0
+    if kind != "int":
+        q = H.certify_queries(3600, q, K, starts, budget, "bf16")
+    layer = build(D, toks, K, V, Hq)
+    qt = t(q, torch.bfloat16)
+    lib.dynsplit_debug_fused_force(force)
+    try:
+        a, b = run_both(D, qt, layer, budget)
+    finally:
+        lib.dynsplit_debug_fused_force(0)
+    assert_same(D, a, b, D.make_shape(B, S, Hq, Hkv, d), Hq // Hkv)
+    res = H.oracle_decode(q, K, V, starts, budget)
+    check_oracle(a[2], a[0], a[1], res, B, Hq)
 
 
 def test_fused_staging_rounds_and_short_blocks(D):
@@ -244,7 +291,11 @@ def test_fused_variants_against_oracle(D, gqa, whole, kind):
     gen = G.decode_qkv_integer if kind == "int" else G.decode_qkv
     qs, Ks, Vs = zip(*[gen(3700 + b, S, Hq, Hkv, d) for b in range(B)])
     q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
-    if kind == "cont":
+    if kind == "lowtail":   # x 1/16 and x 4 keep the keys bf16-exact
+        K[:, S - 1500:] *= 0.0625
+    if kind == "hightail":
+        K[:, S - 600:] *= 4.0
+    if kind in ("cont", "lowtail", "hightail"):
         q = (H.certify_queries_group(3700, q, K, starts, budget) if gqa
              else H.certify_queries(3700, q, K, starts, budget, "bf16"))
     cfg = D.default_config(gqa_mode=gqa, budget_mode=whole)

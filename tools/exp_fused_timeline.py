@@ -60,13 +60,13 @@ for _ in range(3):
     g.replay()
 torch.cuda.synchronize()
 ncta = 148
-dbg = torch.zeros(ncta * 32, dtype=torch.int64, device=dev)
+dbg = torch.zeros(ncta * 64, dtype=torch.int64, device=dev)
 lib.dynsplit_debug_fused_timer.argtypes = [ctypes.c_void_p]
 lib.dynsplit_debug_fused_timer(ctypes.c_void_p(dbg.data_ptr()))
 g.replay()
 torch.cuda.synchronize()
 lib.dynsplit_debug_fused_timer(ctypes.c_void_p(0))
-tc = dbg.view(ncta, 32).cpu().numpy().astype(np.float64)
+tc = dbg.view(ncta, 64).cpu().numpy().astype(np.float64)
 used = tc[:, 0] > 0
 t = tc[used, :16]
 clk = tc[used, 16:]
