@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the c3_b8 / c4 blocks")
+    ap.add_argument("--no-e2e-model", action="store_true", help="skip the NEXT-4 decoder block")
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -552,6 +553,36 @@ def decode_block(args, torch, D, wl: Workload, L, budget, dev, cur, world, barri
     return res
 
 
+def e2e_model_block(D, G, dev, B=8, S0=32768, outs=(64,), budget=2048):
+    """NEXT-4 (the shape of the paper's Fig. 8): ms per generated
+    token of a random-weight Llama-3-8B-shaped decoder (32 layers, cuBLAS
+    projections) over a 32K synthetic prompt, DynSplit-KV sparse attention
+    (the fused layer) vs dense attention (our a9 kernel); one CUDA graph per
+    decode step (append, 32 layers, argmax).  The full sweep (B = 1 / 8, 256 /
+    1024 / 4096 tokens) is tools/exp_e2e_decode.py."""
+    import numpy as np
+    import torch
+    from paper_2602_03184_b200.model import LlamaShape, RandomLlama, time_decode
+    S_cap = S0 + max(outs) + 8
+    ids = torch.from_numpy(G.T7_IDS).to(dev)
+    res = {}
+    for attn in ("sparse", "dense"):
+        w10 = torch.from_numpy(np.tile(G.T7_W10, (B, 1))).to(torch.uint8)
+        cfg = D.default_config(page_cap=(S_cap // 16) + D.max_blocks(S_cap, D.default_config()) // 2 + 64)
+        m = RandomLlama(LlamaShape(), B, S_cap, budget, dev, seed=1, attn=attn, cfg=cfg, delim_ids=ids, w10=w10)
+        toks = torch.from_numpy(np.stack([G.tokens(9000 + b, S0) for b in range(B)])).to(dev)
+        m.prefill_synthetic(toks, seed=2)
+        res[attn] = time_decode(m, toks[:, -1].contiguous(), list(outs))
+        assert D.read_device_error(m.ws_app) == 0 and D.read_device_error(m.ws_dec) == 0
+        del m
+        torch.cuda.empty_cache()
+    n = max(outs)
+    return {"workload": "NEXT-4: Llama-3-8B-shaped decoder, random bf16 weights, %d sequences, %dK prompt, "
+                        "budget %d" % (B, S0 // 1024, budget),
+            "generated_tokens": n, "ms_per_token_sparse": res["sparse"][n], "ms_per_token_dense": res["dense"][n],
+            "speedup": res["dense"][n] / res["sparse"][n]}
+
+
 def cpu_baseline_leg(args, wl: Workload, budget):
     """The oracle on this host's cores: 1 thread, and all cores (forked
     workers over whole KV groups of heads), on a bounded sample (heads of
@@ -755,6 +786,10 @@ def main():
         extra["c4"] = r4
         del wl4
         torch.cuda.empty_cache()
+
+        if not args.no_e2e_model:
+            extra["e2e_model"] = e2e_model_block(D, G, dev)
+            torch.cuda.empty_cache()
 
     prefill = None
     if rank == 0 and not args.no_prefill:

@@ -39,7 +39,8 @@ __all__ = [
     "page_map", "repack", "unpack", "digests", "block_scores",
     "token_scores", "select_tokens", "selection_from_tokens",
     "select_blocks_direct", "sparse_attention", "dense_attention",
-    "merge_partials", "decode_step",
+    "merge_partials", "decode_step", "plan_reuse", "pages_of_tokens", "group_pages",
+    "offload_decode_loop",
 ]
 
 
@@ -601,3 +602,82 @@ def decode_step(q, K, V, block_starts, budget, scale=None, digest_mode="minmax",
         res["o"][h] = o
         res["lse"][h] = lse
     return res
+
+
+# ---------------------------------------------------------------------------
+# O10 Cross-step KV reuse (Appendix B.2 "KVCache Reuse with V2F", Steps 1-3,
+#     P:756-765; SPEC plan_reuse / decode_loop S:379-397) and its paged,
+#     host-offloaded realisation (NEXT-3; the CPU-GPU deployment, P:465-473,
+#     P:583-592).
+# ---------------------------------------------------------------------------
+def plan_reuse(prev, nxt, truncate=True):
+    """Steps 1-3 over per-head index lists prev[h] (the previous step's
+    selection) and nxt[h] (this step's): per head, reusable = the ascending
+    intersection of prev and next (Step 1, "compute the reusable KV for each
+    head"); with truncate, reuse_len = the minimum over heads of |reusable|
+    ("truncate the reusable KV based on the minimum reusable data volume ...
+    a consistent length of reusable KV caches among all heads") and each
+    head reuses the first reuse_len of its reusable entries in ascending index
+    order (Q24 reading); without it every reusable entry is reused
+    (the paged cache needs no equal lengths, DESIGN R26).  fresh = next minus
+    reused (Step 2, "the truncated excess data ... combined with the new
+    required data"), so reused + fresh = next per head (Step 3).  Returns
+    (reuse_len, reused[h], fresh[h]); reuse_len is None without truncate."""
+    if len(prev) != len(nxt):
+        raise ValueError("ShapeMismatch")              # S:381
+    reusable = [np.intersect1d(np.asarray(p_, np.int64), np.asarray(n_, np.int64))
+                for p_, n_ in zip(prev, nxt)]
+    if truncate:
+        reuse_len = min((len(r) for r in reusable), default=0)
+        reused = [r[:reuse_len] for r in reusable]
+    else:
+        reuse_len = None
+        reused = reusable
+    fresh = [np.setdiff1d(np.asarray(n_, np.int64), u) for n_, u in zip(nxt, reused)]
+    return reuse_len, reused, fresh
+
+
+def pages_of_tokens(tokens, block_starts, P=16):
+    """The pages (O4 ids) holding the given tokens: token t of block b at
+    offset o lives in page page_first[b] + o // P (the repack rule).
+    Ascending, without repeats."""
+    t = np.asarray(tokens, np.int64)
+    if t.size == 0:
+        return np.zeros(0, np.int64)
+    bs = np.asarray(block_starts, np.int64)
+    pf, _, _ = page_map(block_starts, P)
+    blk = np.searchsorted(bs, t, side="right") - 1
+    return np.unique(pf[blk] + (t - bs[blk]) // P)
+
+
+def group_pages(sel_tokens_heads, block_starts, P=16):
+    """The pages a KV head must hold for its query heads' selections: the
+    union of pages_of_tokens over the group (a page is stored and moved once
+    per KV head, Q18)."""
+    parts = [pages_of_tokens(t, block_starts, P) for t in sel_tokens_heads]
+    return np.unique(np.concatenate(parts)) if parts else np.zeros(0, np.int64)
+
+
+def offload_decode_loop(qs, K, V, block_starts, budget, P=16, truncate=True, reuse=True, scale=None):
+    """Decode steps over one layer's fixed cache whose KV lives off the GPU
+    (NEXT-3): each step is decode_step (selection and attention unchanged:
+    reuse only decides what is moved, "outputs are bit-identical"); the
+    KV heads' page sets (group_pages of their query heads' tokens) are planned
+    against the previous step's with plan_reuse (the cache holds exactly the
+    previous step's pages); reuse=False moves every needed page.  Per step:
+    o, lse, pages[hk], reused[hk], fresh[hk], reuse_len."""
+    Hkv = np.asarray(K).shape[1]
+    out = []
+    prev = None
+    for q in qs:
+        r = decode_step(q, K, V, block_starts, budget, scale)
+        g = len(r["tokens"]) // Hkv
+        pages = [group_pages(r["tokens"][hk * g:(hk + 1) * g], block_starts, P) for hk in range(Hkv)]
+        if prev is None or not reuse:
+            reuse_len, reused, fresh = 0, [np.zeros(0, np.int64) for _ in pages], pages
+        else:
+            reuse_len, reused, fresh = plan_reuse(prev, pages, truncate)
+        out.append({"o": r["o"], "lse": r["lse"], "pages": pages, "reused": reused, "fresh": fresh,
+                    "reuse_len": reuse_len, "tokens": r["tokens"]})
+        prev = pages
+    return out

@@ -75,6 +75,8 @@ class RandomLlama:
         inv = 1.0 / (sh.rope_theta ** (torch.arange(0, sh.d, 2, device=dev, dtype=torch.float32) / sh.d))
         ang = torch.arange(S_cap, device=dev, dtype=torch.float32)[:, None] * inv[None]
         self.cos, self.sin = ang.cos(), ang.sin()
+        self.cos2 = torch.cat([self.cos, self.cos], -1)  # [S_cap, d] for the fused rotate-half form
+        self.sin2 = torch.cat([self.sin, self.sin], -1)
         # the paged cache: one plan shared by every layer
         self.cfg = cfg if cfg is not None else D.default_config()
         self.delim_ids = delim_ids
@@ -128,26 +130,29 @@ class RandomLlama:
         # the token joins the sequence; the shared plan grows by one (NEXT-1)
         self.tokens.scatter_(1, self.pos.long().expand(B, 1), tok[:, None])
         D.append_plan_dev(self.tokens, self.delim_ids, self.layers[0], self.pos, 1, self.ws_app)
-        cos = self.cos.index_select(0, self.pos.long())[:, None, :]
-        sin = self.sin.index_select(0, self.pos.long())[:, None, :]
+        cos2 = self.cos2.index_select(0, self.pos.long())[:, None, :]               # [1, 1, d]
+        sin2 = self.sin2.index_select(0, self.pos.long())[:, None, :]
+        hd = sh.d // 2
         x = self.emb.index_select(0, tok.long())                                   # [B, dm] bf16
         for l in range(sh.layers):
             h = torch.nn.functional.rms_norm(x, (sh.d_model,), self.n1[l], sh.eps)
             qkv = h @ self.w_qkv[l]
-            q = self._rope(qkv[:, :nq].float().view(B, sh.Hq, sh.d), cos, sin).to(torch.bfloat16)
-            k = self._rope(qkv[:, nq:nq + nk].float().view(B, sh.Hkv, sh.d), cos, sin).to(torch.bfloat16)
-            v = qkv[:, nq + nk:].reshape(B, sh.Hkv, sh.d)
-            D.append_kv_layers_dev([self.layers[l]], [k.contiguous()[:, None]], [v.contiguous()[:, None]],
-                                   self.pos, 1, self.ws_app)
+            # RoPE of q and k together (rotate-half form, fp32): x cos + [-x2 | x1] sin
+            qk = qkv[:, :nq + nk].float().view(B, sh.Hq + sh.Hkv, sh.d)
+            qk = torch.addcmul(qk * cos2, torch.cat([-qk[..., hd:], qk[..., :hd]], -1), sin2).to(torch.bfloat16)
+            q = qk[:, :sh.Hq].contiguous()
+            k = qk[:, sh.Hq:].unsqueeze(1).contiguous()                            # [B, 1, Hkv, d]
+            v = qkv[:, nq + nk:].view(B, 1, sh.Hkv, sh.d).contiguous()
+            D.append_kv_layers_dev([self.layers[l]], [k], [v], self.pos, 1, self.ws_app)
             if self.attn == "sparse":
-                D.decode_layer(q.contiguous(), self.layers[l], self.budget,
+                D.decode_layer(q, self.layers[l], self.budget,
                                out=(self.ns, self.mg, self.kp, self.wl, self.o, self.lse), ws=self.ws_dec)
             else:
-                D.decode_attn(q.contiguous(), self.layers[l], None, out=(self.o, self.lse), ws=self.ws_dec)
-            x = x + self.o.view(B, nq).to(torch.bfloat16) @ self.w_o[l]
+                D.decode_attn(q, self.layers[l], None, out=(self.o, self.lse), ws=self.ws_dec)
+            x = torch.addmm(x, self.o.view(B, nq).to(torch.bfloat16), self.w_o[l])  # residual add in the GEMM
             h2 = torch.nn.functional.rms_norm(x, (sh.d_model,), self.n2[l], sh.eps)
             gu = h2 @ self.w_gu[l]
-            x = x + (torch.nn.functional.silu(gu[:, :sh.ffn]) * gu[:, sh.ffn:]) @ self.w_down[l]
+            x = torch.addmm(x, torch.nn.functional.silu(gu[:, :sh.ffn]).mul_(gu[:, sh.ffn:]), self.w_down[l])
         logits = torch.nn.functional.rms_norm(x, (sh.d_model,), self.nf, sh.eps) @ self.emb.t()
         self.pos.add_(1)
         return logits.argmax(dim=-1).to(torch.int32)
