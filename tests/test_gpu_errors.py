@@ -285,4 +285,6 @@ def test_fused_synccheck_subprocess():
         r = subprocess.run([san, "--tool", tool, "--error-exitcode", "9", sys.executable,
                             os.path.join(ROOT, "tests", "_san_append_decode.py")],
                            capture_output=True, text=True, timeout=600, cwd=ROOT)
+        if r.returncode != 0 and "closed" in r.stderr and not r.stdout:
+            pytest.skip("compute-sanitizer is closed on this GPU pool: " + r.stderr.strip()[:120])
         assert r.returncode == 0 and "ok" in r.stdout, (tool, r.stdout[-3000:], r.stderr[-3000:])
