@@ -81,7 +81,9 @@ typedef enum {
   DYNSPLIT_OP_DECODE_LAYER = 5,
   DYNSPLIT_OP_APPEND = 6,
   DYNSPLIT_OP_MAP_PAGES = 7,   /* header only (the device error word) */
-  DYNSPLIT_OP_REPACK = 8       /* header only */
+  DYNSPLIT_OP_REPACK = 8,      /* header only */
+  DYNSPLIT_OP_REUSE = 9,       /* NEXT-3 reuse plan */
+  DYNSPLIT_OP_DECODE_OFFLOAD = 10  /* NEXT-3 offloaded decode layer */
 } dynsplit_op;
 
 /* Bits of the device error word (first int32 of every workspace). */
@@ -452,6 +454,79 @@ dynsplit_status dynsplit_decode_step_host_layers(const dynsplit_shape* shape, co
                                                  const void* const* Kp, const void* const* Vp, float scale,
                                                  float* o_host, float* lse_host, void* worklist, void* ws,
                                                  size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * NEXT-3: host-offloaded KV with cross-step reuse.
+ * The paper's CPU-GPU deployment keeps the KV cache in host memory and moves
+ * only the selected KV over PCIe each step (Table 5 P:583-592:
+ * the transfer is > 99 % of the attention time at 128K); "KVCache Reuse with
+ * V2F" (Appendix B.2) keeps what the previous step already moved:
+ *   Step 1  per head, reusable = this step's selection AND the previous
+ *           step's; with truncate, reuse_len = the minimum over the heads and
+ *           each head keeps its first reuse_len reusable entries (ascending,
+ *           reading Q24);
+ *   Step 2  the rest of the selection (including the truncated excess) is
+ *           moved;
+ *   Step 3  reused + moved = the step's KV.
+ * The unit of storage and transfer is the V2F page of a KV head (the union
+ * of its query heads' selections, Q18); "heads" in Step 1 are the KV heads of
+ * one sequence.  The device keeps, per (b, KV head), n_slots page slots
+ * holding exactly the previous step's pages; truncate = 0 reuses every
+ * reusable page (DESIGN R26: a paged cache needs no equal lengths).  Reuse
+ * decides what is moved, never what is computed: o and lse equal
+ * dynsplit_decode_attn over the resident pages bit for bit.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t n_slots;       /* page slots per (b, KV head); 1 <= n_slots <= max_pages */
+  int32_t* slot_page;    /* [B, Hkv, n_slots] in/out: logical page held by each slot, -1 = empty
+                            (initialise to -1); after a plan: exactly this step's pages */
+  void* Kc;              /* [B, Hkv, n_slots, P, d] kv dtype: the device page cache */
+  void* Vc;
+  int32_t* fetch;        /* [B, Hkv, n_slots, 2] out: (page, slot) of each page to move, ascending pages */
+  int32_t* fetch_count;  /* [B, Hkv] out */
+  int32_t* reuse_stats;  /* [B, Hkv, 2] out: (reused pages, fresh pages) | NULL */
+  int32_t* reuse_len;    /* [B] out: min over the KV heads of the reusable pages (truncate), else -1 | NULL */
+  void* worklist_cache;  /* out, dynsplit_worklist_bytes(): the step's worklist with page = cache slot */
+} dynsplit_kv_cache;
+
+/* Slots that always hold one step's pages of a (b, KV head): per query head
+ * at most ceil(budget / P) + max_selected pages, times g, capped at max_pages. */
+int32_t dynsplit_cache_slots(const dynsplit_shape* shape, const dynsplit_config* cfg, int32_t budget);
+
+/* Steps 1 and 3 (reuse plan): from `worklist` (dynsplit_select /
+ * dynsplit_decode_layer output, logical pages) and cache->slot_page, writes
+ * fetch / fetch_count, the new slot_page, reuse_stats, reuse_len and
+ * worklist_cache.  reuse = 0: nothing is reused (every page is moved).
+ * Data errors (DYNSPLIT_DEVERR_PAGE_CAPACITY): more pages than n_slots, a
+ * page outside [0, max_pages).  Workspace: DYNSPLIT_OP_REUSE. */
+dynsplit_status dynsplit_reuse_plan(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                    const void* worklist, int32_t truncate, int32_t reuse,
+                                    const dynsplit_kv_cache* cache, void* ws, size_t ws_bytes, void* stream);
+
+/* Step 2 (move): the valid rows of each fetched page, Kp_host / Vp_host
+ * [B, Hkv, max_pages, P, d] in PINNED host memory (cudaHostAlloc /
+ * torch pin_memory; read by the kernel over PCIe, zero-copy) -> cache slot.
+ * dense = 1: every page p < n_pages[b] -> slot p (the offloaded dense
+ * baseline; needs n_slots == max_pages), fetch lists unused.
+ * Errors: INVALID_ARGUMENT for a host pointer the device cannot map. */
+dynsplit_status dynsplit_fetch_pages(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                     const void* Kp_host, const void* Vp_host, const int16_t* page_valid,
+                                     const int32_t* n_pages, int32_t dense, const dynsplit_kv_cache* cache,
+                                     void* stream);
+
+/* One offloaded decode layer: a5+a6 (dynsplit_select, resident digests and
+ * plan), the reuse plan, the move, a7+a8 over the cache.  Arguments as in
+ * dynsplit_select / dynsplit_reuse_plan / dynsplit_fetch_pages; Kp_host and
+ * Vp_host pinned host memory.  Workspace: DYNSPLIT_OP_DECODE_OFFLOAD. */
+dynsplit_status dynsplit_decode_layer_offload(const dynsplit_shape* shape, const dynsplit_config* cfg,
+                                              int32_t budget, const void* q, const void* digests,
+                                              const int32_t* block_starts, const int32_t* n_blocks,
+                                              const int32_t* page_first, const int16_t* page_valid,
+                                              const void* Kp_host, const void* Vp_host, int32_t truncate,
+                                              int32_t reuse, const dynsplit_kv_cache* cache, float scale,
+                                              int32_t* n_sel, int32_t* marginal_block, int32_t* marginal_keep,
+                                              void* worklist, float* o, float* lse, void* ws, size_t ws_bytes,
+                                              void* stream);
 
 #ifdef __cplusplus
 }

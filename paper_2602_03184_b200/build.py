@@ -21,7 +21,8 @@ BUILD = os.path.join(PKG, "build")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libdynsplit.so")
 SOURCES = ["api.cu", "decode_kernels.cu", "select_kernels.cu", "attn_kernels.cu", "build_kernels.cu",
-           "score_kernels.cu", "append_kernels.cu", "fused_kernels.cu"]
+           "score_kernels.cu", "append_kernels.cu", "fused_kernels.cu",
+           "offload_kernels.cu"]
 HEADERS = ["common.cuh", "kernels.h", "attn_core.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

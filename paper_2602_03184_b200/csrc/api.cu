@@ -238,6 +238,14 @@ size_t layer_ws(const dynsplit_shape* s, const dynsplit_config* c) {
   return kWsHdr + decode_body(s) + select_body(s, c) +
          align_up(fused_scratch_bytes(s->B, s->Hq, dynsplit_max_blocks(s->S, c)));
 }
+// NEXT-3 reuse plan: [reusable counts BH][map BH x max_pages][freelist BH x max_pages]
+size_t reuse_body(const dynsplit_shape* s, const dynsplit_config* c) {
+  const size_t bh = (size_t)s->B * s->Hkv, mp = (size_t)dynsplit_max_pages(s->S, c);
+  return align_up(bh * 4) + 2 * align_up(bh * mp * 4);
+}
+size_t offload_ws(const dynsplit_shape* s, const dynsplit_config* c) {
+  return kWsHdr + decode_body(s) + select_body(s, c) + reuse_body(s, c);
+}
 size_t step_host_extra(const dynsplit_shape* s) {
   return align_up((size_t)s->B * s->Hq * kD * esize(s)) + align_up((size_t)s->B * s->Hq * kD * 4) +
          align_up((size_t)s->B * s->Hq * 4) + 3 * align_up((size_t)s->B * s->Hq * 4);
@@ -310,6 +318,8 @@ size_t dynsplit_workspace_bytes(int32_t op, const dynsplit_shape* s, const dynsp
     case DYNSPLIT_OP_APPEND: return kWsHdr + append_ws_bytes(s->B);
     case DYNSPLIT_OP_MAP_PAGES: return kWsHdr;
     case DYNSPLIT_OP_REPACK: return kWsHdr;
+    case DYNSPLIT_OP_REUSE: return kWsHdr + reuse_body(s, c);
+    case DYNSPLIT_OP_DECODE_OFFLOAD: return offload_ws(s, c);
     default: return 0;
   }
 }
@@ -910,6 +920,126 @@ dynsplit_status dynsplit_decode_step_host_layers(const dynsplit_shape* s, const 
       cudaMemcpyAsync(lse_host, lse_dev, L * rows * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return DYNSPLIT_ERR_CUDA;
   return DYNSPLIT_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ NEXT-3: offloaded KV + reuse
+namespace {
+dynsplit_status check_cache(const dynsplit_shape* s, const dynsplit_config* c, const dynsplit_kv_cache* k,
+                            bool need_plan) {
+  if (!k || !k->Kc || !k->Vc) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (k->n_slots < 1 || k->n_slots > dynsplit_max_pages(s->S, c)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (need_plan && (!k->slot_page || !k->fetch || !k->fetch_count || !k->worklist_cache))
+    return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return DYNSPLIT_OK;
+}
+// the device address of pinned host memory (zero-copy); nullptr if the
+// pointer is not host memory the device can map
+const void* mapped_host(const void* h) {
+  cudaPointerAttributes a;
+  if (!h || cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return a.devicePointer;
+}
+}  // namespace
+
+static dynsplit_status reuse_impl(const dynsplit_shape* s, const dynsplit_config* c, const void* worklist,
+                                  int32_t truncate, int32_t reuse, const dynsplit_kv_cache* k, char* rbody,
+                                  int* err, void* stream) {
+  const size_t bh = (size_t)s->B * s->Hkv, mp = (size_t)dynsplit_max_pages(s->S, c);
+  int32_t* reusable = reinterpret_cast<int32_t*>(rbody);
+  int32_t* map = reinterpret_cast<int32_t*>(rbody + align_up(bh * 4));
+  int32_t* freelist = reinterpret_cast<int32_t*>(rbody + align_up(bh * 4) + align_up(bh * mp * 4));
+  WorklistView v = worklist_view(const_cast<void*>(worklist), s);
+  WorklistView w = worklist_view(k->worklist_cache, s);
+  return cuda_status(launch_reuse_plan(v.hdr, v.count, v.entries, s->B, s->Hkv, (int)mp, k->n_slots, reuse != 0,
+                                       truncate != 0, reusable, map, freelist, k->slot_page, k->fetch,
+                                       k->fetch_count, k->reuse_stats, k->reuse_len, w.hdr, w.count, w.entries,
+                                       err, static_cast<cudaStream_t>(stream)));
+}
+
+static dynsplit_status fetch_impl(const dynsplit_shape* s, const dynsplit_config* c, const void* Kp_host,
+                                  const void* Vp_host, const int16_t* page_valid, const int32_t* n_pages,
+                                  int32_t dense, const dynsplit_kv_cache* k, void* stream) {
+  if (!page_valid || (dense && !n_pages)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (!dense && (!k->fetch || !k->fetch_count)) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  const int mp = dynsplit_max_pages(s->S, c);
+  if (dense && k->n_slots != mp) return DYNSPLIT_ERR_DIMENSION_MISMATCH;
+  const void* kd = mapped_host(Kp_host);
+  const void* vd = mapped_host(Vp_host);
+  if (!kd || !vd) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  return cuda_status(launch_fetch_pages(s->kv_dtype, kd, vd, page_valid, n_pages, k->fetch, k->fetch_count,
+                                        dense != 0, s->B, s->Hkv, mp, k->n_slots, c->page_size, k->Kc, k->Vc,
+                                        static_cast<cudaStream_t>(stream)));
+}
+
+extern "C" {
+
+int32_t dynsplit_cache_slots(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget) {
+  if (check_shape(s) != DYNSPLIT_OK || check_cfg(c) != DYNSPLIT_OK || budget < 1) return 0;
+  const long long per_head =
+      (budget + c->page_size - 1) / c->page_size + (long long)dynsplit_max_selected(budget, s->S, c);
+  const long long v = per_head * (s->Hq / s->Hkv);
+  const long long mp = dynsplit_max_pages(s->S, c);
+  return (int32_t)(v < mp ? v : mp);
+}
+
+dynsplit_status dynsplit_reuse_plan(const dynsplit_shape* s, const dynsplit_config* c, const void* worklist,
+                                    int32_t truncate, int32_t reuse, const dynsplit_kv_cache* cache, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  DSK_TRY(check_cache(s, c, cache, true));
+  if (!worklist || !ws) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < kWsHdr + reuse_body(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  return reuse_impl(s, c, worklist, truncate, reuse, cache, ws_body(ws), err_word(ws), stream);
+}
+
+dynsplit_status dynsplit_fetch_pages(const dynsplit_shape* s, const dynsplit_config* c, const void* Kp_host,
+                                     const void* Vp_host, const int16_t* page_valid, const int32_t* n_pages,
+                                     int32_t dense, const dynsplit_kv_cache* cache, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  DSK_TRY(check_cache(s, c, cache, false));
+  return fetch_impl(s, c, Kp_host, Vp_host, page_valid, n_pages, dense, cache, stream);
+}
+
+dynsplit_status dynsplit_decode_layer_offload(const dynsplit_shape* s, const dynsplit_config* c, int32_t budget,
+                                              const void* q, const void* digests, const int32_t* block_starts,
+                                              const int32_t* n_blocks, const int32_t* page_first,
+                                              const int16_t* page_valid, const void* Kp_host,
+                                              const void* Vp_host, int32_t truncate, int32_t reuse,
+                                              const dynsplit_kv_cache* cache, float scale, int32_t* n_sel,
+                                              int32_t* marginal_block, int32_t* marginal_keep, void* worklist,
+                                              float* o, float* lse, void* ws, size_t ws_bytes, void* stream) {
+  DSK_NVTX;
+  DSK_TRY(check_shape(s));
+  DSK_TRY(check_cfg(c));
+  DSK_TRY(check_cache(s, c, cache, true));
+  if (!q || !digests || !o || !lse || !ws || !worklist) return DYNSPLIT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < offload_ws(s, c)) return DYNSPLIT_ERR_WORKSPACE_TOO_SMALL;
+  char* body = ws_body(ws);
+  char* dec_body = body;  // counters first (shape-independent offset)
+  float* sc = reinterpret_cast<float*>(body + decode_body(s));
+  char* rbody = body + decode_body(s) + select_body(s, c);
+  // a5 + a6 on the resident digests and plan (Step 1 of the decode step)
+  DSK_TRY(dynsplit_score_blocks(s, c, q, digests, n_blocks, sc, stream));
+  DSK_TRY(select_impl(s, c, budget, sc, block_starts, n_blocks, page_first, 0, 0x7fffffff, nullptr, n_sel,
+                      marginal_block, marginal_keep, worklist, err_word(ws), stream));
+  // reuse plan (Appendix B.2 Steps 1 and 3) and the move (Step 2)
+  DSK_TRY(reuse_impl(s, c, worklist, truncate, reuse, cache, rbody, err_word(ws), stream));
+  DSK_TRY(fetch_impl(s, c, Kp_host, Vp_host, page_valid, nullptr, 0, cache, stream));
+  // a7 + a8 over the cache: the slot count is the page stride
+  dynsplit_config cc = *c;
+  cc.page_cap = cache->n_slots;
+  return decode_attn_impl(s, &cc, q, cache->Kc, cache->Vc, nullptr, nullptr, cache->worklist_cache, scale, o, lse,
+                          dec_body, stream);
 }
 
 }  // extern "C"

@@ -131,6 +131,17 @@ cudaError_t launch_kv_append(int dtype, int n_layers, const void* const* K_new, 
                              const int32_t* ws, void* const* Kp, void* const* Vp, void* const* dig,
                              int mean_mode, cudaStream_t st, const int32_t* Lp_dev, int* err);
 
+// NEXT-3 offloaded KV + cross-step reuse (offload_kernels.cu)
+cudaError_t launch_reuse_plan(const int32_t* wl_hdr, const int32_t* wl_count, const WLEntry* wl, int B, int Hkv,
+                              int max_pages, int n_slots, int reuse, int truncate, int32_t* reusable,
+                              int32_t* map, int32_t* freelist, int32_t* slot_page, int32_t* fetch,
+                              int32_t* fetch_count, int32_t* stats, int32_t* reuse_len, int32_t* c_hdr,
+                              int32_t* c_count, WLEntry* c_wl, int* err, cudaStream_t st);
+cudaError_t launch_fetch_pages(int dtype, const void* Kh, const void* Vh, const int16_t* page_valid,
+                               const int32_t* n_pages, const int32_t* fetch, const int32_t* fetch_count,
+                               int dense, int B, int Hkv, int max_pages, int n_slots, int P, void* Kc, void* Vc,
+                               cudaStream_t st);
+
 // prefill scoring (score_kernels.cu)
 size_t score_ws_bytes(int Ls, int B, int S, int Hq);
 cudaError_t launch_score_delimiters(const int32_t* tokens, const int32_t* delim_ids, int n_ids,

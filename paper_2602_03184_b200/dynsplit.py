@@ -24,7 +24,7 @@ if os.environ.get("DYNSPLIT_LIB_AB"):  # A/B timing of another in-tree build (to
 OK = 0
 BF16, FP32 = 0, 1
 (OP_SCORE_DELIMITERS, OP_SEGMENT, OP_BUILD_BLOCKS, OP_SELECT, OP_DECODE_ATTN, OP_DECODE_LAYER,
- OP_APPEND, OP_MAP_PAGES, OP_REPACK) = range(9)
+ OP_APPEND, OP_MAP_PAGES, OP_REPACK, OP_REUSE, OP_DECODE_OFFLOAD) = range(11)
 # device error word bits (include/dynsplit.h DYNSPLIT_DEVERR_*)
 DEVERR_PLAN_COVERAGE, DEVERR_PLAN_MISMATCH, DEVERR_PAGE_CAPACITY = 1, 2, 4
 DEVERR_SELECT_OVERFLOW, DEVERR_BLOCK_TOO_LONG, DEVERR_SYNC_TIMEOUT = 8, 16, 32
@@ -50,6 +50,14 @@ class Config(ctypes.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class KVCache(ctypes.Structure):
+    """dynsplit_kv_cache (include/dynsplit.h, NEXT-3)."""
+    _fields_ = [("n_slots", ctypes.c_int32), ("slot_page", ctypes.c_void_p), ("Kc", ctypes.c_void_p),
+                ("Vc", ctypes.c_void_p), ("fetch", ctypes.c_void_p), ("fetch_count", ctypes.c_void_p),
+                ("reuse_stats", ctypes.c_void_p), ("reuse_len", ctypes.c_void_p),
+                ("worklist_cache", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p
@@ -96,6 +104,12 @@ SIGNATURES = {
     "dynsplit_step_host_workspace_bytes": (_SZ, [_PS, _PC, _I]),
     "dynsplit_decode_step_host": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P,
                                        ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
+    "dynsplit_cache_slots": (_I, [_PS, _PC, _I]),
+    "dynsplit_reuse_plan": (_I, [_PS, _PC, _P, _I, _I, ctypes.POINTER(KVCache), _P, _SZ, _P]),
+    "dynsplit_fetch_pages": (_I, [_PS, _PC, _P, _P, _P, _P, _I, ctypes.POINTER(KVCache), _P]),
+    "dynsplit_decode_layer_offload": (_I, [_PS, _PC, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I,
+                                           ctypes.POINTER(KVCache), ctypes.c_float, _P, _P, _P, _P, _P, _P,
+                                           _P, _SZ, _P]),
     "dynsplit_step_host_layers_workspace_bytes": (_SZ, [_PS, _PC, _I, _I]),
     "dynsplit_decode_step_host_layers": (_I, [_PS, _PC, _I, _I, _P, _P, _P, _P, _P, _P, _P,
                                               ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
@@ -640,3 +654,140 @@ def worklist_rows(worklist: torch.Tensor, shape: Shape, G: int):
     rows = ent[:, :, 8:8 + G].max(axis=2).astype(np.int64)
     streamed = np.array([rows[i, : counts[i]].sum() for i in range(nbh)])
     return counts, streamed
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: host-offloaded KV with cross-step reuse (Appendix B.2, P:756-765;
+# the CPU-GPU deployment)
+# ---------------------------------------------------------------------------
+def cache_slots(shape: Shape, cfg: Config, budget: int) -> int:
+    return lib().dynsplit_cache_slots(ctypes.byref(shape), ctypes.byref(cfg), budget)
+
+
+@dataclass
+class OffloadedLayer:
+    """One layer whose pages live in pinned host memory (Kh, Vh [B, Hkv,
+    max_pages, P, d]) while the plan, page tables and digests stay resident
+    (layer, with Kp = Vp = None), plus the device page cache of n_slots slots
+    per (b, KV head) and its per-step outputs (dynsplit_kv_cache)."""
+    layer: PagedLayer
+    Kh: torch.Tensor
+    Vh: torch.Tensor
+    n_slots: int
+    slot_page: torch.Tensor      # int32 [B, Hkv, n_slots], -1 = empty
+    Kc: torch.Tensor             # [B, Hkv, n_slots, P, d]
+    Vc: torch.Tensor
+    fetch: torch.Tensor          # int32 [B, Hkv, n_slots, 2] (page, slot)
+    fetch_count: torch.Tensor    # int32 [B, Hkv]
+    reuse_stats: torch.Tensor    # int32 [B, Hkv, 2] (reused, fresh)
+    reuse_len: torch.Tensor      # int32 [B]
+    worklist_cache: torch.Tensor  # opaque, page = cache slot
+
+    def c(self) -> KVCache:
+        p = lambda t: ctypes.c_void_p(t.data_ptr())
+        return KVCache(self.n_slots, p(self.slot_page), p(self.Kc), p(self.Vc), p(self.fetch),
+                       p(self.fetch_count), p(self.reuse_stats), p(self.reuse_len), p(self.worklist_cache))
+
+    def reset(self) -> None:
+        """Empty the cache (the next step moves every page)."""
+        self.slot_page.fill_(-1)
+
+
+def offload_layer(layer: PagedLayer, budget: int, Hq: int, n_slots: Optional[int] = None,
+                  keep_device: bool = False) -> OffloadedLayer:
+    """Move a built layer's pages to pinned host memory and allocate its page
+    cache (n_slots defaults to dynsplit_cache_slots: always enough for one
+    step).  keep_device=False drops the device copies of Kp / Vp."""
+    s = layer.shape
+    shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
+    if n_slots is None:
+        n_slots = cache_slots(shape, layer.cfg, budget)
+    dev = layer.block_starts.device
+    Kh = layer.Kp.cpu().pin_memory()
+    Vh = layer.Vp.cpu().pin_memory()
+    B, Hkv, _, P, d = layer.Kp.shape
+    Kc = torch.zeros(B, Hkv, n_slots, P, d, dtype=layer.Kp.dtype, device=dev)
+    Vc = torch.zeros_like(Kc)
+    res = PagedLayer(shape, layer.cfg, layer.w10, layer.block_starts, layer.n_blocks, layer.page_first,
+                     layer.page_block, layer.page_valid, layer.n_pages,
+                     layer.Kp if keep_device else None, layer.Vp if keep_device else None, layer.digests)
+    i32 = dict(dtype=torch.int32, device=dev)
+    return OffloadedLayer(res, Kh, Vh, n_slots, torch.full((B, Hkv, n_slots), -1, **i32), Kc, Vc,
+                          torch.zeros(B, Hkv, n_slots, 2, **i32), torch.zeros(B, Hkv, **i32),
+                          torch.zeros(B, Hkv, 2, **i32), torch.zeros(B, **i32),
+                          torch.zeros(worklist_bytes(shape, layer.cfg, budget), dtype=torch.uint8, device=dev))
+
+
+def _host_ptr(t: torch.Tensor):
+    if t.is_cuda or not t.is_pinned():
+        raise DynsplitError("expected a pinned host tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def reuse_plan(off: OffloadedLayer, worklist, Hq: int, truncate: bool = True, reuse: bool = True, ws=None):
+    """dynsplit_reuse_plan: Steps 1 and 3 against the cache's previous pages."""
+    s = off.layer.shape
+    shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
+    if ws is None:
+        ws = workspace(workspace_bytes(OP_REUSE, shape, off.layer.cfg), worklist.device, "reuse")
+    c = off.c()
+    _check(lib().dynsplit_reuse_plan(ctypes.byref(shape), ctypes.byref(off.layer.cfg), _ptr(worklist),
+                                     int(truncate), int(reuse), ctypes.byref(c), _ptr(ws), ws.numel(), _stream()),
+           "reuse_plan")
+
+
+def fetch_pages(off: OffloadedLayer, Hq: int, dense: bool = False) -> None:
+    """dynsplit_fetch_pages: move the planned pages (dense: every page) host -> cache."""
+    s = off.layer.shape
+    shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
+    c = off.c()
+    _check(lib().dynsplit_fetch_pages(ctypes.byref(shape), ctypes.byref(off.layer.cfg), _host_ptr(off.Kh),
+                                      _host_ptr(off.Vh), _ptr(off.layer.page_valid), _ptr(off.layer.n_pages),
+                                      int(dense), ctypes.byref(c), _stream()), "fetch_pages")
+
+
+def cache_view(off: OffloadedLayer) -> PagedLayer:
+    """The cache as a PagedLayer (Kp = Kc, page stride n_slots) for dynsplit_decode_attn."""
+    lay = off.layer
+    cfg = Config.from_buffer_copy(lay.cfg)
+    cfg.page_cap = off.n_slots
+    return PagedLayer(lay.shape, cfg, lay.w10, lay.block_starts, lay.n_blocks, lay.page_first, lay.page_block,
+                      lay.page_valid, lay.n_pages, off.Kc, off.Vc, lay.digests)
+
+
+def decode_layer_offload(q, off: OffloadedLayer, budget: int, truncate: bool = True, reuse: bool = True,
+                         scale: float = 0.0, out=None, ws=None):
+    """dynsplit_decode_layer_offload: a5+a6 on the resident digests, the reuse
+    plan, the move of the fresh pages from pinned host memory, a7+a8 over the
+    cache.  out = (n_sel, marginal_block, marginal_keep, worklist, o, lse).
+    -> (o, lse, Selection without scores / sel_blocks)."""
+    shape = _decode_shape(q, off.layer)
+    lay = off.layer
+    if out is None:
+        _, ns, mg, kp, wl = _sel_outputs(shape, lay.cfg, budget, q.device, want_blocks=False)
+        o = torch.empty(shape.B, shape.Hq, shape.d, dtype=torch.float32, device=q.device)
+        lse = torch.empty(shape.B, shape.Hq, dtype=torch.float32, device=q.device)
+    else:
+        ns, mg, kp, wl, o, lse = out
+    if ws is None:
+        ws = workspace(workspace_bytes(OP_DECODE_OFFLOAD, shape, lay.cfg, budget), q.device, "offload")
+    c = off.c()
+    _check(lib().dynsplit_decode_layer_offload(
+        ctypes.byref(shape), ctypes.byref(lay.cfg), budget, _ptr(q), _ptr(lay.digests), _ptr(lay.block_starts),
+        _ptr(lay.n_blocks), _ptr(lay.page_first), _ptr(lay.page_valid), _host_ptr(off.Kh), _host_ptr(off.Vh),
+        int(truncate), int(reuse), ctypes.byref(c), ctypes.c_float(scale), _ptr(ns), _ptr(mg), _ptr(kp), _ptr(wl),
+        _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream()), "decode_layer_offload")
+    return o, lse, Selection(None, ns, mg, kp, wl, None)
+
+
+def worklist_pages(worklist: torch.Tensor, shape: Shape):
+    """Host-side reading of a worklist (tests and metrics): per (b, KV head)
+    the page field of its entries, in entry order."""
+    import numpy as np
+    raw = worklist.cpu().numpy()
+    nbh = shape.B * shape.Hkv
+    max_wl = int(raw[:256].view(np.int32)[1])
+    counts = raw[256:256 + 4 * nbh].view(np.int32).copy()
+    off = 256 + ((4 * nbh + 255) // 256) * 256
+    ent = raw[off: off + 16 * nbh * max_wl].reshape(max_wl, nbh, 16).transpose(1, 0, 2)
+    return [ent[i, : counts[i], 0:4].copy().view(np.int32).ravel() for i in range(nbh)]

@@ -19,6 +19,9 @@ Recipes:
            exact integer in fp32, ties are frequent (tests the tie rule).
   scoring  Qs, Ks ~ N(0, I) plus a slowly drifting per-position component so
            attention has local structure; bf16.
+  walk     (NEXT-3) consecutive decode steps' queries as an AR(1) walk
+           q_t = tau q_{t-1} + sqrt(1 - tau^2) z_t, so neighbouring steps
+           select overlapping KV (the premise of cross-step reuse).
 """
 from __future__ import annotations
 
@@ -103,6 +106,20 @@ def decode_qkv_integer(seed: int, S: int, Hq: int, Hkv: int, d: int = 128,
     return q, K, V
 
 
+def decode_query_walk(seed: int, T: int, q0: np.ndarray, tau: float = 0.9,
+                      dtype: str = "bf16") -> np.ndarray:
+    """T consecutive decode-step queries [T, Hq, d] starting at q0 [Hq, d]:
+    q_t = tau q_{t-1} + sqrt(1 - tau^2) z_t (z_t ~ N(0, I)), rounded to bf16."""
+    r = rng(seed, 606)
+    out = np.empty((T,) + q0.shape, np.float32)
+    q = np.asarray(q0, np.float64)
+    for t in range(T):
+        if t:
+            q = tau * q + np.sqrt(1.0 - tau * tau) * r.standard_normal(q.shape)
+        out[t] = q
+    return to_bf16(out) if dtype == "bf16" else out
+
+
 def query_resample(seed: int, b: int, h: int, retry: int, d: int = 128,
                    dtype: str = "bf16") -> np.ndarray:
     """Replacement query for head h of sequence b (margin-certificate retry)."""
@@ -151,3 +168,14 @@ def torch_decode_layer(gen, S: int, Hq: int, Hkv: int, d: int, B: int, device,
     del K
     V = torch.randn(B, S, Hkv, d, generator=gen, device=device, dtype=torch.float32).to(torch.bfloat16)
     return q.to(torch.bfloat16), Kb, V
+
+
+def torch_query_walk(gen, T: int, q0, tau: float = 0.9):
+    """Device form of decode_query_walk: [T, *q0.shape] bf16 from q0 (bf16)."""
+    import torch
+    out = [q0]
+    q = q0.float()
+    for _ in range(T - 1):
+        q = tau * q + (1.0 - tau * tau) ** 0.5 * torch.randn(q.shape, generator=gen, device=q.device)
+        out.append(q.to(torch.bfloat16))
+    return torch.stack(out)
