@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the c3_b8 / c4 blocks")
     ap.add_argument("--no-e2e-model", action="store_true", help="skip the NEXT-4 decoder block")
+    ap.add_argument("--no-offload", action="store_true", help="skip the NEXT-3 offloaded-KV block")
+    ap.add_argument("--only-offload", action="store_true", help="run only the NEXT-3 block (development)")
     ap.add_argument("--cpu-sample-heads", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -583,6 +585,146 @@ def e2e_model_block(D, G, dev, B=8, S0=32768, outs=(64,), budget=2048):
             "speedup": res["dense"][n] / res["sparse"][n]}
 
 
+def measured_h2d_gbs(torch, dev, nbytes=1 << 28):
+    """Host -> device copy-engine bandwidth from pinned memory (cudaMemcpyAsync,
+    256 MiB, best of 5): the PCIe / C2C yardstick of the offload tier."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dbuf.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del h, dbuf
+    return best
+
+
+def offload_block(args, torch, D, G, dev, cur, barrier, S=32768, L=32, budget=2048, tau=0.9):
+    """NEXT-3 (the paper's CPU-GPU deployment, with KV
+    Reuse Steps 1-3): config 2's shape (Llama-3-8B decode, 32K,
+    budget 2K, one sequence) with every layer's pages in pinned host memory.
+    A decode step = per layer a5+a6 on the resident digests, the reuse plan,
+    the move of the fresh pages host -> device cache (zero-copy kernel reads
+    over PCIe), a7+a8 over the cache (dynsplit_decode_layer_offload), over a
+    walk of consecutive queries (q_t = tau q_{t-1} + sqrt(1 - tau^2) z).
+    Modes: paper (reuse, truncated to the min over KV heads), reuse without
+    truncation, no reuse, and the dense offloaded baseline (every page moved,
+    dense attention)."""
+    import dataclasses
+    Hq, Hkv, d = 32, 8, 128
+    wl = Workload(D, G, 1, S, Hq, Hkv, L, 0.0, 4242 + args.seed, dev, args.seed * 7919 + 300)
+    cfg, shape = wl.cfg, wl.shape
+    offs = []
+    for l in range(L):
+        offs.append(D.offload_layer(wl.layers[l], budget, Hq))
+        wl.layers[l] = None
+    torch.cuda.empty_cache()
+    T = args.warmup + args.steps
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(31 + args.seed)
+    walks = [G.torch_query_walk(gen, T, wl.qs[l], tau) for l in range(L)]   # [T, 1, Hq, d] per layer
+    qb = [torch.empty_like(wl.qs[l]) for l in range(L)]
+    outs = [(torch.empty(1, Hq, d, device=dev), torch.empty(1, Hq, device=dev)) for _ in range(L)]
+    sel = [D._sel_outputs(shape, cfg, budget, dev, want_blocks=False) for _ in range(L)]
+    ws = D.workspace(D.workspace_bytes(D.OP_DECODE_OFFLOAD, shape, cfg, budget), dev, "offload_bench")
+    pv = offs[0].layer.page_valid[0].long().cpu()
+
+    def run_mode(truncate, reuse):
+        def step():
+            for l in range(L):
+                _, ns, mg, kp, w = sel[l]
+                D.decode_layer_offload(qb[l], offs[l], budget, truncate=truncate, reuse=reuse,
+                                       out=(ns, mg, kp, w, outs[l][0], outs[l][1]), ws=ws)
+        for l in range(L):
+            qb[l].copy_(walks[l][0])
+        s2 = torch.cuda.Stream(dev)
+        s2.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s2):
+            step()
+        torch.cuda.current_stream(dev).wait_stream(s2)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        # timed: the walk from an empty cache; steps after the warm-up timed
+        for o_ in offs:
+            o_.reset()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(T + 1)]
+        moved, reused, pages = [], [], []
+        for t_ in range(T):
+            for l in range(L):
+                qb[l].copy_(walks[l][t_])
+            evs[t_].record(cur)
+            g.replay()
+        evs[T].record(cur)
+        barrier()
+        ms = evs[args.warmup].elapsed_time(evs[T]) / args.steps
+        # untimed replay of the same walk: bytes moved per step (valid rows of the fresh pages)
+        for o_ in offs:
+            o_.reset()
+        for t_ in range(T):
+            for l in range(L):
+                qb[l].copy_(walks[l][t_])
+            g.replay()
+            if t_ >= args.warmup:
+                mb = rb = npg = 0
+                for o_ in offs:
+                    fc = o_.fetch_count[0].cpu()
+                    fl = o_.fetch[0].cpu()
+                    for hk in range(Hkv):
+                        mb += int(pv[fl[hk, : int(fc[hk]), 0].long()].sum())
+                    st = o_.reuse_stats[0].cpu()
+                    rb += int(st[:, 0].sum())
+                    npg += int(st.sum())
+                moved.append(mb * 2 * d * 2)
+                reused.append(rb)
+                pages.append(npg)
+        assert D.read_device_error(ws) == 0
+        del g
+        return {"ms_per_step": ms, "moved_bytes_per_step": float(np.mean(moved)),
+                "pcie_GB_s": float(np.mean(moved)) / (ms * 1e-3) / 1e9,
+                "reused_page_frac": float(np.sum(reused)) / max(1, float(np.sum(pages)))}
+
+    res = {"paper_reuse_truncated": run_mode(True, True), "reuse_untruncated": run_mode(False, True),
+           "no_reuse": run_mode(True, False)}
+    # the fetch kernel alone (the last step's fetch lists, no-reuse mode: every selected page)
+    def fetch_only():
+        for l in range(L):
+            D.fetch_pages(offs[l], Hq)
+    fms, _, gf = time_graph(torch, fetch_only, args.steps, args.warmup, cur, dev, 1, barrier)
+    del gf
+    h2d = measured_h2d_gbs(torch, dev)
+    nm = res["no_reuse"]["moved_bytes_per_step"]
+    res["fetch_kernel"] = {"bound": "pcie", "achieved": nm / (fms * 1e-3) / 1e9, "unit": "GB/s",
+                           "peak": h2d, "frac": nm / (fms * 1e-3) / 1e9 / h2d, "us_per_layer": fms * 1e3 / L,
+                           "peak_source": "cudaMemcpyAsync pinned host -> device, 256 MiB, measured in this run"}
+    # dense offloaded baseline: every page of every layer moved, dense attention (shared device cache)
+    mp = D.max_pages(S, cfg)
+    Kc = torch.empty(1, Hkv, mp, cfg.page_size, d, dtype=torch.bfloat16, device=dev)
+    Vc = torch.empty_like(Kc)
+    dls = [dataclasses.replace(offs[l], n_slots=mp, Kc=Kc, Vc=Vc) for l in range(L)]
+    wsd = D.workspace(D.workspace_bytes(D.OP_DECODE_ATTN, shape, cfg), dev, "decode")
+
+    def dense_step():
+        for l in range(L):
+            D.fetch_pages(dls[l], Hq, dense=True)
+            D.decode_attn(qb[l], D.cache_view(dls[l]), None, out=outs[l], ws=wsd)
+    dms, _, gd = time_graph(torch, dense_step, 2, 1, cur, dev, 1, barrier)
+    del gd
+    dense_bytes = L * Hkv * S * 2 * d * 2
+    res["dense_offload"] = {"ms_per_step": dms, "moved_bytes_per_step": dense_bytes,
+                            "pcie_GB_s": dense_bytes / (dms * 1e-3) / 1e9}
+    res["speedup_vs_dense_offload"] = dms / res["paper_reuse_truncated"]["ms_per_step"]
+    res["workload"] = ("NEXT-3: C2 shape (Llama-3-8B decode, 32 layers, 32Q/8KV) at 32K, budget 2K, 1 sequence, "
+                       "KV pages in pinned host memory, query walk tau = %.2f" % tau)
+    res["context"] = "paper: 2.4x over full attention in its CPU-GPU deployment (P:473), A800 + PCIe, other models"
+    del offs, dls, Kc, Vc
+    torch.cuda.empty_cache()
+    return res
+
+
 def cpu_baseline_leg(args, wl: Workload, budget):
     """The oracle on this host's cores: 1 thread, and all cores (forked
     workers over whole KV groups of heads), on a bounded sample (heads of
@@ -720,6 +862,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if args.only_offload:
+        print(json.dumps({"offload": offload_block(args, torch, D, G, dev, cur, barrier)}), flush=True)
+        return
+
     # ---- the headline block: config 3's per-GPU shard, every layer its own cache
     wl = Workload(D, G, B, S, Hq, Hkv, L, args.rho, 1000003 * (args.seed + 1) + rank, dev,
                   args.seed * 7919 + rank * B)
@@ -790,6 +936,8 @@ def main():
         if not args.no_e2e_model:
             extra["e2e_model"] = e2e_model_block(D, G, dev)
             torch.cuda.empty_cache()
+        if not args.no_offload:
+            extra["offload"] = offload_block(args, torch, D, G, dev, cur, barrier)
 
     prefill = None
     if rank == 0 and not args.no_prefill:
