@@ -68,7 +68,7 @@ constexpr int kFBox = 32;            // digest rows per TMA box and per scoring-
 constexpr int kFSlabRowB = 128;      // bytes per row of one 64-dim digest slab
 constexpr int kFMaxGroups = 1024;    // (b, KV head) groups x NS bound of the moment slots
 constexpr int kBandCap = 256;        // band entries resolved by one warp (8 per lane)
-constexpr int kSlot = 64;            // band entries one CTA publishes per head
+constexpr int kSlot = kBandCap;      // band entries one CTA publishes per head (any range may hold the whole band)
 constexpr int kSub = 16;             // sub-bands of [t_lo, t_hi] (per-range token weights)
 constexpr int kH = 256;              // bins of a head's score histogram (the fallback of R25)
 

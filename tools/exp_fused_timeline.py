@@ -2,7 +2,7 @@
 graph of L layers, from the debug build's %globaltimer stamps (last layer's
 launch is the last writer of the stamp buffer).
 
-    DYNSPLIT_DEBUG_BUILD=1 python tools/exp_fused_timeline.py [budget] [B]
+    DYNSPLIT_DEBUG_BUILD=1 python tools/exp_fused_timeline.py [budget] [B] [Hq] [Hkv]
 """
 import ctypes
 import os
@@ -19,7 +19,9 @@ assert os.environ.get("DYNSPLIT_DEBUG_BUILD"), "needs the debug build"
 dev = torch.device("cuda:0")
 budget = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-S, Hq, Hkv, d, L = 131072, 32, 8, 128, 4
+Hq = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+Hkv = int(sys.argv[4]) if len(sys.argv) > 4 else 8
+S, d, L = 131072, 128, 4
 cfg = D.default_config()
 gen = torch.Generator(device=dev)
 gen.manual_seed(1)
@@ -60,6 +62,7 @@ for _ in range(3):
     g.replay()
 torch.cuda.synchronize()
 ncta = 148
+print(f"Hq {Hq} Hkv {Hkv}")
 dbg = torch.zeros(ncta * 64, dtype=torch.int64, device=dev)
 lib.dynsplit_debug_fused_timer.argtypes = [ctypes.c_void_p]
 lib.dynsplit_debug_fused_timer(ctypes.c_void_p(dbg.data_ptr()))

@@ -1,6 +1,6 @@
 """Per-layer time of the fused decode layer in a CUDA graph of L layers
 (release build; DYNSPLIT_LIB_AB=<file in lib/> times another build):
-    python tools/time_fused.py [S] [B] [budget] [L]"""
+    python tools/time_fused.py [S] [B] [budget] [L] [Hq] [Hkv]"""
 import os
 import sys
 
@@ -11,9 +11,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_03184_b200 import dynsplit as D  # noqa: E402
 from synth import generators as G  # noqa: E402
 
-S, B, budget, L = [int(x) for x in (sys.argv[1:] + ["131072", "1", "4096", "8"][len(sys.argv) - 1:])]
+S, B, budget, L, Hq, Hkv = [int(x) for x in (sys.argv[1:] + ["131072", "1", "4096", "8", "32", "8"][len(sys.argv) - 1:])]
 dev = torch.device("cuda:0")
-Hq, Hkv, d = 32, 8, 128
+d = 128
 cfg = D.default_config()
 gen = torch.Generator(device=dev)
 gen.manual_seed(1)
@@ -58,4 +58,4 @@ for rep in range(5):
     torch.cuda.synchronize()
     res.append(e0.elapsed_time(e1) / 50 / L * 1e3)
 print(f"{os.environ.get('DYNSPLIT_LIB_AB', 'libdynsplit.so')}: S {S} B {B} budget {budget}: "
-      f"{np.median(res):.2f} us/layer (min {min(res):.2f}), err {D.read_device_error(ws)}", flush=True)
+      f"Hq {Hq} Hkv {Hkv}: {np.median(res):.2f} us/layer (min {min(res):.2f}), err {D.read_device_error(ws)}", flush=True)
