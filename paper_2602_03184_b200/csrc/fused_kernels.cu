@@ -134,6 +134,14 @@ DSK_DEVICE unsigned ld_relaxed_gpu_u(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+DSK_DEVICE unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+DSK_DEVICE void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 DSK_DEVICE int ld_relaxed_gpu(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -152,17 +160,22 @@ constexpr int kGbarWords = 8 + kMaxSplit;
 DSK_DEVICE void gbar_arrive(unsigned* g, int split, unsigned e) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g + 8 + split), "r"(e) : "memory");
 }
-// one warp; true when all NS flags hold e
+// one warp; true when all NS flags hold e.  Relaxed polls, then one
+// fence.acq_rel (the acquire pattern of the PTX memory model: a relaxed read
+// that observes the release store, followed by the fence)
 DSK_DEVICE bool gbar_wait_warp(const unsigned* g, int NS, unsigned e) {
   const int lane = threadIdx.x & 31;
   for (int it = 0; it < (1 << 22); ++it) {
     bool ok = true;
     for (int r = lane; r < NS; r += 32) {
       unsigned v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g + 8 + r) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g + 8 + r) : "memory");
       ok &= v == e;
     }
-    if (__all_sync(0xffffffffu, ok)) return true;
+    if (__all_sync(0xffffffffu, ok)) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      return true;
+    }
   }
   return false;
 }
@@ -552,7 +565,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int gqa_mode, int budget_mode, int cap, int cap2,
     int ent_cap, int nwords,
     int sstride, size_t region_a, int per_cap, float scale_log2, float* __restrict__ scores,
-    float4* __restrict__ mom, int4* __restrict__ cls_w, int* __restrict__ cls_sub, uint2* __restrict__ cls_band,
+    unsigned long long* __restrict__ mom, int4* __restrict__ cls_w, int* __restrict__ cls_sub, uint2* __restrict__ cls_band,
     uint32_t* __restrict__ gbits,
     int* __restrict__ counters, unsigned* __restrict__ gbar, float* __restrict__ part_o,
     float* __restrict__ part_lse, int32_t* __restrict__ n_sel_out, int32_t* __restrict__ marg_out,
@@ -825,9 +838,17 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       mn = fminf(mn, r.z);
       mx = fmaxf(mx, r.w);
     }
-    mom[((size_t)bh * NS + split) * G + tid] = make_float4(a, c2, mn, mx);
+    // barrier A is the moments themselves: each value goes out as one 64-bit
+    // word tagged with the launch's epoch (single-copy atomic), so a reader
+    // that sees the tag sees the value -- no flag and no second round trip
+    const unsigned long long tag = (unsigned long long)s_target << 32;
+    unsigned long long* mw = mom + (((size_t)bh * NS + split) * G + tid) * 4;
+    st_relaxed_u64(mw + 0, tag | __float_as_uint(a));
+    st_relaxed_u64(mw + 1, tag | __float_as_uint(c2));
+    st_relaxed_u64(mw + 2, tag | __float_as_uint(mn));
+    st_relaxed_u64(mw + 3, tag | __float_as_uint(mx));
   }
-  __syncthreads();  // every score and moment write of the CTA precedes the arrive
+  __syncthreads();  // (the scores this CTA wrote to global are read only after barrier B)
   fstamp(3);
 
   // ---- 2. (a6) selection, distributed over the group's CTAs.  After
@@ -839,26 +860,38 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   //      block inside the band (exact, f_band_select), or -- when the bounds
   //      do not bracket it -- over every score of the head (slow path).
   unsigned* gb = gbar + (size_t)bh * kGbarWords;
-  if (warp == 0) {
-    const unsigned e = s_target;  // read after the PDL wait
-    if (lane == 0) gbar_arrive(gb, split, e);
-    if (!gbar_wait_warp(gb, NS, e) && lane == 0) raise_err(err, kErrSyncTimeout);
-  }
-  __syncthreads();
-  fstamp(4);
   // bounds per head from the group's moments (fixed order); keys above t_hi
   // are surely selected, the marginal block lies in [t_lo, t_hi] when the
-  // published weights verify it
+  // published weights verify it.  Warp g polls head g's NS tagged records
+  // until every tag is this launch's epoch (barrier A).
   if (warp < G) {
     const int g2 = warp;
     float c1 = 0.f, c2 = 0.f, gmn = CUDART_INF_F, gmx = -CUDART_INF_F;
-    for (int r = lane; r < NS; r += 32) {
-      const float4 mm = __ldcg(mom + ((size_t)bh * NS + r) * G + g2);
-      c1 += mm.x;
-      c2 += mm.y;
-      gmn = fminf(gmn, mm.z);
-      gmx = fmaxf(gmx, mm.w);
+    const unsigned e = s_target;
+    bool done = false;
+    for (int it = 0; it < (1 << 22) && !done; ++it) {
+      float x1 = 0.f, x2 = 0.f, xn = CUDART_INF_F, xx = -CUDART_INF_F;
+      bool ok = true;
+      for (int r = lane; r < NS; r += 32) {
+        const unsigned long long* mw = mom + (((size_t)bh * NS + r) * G + g2) * 4;
+        const unsigned long long w0 = ld_relaxed_u64(mw), w1 = ld_relaxed_u64(mw + 1);
+        const unsigned long long w2 = ld_relaxed_u64(mw + 2), w3 = ld_relaxed_u64(mw + 3);
+        ok &= (unsigned)(w0 >> 32) == e && (unsigned)(w1 >> 32) == e && (unsigned)(w2 >> 32) == e &&
+              (unsigned)(w3 >> 32) == e;
+        x1 += __uint_as_float((unsigned)w0);
+        x2 += __uint_as_float((unsigned)w1);
+        xn = fminf(xn, __uint_as_float((unsigned)w2));
+        xx = fmaxf(xx, __uint_as_float((unsigned)w3));
+      }
+      if (__all_sync(0xffffffffu, ok)) {
+        done = true;
+        c1 = x1;
+        c2 = x2;
+        gmn = xn;
+        gmx = xx;
+      }
     }
+    if (!done && lane == 0) raise_err(err, kErrSyncTimeout);
     c1 = warp_sum(c1);
     c2 = warp_sum(c2);
     gmn = -warp_max(-gmn);
@@ -884,6 +917,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     }
   }
   __syncthreads();
+  fstamp(4);
   // classification of this CTA's range: warp w takes head g = w % G and the
   // range's words w / G, w / G + 8 / G, ...; lane l is block lo + 32 word + l.
   // A band entry also gets its sub-band sb = floor(16 (x - t_lo) / (t_hi -
@@ -1370,7 +1404,8 @@ namespace dsk {
 static size_t fs_al(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t fused_scratch_bytes(int B, int Hq, int maxb) {
   const size_t nwords = ((size_t)maxb + 31) / 32;
-  return 2 * fs_al((size_t)kFMaxGroups * kMaxG * 16) + fs_al((size_t)kFMaxGroups * kMaxG * kSlot * 8) +
+  return fs_al((size_t)kFMaxGroups * kMaxG * 32) + fs_al((size_t)kFMaxGroups * kMaxG * 16) +
+         fs_al((size_t)kFMaxGroups * kMaxG * kSlot * 8) +
          fs_al((size_t)B * Hq * nwords * 4) + fs_al((size_t)kFMaxGroups * kMaxG * kSub * 4);
 }
 
@@ -1380,7 +1415,7 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
                              const bf16* Vp, int Hq, int Hkv, int maxb, int max_pages, int S, int Pshift,
                              int budget, int gqa_mode, int budget_mode, int cap, int cap2, int ent_cap, int nwords,
                              int sstride, size_t region_a,
-                             int per_cap, float sl2, float* scores, float4* mom, int4* cls_w, int* cls_sub,
+                             int per_cap, float sl2, float* scores, unsigned long long* mom, int4* cls_w, int* cls_sub,
                              uint2* cls_band, uint32_t* gbits, int* counters, unsigned* gbar,
                              float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
                              int32_t* wl_count, WLEntry* wl, float* o, float* lse, int* err) {
@@ -1446,10 +1481,11 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
   char* fs = static_cast<char*>(fscratch);
-  float4* mom = reinterpret_cast<float4*>(fs);
-  int4* cls_w = reinterpret_cast<int4*>(fs + fs_al((size_t)kFMaxGroups * kMaxG * 16));
-  uint2* cls_band = reinterpret_cast<uint2*>(fs + 2 * fs_al((size_t)kFMaxGroups * kMaxG * 16));
-  uint32_t* gbits = reinterpret_cast<uint32_t*>(fs + 2 * fs_al((size_t)kFMaxGroups * kMaxG * 16) +
+  unsigned long long* mom = reinterpret_cast<unsigned long long*>(fs);  // [groups x NS][G][4] tagged
+  const size_t o_w = fs_al((size_t)kFMaxGroups * kMaxG * 32);
+  int4* cls_w = reinterpret_cast<int4*>(fs + o_w);
+  uint2* cls_band = reinterpret_cast<uint2*>(fs + o_w + fs_al((size_t)kFMaxGroups * kMaxG * 16));
+  uint32_t* gbits = reinterpret_cast<uint32_t*>(fs + o_w + fs_al((size_t)kFMaxGroups * kMaxG * 16) +
                                                 fs_al((size_t)kFMaxGroups * kMaxG * kSlot * 8));
   int* cls_sub = reinterpret_cast<int*>(reinterpret_cast<char*>(gbits) + fs_al((size_t)B * Hq * nwords * 4));
   unsigned* gbar = reinterpret_cast<unsigned*>(bar);
