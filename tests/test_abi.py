@@ -102,3 +102,34 @@ def test_append_argument_validation(D):
                                   1 << 20, None)
     assert st == 5  # DYNSPLIT_ERR_UNSUPPORTED (C + Delta above the staging bound)
     assert D.workspace_bytes(D.OP_APPEND, sh, cfg) > 0
+
+
+def test_offload_abi_without_gpu(D):
+    """NEXT-3 entry points: the cache-slot bound (per query head at most
+    ceil(budget / P) + max_selected pages, times g, capped at max_pages), the
+    workspace sizes, and host-side rejection of bad caches before any launch."""
+    import ctypes as C
+    lib = D.lib()
+    c = D.default_config()
+    sh = D.make_shape(1, 32768, 32, 8)
+    g = 4
+    per_head = (2048 + 15) // 16 + D.max_selected(2048, 32768, c)
+    assert D.cache_slots(sh, c, 2048) == min(g * per_head, D.max_pages(32768, c))
+    tiny = D.make_shape(1, 100, 32, 8)
+    assert D.cache_slots(tiny, c, 4096) == D.max_pages(100, c)       # capped
+    assert D.cache_slots(sh, c, 0) == 0                               # budget < 1
+    assert D.workspace_bytes(D.OP_REUSE, sh, c) > 0
+    assert D.workspace_bytes(D.OP_DECODE_OFFLOAD, sh, c, 2048) > D.workspace_bytes(D.OP_DECODE_ATTN, sh, c)
+    p = C.c_void_p(16)  # never dereferenced: validation fails first
+    ws_ok = D.workspace_bytes(D.OP_REUSE, sh, c)
+    # null cache, zero / oversize slot counts, missing outputs -> INVALID_ARGUMENT (1)
+    assert lib.dynsplit_reuse_plan(C.byref(sh), C.byref(c), p, 1, 1, None, p, ws_ok, None) == 1
+    for n_slots in (0, D.max_pages(32768, c) + 1):
+        k = D.KVCache(n_slots, p, p, p, p, p, p, p, p)
+        assert lib.dynsplit_reuse_plan(C.byref(sh), C.byref(c), p, 1, 1, C.byref(k), p, ws_ok, None) == 1
+    k = D.KVCache(64, p, p, p, None, p, p, p, p)
+    assert lib.dynsplit_reuse_plan(C.byref(sh), C.byref(c), p, 1, 1, C.byref(k), p, ws_ok, None) == 1
+    k = D.KVCache(64, p, p, p, p, p, p, p, p)
+    assert lib.dynsplit_reuse_plan(C.byref(sh), C.byref(c), p, 1, 1, C.byref(k), p, ws_ok - 1, None) == 4
+    # dense fetch needs n_slots == max_pages (DIMENSION_MISMATCH, 2)
+    assert lib.dynsplit_fetch_pages(C.byref(sh), C.byref(c), p, p, p, p, 1, C.byref(k), None) == 2

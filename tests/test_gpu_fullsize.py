@@ -121,3 +121,43 @@ def test_decode_128k_batch8():
                 and kp[b, h] == res["keep"][h], (b, h)
         assert np.all(H.row_rel_err(o_np[b], res["o"]) <= 2e-3)
         assert np.all(np.abs(lse_np[b] - res["lse"]) <= 1e-4 * np.maximum(1, np.abs(res["lse"])))
+
+
+def test_offload_reuse_32k():
+    """NEXT-3 at config 2's size (32K, 32Q/8KV, budget 2K) with the page cache
+    sized by dynsplit_cache_slots, through dynsplit_decode_layer_offload over a
+    3-step query walk: every KV head's page set, moved (fresh) pages, reuse
+    counts and reuse_len bit-exact against O.offload_decode_loop, o / lse
+    bit-identical to the resident path and within R17 of the oracle."""
+    from paper_2602_03184_b200 import dynsplit as D
+    S, Hq, Hkv, d, budget, T = 32768, 32, 8, 128, 2048, 3
+    cfg = D.default_config()
+    toks = G.tokens(2100, S)
+    q0, K, V = G.decode_qkv(2101, S, Hq, Hkv, d)
+    starts = O.segment(toks, G.T7_IDS, G.T7_W10, cfg.C, cfg.delta)
+    qs = G.decode_query_walk(2102, T, q0, 0.9)
+    qs = np.stack([H.certify_queries(2103 + i, qs[i][None], K[None], [starts], budget)[0] for i in range(T)])
+    layer = D.build_blocks(t(toks[None]), t(G.T7_IDS), t(K[None], torch.bfloat16),
+                           t(V[None], torch.bfloat16), cfg, static_w10=G.T7_W10, Hq=Hq)
+    off = D.offload_layer(layer, budget, Hq, keep_device=True)
+    shape = D.make_shape(1, S, Hq, Hkv)
+    ref = O.offload_decode_loop(qs, K, V, starts, budget, P=cfg.page_size, truncate=True)
+    for i in range(T):
+        qt = t(qs[i][None], torch.bfloat16)
+        o, lse, sel = D.decode_layer_offload(qt, off, budget)
+        o_r, lse_r = D.decode_attn(qt, layer, sel.worklist)
+        torch.cuda.synchronize()
+        assert torch.equal(o, o_r) and torch.equal(lse, lse_r)
+        pages = D.worklist_pages(sel.worklist, shape)
+        fc = off.fetch_count.cpu().numpy()[0]
+        fl = off.fetch.cpu().numpy()[0]
+        st = off.reuse_stats.cpu().numpy()[0]
+        r = ref[i]
+        for hk in range(Hkv):
+            assert np.sort(pages[hk]).tolist() == r["pages"][hk].tolist(), (i, hk)
+            assert fl[hk, : fc[hk], 0].tolist() == r["fresh"][hk].tolist(), (i, hk)
+            assert st[hk].tolist() == [len(r["reused"][hk]), len(r["fresh"][hk])], (i, hk)
+        assert int(off.reuse_len[0]) == r["reuse_len"]
+        assert np.all(H.row_rel_err(o[0].cpu().numpy(), r["o"]) <= 2e-3)
+        assert np.all(np.abs(lse[0].cpu().numpy() - r["lse"]) <= 1e-4 * np.maximum(1, np.abs(r["lse"])))
+    assert sum(len(x) for x in ref[-1]["reused"]) > 0
