@@ -918,6 +918,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   }
   __syncthreads();
   fstamp(4);
+  if (tid == 0) fstampx(4);
   // classification of this CTA's range: warp w takes head g = w % G and the
   // range's words w / G, w / G + 8 / G, ...; lane l is block lo + 32 word + l.
   // A band entry also gets its sub-band sb = floor(16 (x - t_lo) / (t_hi -
@@ -956,6 +957,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         }
       }
     }
+    if (tid == 0) fstampx(5);
     whi = warp_sum_i(whi);
     wbd = warp_sum_i(wbd);
     if (lane == 0) {
@@ -1049,7 +1051,9 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     } else if (W_hi >= budget || W_hi + W_bd < budget || over || nband > kBandCap || force) {
       fb = 1;  // the bounds did not bracket the marginal block: exact slow path below
     } else {
+      if (tid == 0) fstampx(6);
       const int4 r = f_band_select(sband + (size_t)g2 * kBandCap, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
+      if (tid == 0) fstampx(7);
       m = r.x;
       keep = r.y;
       T = (uint32_t)r.z;

@@ -93,6 +93,15 @@ for k in ORDER:
             mhz = f"  SM clock over the phase {dc.sum() / dt.sum() * 1e3:6.0f} MHz, {np.median(dc):8.0f} cycles p50"
     print(f"{k:2d} {name:18s} n={len(col):3d}  min {r.min():7.2f}  p50 {np.median(r):7.2f}  max {r.max():7.2f} us{mhz}")
     prev = k
+# extra %globaltimer stamps (thread 0): 56 + k
+XN = {4: "bounds ready", 5: "classified (loop)", 6: "gathered (warp 0)", 7: "band-selected (warp 0)"}
+tx = tc[used, 56:64]
+for k, name in XN.items():
+    col = tx[:, k]
+    col = col[col > 0]
+    if len(col):
+        r = (col - t0) / 1e3
+        print(f"x{k} {name:22s} n={len(col):3d}  min {r.min():7.2f}  p50 {np.median(r):7.2f}  max {r.max():7.2f} us")
 # per-layer time from the graph
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
