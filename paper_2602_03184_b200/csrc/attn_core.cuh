@@ -252,6 +252,169 @@ DSK_DEVICE void attn_bf16_pipeline(unsigned char* smem, uint32_t (*s_rows)[2], c
 }
 
 // ---------------------------------------------------------------------------
+// The same pipeline with the pages moved by TMA tensor copies instead of
+// per-lane LDGSTS (A/B variant, DYNSPLIT_ATTN_TMA=1, bf16, P = 16): per page
+// lane 0 issues four 2-D boxes (K / V x two 64-dim slabs, 16 rows x 128 B,
+// 128-byte hardware swizzle) into an unpadded 8 KiB stage completing on the
+// stage's mbarrier; ldmatrix reads the swizzled rows (chunk c of row r at
+// (c ^ (r & 7)) * 16).  A box always moves all 16 rows of a page (its padding
+// rows are zero in HBM), where LDGSTS moves only the rows some head needs.
+// ---------------------------------------------------------------------------
+template <int G, int NW, int D, typename EntryFn>
+DSK_DEVICE void attn_bf16_pipeline_tma(unsigned char* ring, uint64_t* bars, uint32_t (*s_rows)[2],
+                                       const bf16* s_q, int nd, int n_mine, EntryFn entry, const CUtensorMap* tmK,
+                                       const CUtensorMap* tmV, size_t bh, int max_pages, float scale_log2) {
+  constexpr int STAGE = 8192, SLAB = 2048;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wring = ring + (size_t)warp * nd * STAGE;
+  uint64_t* wb = bars + warp * D;
+  auto issue = [&](int j) {
+    if (j >= n_mine) return;
+    int pg;
+    uint32_t a, c;
+    entry(j, pg, a, c);
+    int rmax = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) rmax = max(rmax, entry_rows(a, c, g));
+    if ((unsigned)pg >= (unsigned)max_pages) rmax = 0;
+    const int st = j % nd;
+    if (lane == 0) {
+      s_rows[warp * D + st][0] = rmax ? a : 0u;
+      s_rows[warp * D + st][1] = rmax ? c : 0u;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // this stage's reads before the TMA writes
+    __syncwarp();
+    if (lane == 0) {
+      if (rmax > 0) {
+        const int row = (int)((bh * max_pages + pg) * 16);
+        unsigned char* d = wring + st * STAGE;
+        mbar_arrive_expect_tx(&wb[st], STAGE);
+        tma_load_2d(d, tmK, 0, row, &wb[st]);
+        tma_load_2d(d + SLAB, tmK, 64, row, &wb[st]);
+        tma_load_2d(d + 2 * SLAB, tmV, 0, row, &wb[st]);
+        tma_load_2d(d + 3 * SLAB, tmV, 64, row, &wb[st]);
+      } else {
+        mbar_arrive(&wb[st]);
+      }
+    }
+  };
+  for (int j = 0; j < nd; ++j) issue(j);
+
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t qa[8][2];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    qa[ks][0] = qa[ks][1] = 0u;
+    if (g < G) {
+      const uint32_t* qw = reinterpret_cast<const uint32_t*>(s_q + (size_t)g * kD + ks * 16 + 2 * t);
+      qa[ks][0] = qw[0];
+      qa[ks][1] = qw[4];
+    }
+  }
+  float m_run = -CUDART_INF_F, l_run = 0.f;
+  float acc[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  // ldmatrix.x4 lane address: matrix mi = lane / 8 covers rows 8 (mi / 2) + lr
+  // and 16-byte chunk 2 k + mi % 2 of the k-th 32-byte column step
+  const int mi = lane >> 3, lr = lane & 7;
+  const int rl = (mi >> 1) * 8 + lr;
+  const uint32_t wring_s = smem_u32(wring);
+  auto sw = [&](int chunk) {  // byte offset of 16-byte chunk `chunk` (0..15) of row rl, slabbed + swizzled
+    return (uint32_t)((chunk >> 3) * SLAB + rl * 128 + (((chunk & 7) ^ lr) << 4));
+  };
+  for (int j = 0; j < n_mine; ++j) {
+    const int st = j % nd;
+    mbar_wait(&wb[st], (uint32_t)((j / nd) & 1));
+    const uint32_t ra = s_rows[warp * D + st][0], rc = s_rows[warp * D + st][1];
+    int rmax = 0;
+#pragma unroll
+    for (int h = 0; h < G; ++h) rmax = max(rmax, entry_rows(ra, rc, h));
+    const int myrows = g < G ? entry_rows(ra, rc, g) : 0;
+    if (rmax > 0) {
+      const uint32_t kb = wring_s + (uint32_t)(st * STAGE);
+      const uint32_t vb = kb + 2 * SLAB;
+      float s[4][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[c][0] = s[c][1] = s[c][2] = s[c][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t bk[4];
+        ldsm_x4(bk, kb + sw(2 * ks + (mi & 1)));
+        mma_rows8(s[(ks & 1) * 2 + 0], qa[ks][0], qa[ks][1], bk[0], bk[1]);
+        mma_rows8(s[(ks & 1) * 2 + 1], qa[ks][0], qa[ks][1], bk[2], bk[3]);
+      }
+      const int k0 = 2 * t;
+      float z[4];
+      z[0] = k0 < myrows ? (s[0][0] + s[2][0]) * scale_log2 : -CUDART_INF_F;
+      z[1] = k0 + 1 < myrows ? (s[0][1] + s[2][1]) * scale_log2 : -CUDART_INF_F;
+      z[2] = k0 + 8 < myrows ? (s[1][0] + s[3][0]) * scale_log2 : -CUDART_INF_F;
+      z[3] = k0 + 9 < myrows ? (s[1][1] + s[3][1]) * scale_log2 : -CUDART_INF_F;
+      const float zmax = fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3]));
+      if (__any_sync(0xffffffffu, zmax > m_run + 8.f)) {
+        float mx = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mnew = fmaxf(m_run, mx);
+        const float corr = (mnew == -CUDART_INF_F || m_run == mnew) ? 1.f : exp2f(m_run - mnew);
+        m_run = mnew;
+        l_run *= corr;
+        const float c0 = __shfl_sync(0xffffffffu, corr, 8 * t);
+        const float c1 = __shfl_sync(0xffffffffu, corr, 8 * t + 4);
+#pragma unroll
+        for (int j2 = 0; j2 < 8; ++j2) {
+          acc[j2][0] *= c0;
+          acc[j2][1] *= c1;
+          acc[j2][2] *= c0;
+          acc[j2][3] *= c1;
+        }
+      }
+      float p[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        p[k] = z[k] == -CUDART_INF_F ? 0.f : exp2f(z[k] - m_run);
+        l_run += p[k];
+      }
+      const __nv_bfloat162 h01 = __floats2bfloat162_rn(p[0], p[1]);
+      const __nv_bfloat162 h23 = __floats2bfloat162_rn(p[2], p[3]);
+      const __nv_bfloat162 l01 = __floats2bfloat162_rn(p[0] - __low2float(h01), p[1] - __high2float(h01));
+      const __nv_bfloat162 l23 = __floats2bfloat162_rn(p[2] - __low2float(h23), p[3] - __high2float(h23));
+      const uint32_t bh0 = bf16x2_bits(h01), bh1 = bf16x2_bits(h23);
+      const uint32_t bl0 = bf16x2_bits(l01), bl1 = bf16x2_bits(l23);
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) {
+        uint32_t av[4];
+        ldsm_x4_t(av, vb + sw(2 * j2 + (mi & 1)));
+        const uint32_t a4[4] = {av[0], av[1], av[2], av[3]};
+        mma_16816(acc[j2], a4, bh0, bh1);
+        mma_16816(acc[j2], a4, bl0, bl1);
+      }
+    }
+    __syncwarp();  // the stage is free
+    issue(j + nd);
+  }
+  float* sc = reinterpret_cast<float*>(ring);
+  named_bar_sync(1, NW * 32);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int h = 2 * t + e;
+    if (h < G) {
+      float* row = sc + (warp * G + h) * kScStride + g;
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) {
+        row[16 * j2] = acc[j2][e];
+        row[16 * j2 + 8] = acc[j2][2 + e];
+      }
+    }
+  }
+  if (g < G && t == 0) {
+    sc[(warp * G + g) * kScStride + kD] = m_run;
+    sc[(warp * G + g) * kScStride + kD + 1] = l_run;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Merge the NW warps' states in sc (fixed order) into this split's (o, lse);
 // with n_eff > 1 write the split partial, take the (b, KV head) ticket and,
 // in the last CTA, merge the n_eff splits in split order.  All NW warps of the

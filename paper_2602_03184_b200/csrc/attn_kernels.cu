@@ -33,8 +33,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cudaTypedefs.h>
 #include <math_constants.h>
 #include <stdlib.h>
+#include <string.h>
 
 namespace dsk {
 
@@ -87,7 +89,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
     const int32_t* __restrict__ wl_hdr, const int32_t* __restrict__ wl_count,
     const WLEntry* __restrict__ wl, int dense, int Hq, int Hkv, int max_pages, int P,
     float scale_log2, float* __restrict__ part_o, float* __restrict__ part_lse,
-    int* __restrict__ counters, int n_split, float* __restrict__ o, float* __restrict__ lse) {
+    int* __restrict__ counters, int n_split, float* __restrict__ o, float* __restrict__ lse, int tma,
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
   constexpr bool kTC = sizeof(T) == 2;  // bf16: QK and PV on the tensor cores (mma.sync)
   extern __shared__ __align__(128) unsigned char smem[];
   // K and V rows are staged with a 16-byte pad (row stride ROW + 16): the 8
@@ -105,6 +108,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
   T* s_q = reinterpret_cast<T*>(s_rows + NW * D);                  // [G][kD]
   float2* pbuf = reinterpret_cast<float2*>(s_q + G * kD);          // [NW][16][G] (fp32 path)
   __shared__ int s_last;
+  __shared__ __align__(8) uint64_t s_tbar[NW * D];  // TMA variant: one mbarrier per (warp, stage)
+  unsigned char* ring_t = smem + ((1024u - (smem_u32(smem) & 1023u)) & 1023u);  // TMA variant: 1024-aligned
 
   const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -113,6 +118,10 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
   if (threadIdx.x == 0) astamp(0);
   // prologue independent of the preceding kernel (PDL overlap): V ring reset
   if (kTC) attn_zero_v_rings(smem, NW * nd, kstage, stage);
+  if (kTC && tma && (threadIdx.x & 31) == 0) {
+    for (int s2 = 0; s2 < D; ++s2) mbar_init(&s_tbar[warp * D + s2], 1);
+    fence_mbar_init();
+  }
   pdl_trigger();
   pdl_wait();  // q and the worklist belong to the step: read only after the wait
   if (threadIdx.x == 0) astamp(1);
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
 #else
   const bool noload = false;
 #endif
-  float* sc = reinterpret_cast<float*>(smem);  // merge scratch [NW][G][kScStride], reuses the ring
+  float* sc = reinterpret_cast<float*>(kTC && tma ? ring_t : smem);  // merge scratch [NW][G][kScStride] (ring)
   if constexpr (kTC) {
     auto entry = [&](int j, int& pg, uint32_t& a, uint32_t& c) {
       if ((j & 31) == 0 && j) load_batch(j, n_eff);
@@ -186,8 +195,12 @@ __global__ void __launch_bounds__(NW * 32, NW >= 8 ? 1 : 3) k_decode_attn(
       c = __shfl_sync(0xffffffffu, e_r1, j & 31);
     };
     if (threadIdx.x == 0) astamp(2);
-    attn_bf16_pipeline<G, NW, D>(smem, s_rows, s_q, nd, P, n_mine, entry, Kp, Vp, (size_t)bh, max_pages,
-                                 scale_log2, noload);
+    if (tma)
+      attn_bf16_pipeline_tma<G, NW, D>(ring_t, s_tbar, s_rows, s_q, D, n_mine, entry, &tmK, &tmV, (size_t)bh,
+                                       max_pages, scale_log2);
+    else
+      attn_bf16_pipeline<G, NW, D>(smem, s_rows, s_q, nd, P, n_mine, entry, Kp, Vp, (size_t)bh, max_pages,
+                                   scale_log2, noload);
     if (threadIdx.x == 0) astamp(3);
   } else {
   // ---- fp32: per-warp load pipeline (as in attn_bf16_pipeline) + CUDA-core consumer
@@ -415,10 +428,28 @@ struct AttnLaunch {
     const int occ = occupancy(P);
     allow_max_dyn_smem(k_decode_attn<T, G, NW, D>);
     const int n_split = max(1, min(kMaxSplit, (num_sms() * occ) / max(1, B * Hkv)));
+    // A/B variant (DYNSPLIT_ATTN_TMA=1): pages by 2-D TMA boxes (bf16, P = 16, 8 warps)
+    CUtensorMap tmK, tmV;
+    memset(&tmK, 0, sizeof(tmK));
+    memset(&tmV, 0, sizeof(tmV));
+    int tma = 0;
+    if (sizeof(T) == 2 && P == 16 && NW == 8 && getenv("DYNSPLIT_ATTN_TMA")) {
+      const auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+      const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)B * Hkv * max_pages * 16};
+      const cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
+      const cuuint32_t box[2] = {64, 16};
+      const cuuint32_t es[2] = {1, 1};
+      tma = encode && encode(&tmK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(Kp), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+            encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(Vp), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     launch_ex(k_decode_attn<T, G, NW, D>, dim3(n_split, Hkv, B), dim3(NW * 32),
-              attn_smem<T, G, NW, D>(P), st, 1, static_cast<const T*>(q), static_cast<const T*>(Kp),
+              attn_smem<T, G, NW, D>(P) + (tma ? 1024 : 0), st, 1, static_cast<const T*>(q), static_cast<const T*>(Kp),
               static_cast<const T*>(Vp), pv, n_pages, wl_hdr, wl_count, wl, dense, Hq, Hkv,
-              max_pages, P, scale_log2, part_o, part_lse, counters, n_split, o, lse);
+              max_pages, P, scale_log2, part_o, part_lse, counters, n_split, o, lse, tma, tmK, tmV);
     return post_launch("k_decode_attn", st);
   }
 };

@@ -684,3 +684,34 @@ def test_mean_mode_parity(D, dtype, S, Hq, Hkv, budget):
     res = [O.decode_step(q[b], K[b], V[b], starts[b], budget, digest_mode="mean") for b in range(B)]
     _check_selection(layer, sel, res, B, Hq)
     _check_attention(o, lse, res, B, Hq)
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,budget,rho", [(8192, 32, 8, 2048, 0.0), (6001, 40, 40, 700, 0.0),
+                                                 (4000, 64, 8, 333, 0.5), (47, 8, 2, 20, 0.0)])
+def test_sparse_decode_parity_tma_variant(D, monkeypatch, S, Hq, Hkv, budget, rho):
+    """The A/B variant of k_decode_attn whose pages move by 2-D TMA boxes
+    (DYNSPLIT_ATTN_TMA=1; measured slower): same selection,
+    attention against the oracle, and the sparse / dense results equal to the
+    LDGSTS kernel up to fp32 rounding (same page order, same arithmetic)."""
+    B, d, dtype = 2, 128, "bf16"
+    cfg = D.default_config()
+    toks = np.stack([G.tokens(1700 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    qs, Ks, Vs = zip(*[G.decode_qkv(1800 + b, S, Hq, Hkv, d, rho=rho, dtype=dtype) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    q = H.certify_queries(1800, q, K, starts, budget, dtype)
+    layer = _build(D, toks, K, V, cfg, dtype, Hq)
+    qt = t(q, kv_dtype(dtype))
+    sel = D.select(qt, layer, budget)
+    o_l, lse_l = D.decode_attn(qt, layer, sel.worklist)
+    od_l, lsed_l = D.decode_attn(qt, layer, None)
+    monkeypatch.setenv("DYNSPLIT_ATTN_TMA", "1")
+    o, lse = D.decode_attn(qt, layer, sel.worklist)
+    od, lsed = D.decode_attn(qt, layer, None)
+    torch.cuda.synchronize()
+    monkeypatch.delenv("DYNSPLIT_ATTN_TMA")
+    res = H.oracle_decode(q, K, V, starts, budget)
+    _check_attention(o, lse, res, B, Hq)
+    for a, b_ in ((o, o_l), (od, od_l)):
+        assert np.all(H.row_rel_err(a.cpu().numpy().reshape(-1, d), b_.cpu().numpy().reshape(-1, d)) <= 1e-5)
+    assert torch.allclose(lse, lse_l, rtol=0, atol=1e-5) and torch.allclose(lsed, lsed_l, rtol=0, atol=1e-5)
