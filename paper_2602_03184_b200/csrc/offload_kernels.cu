@@ -15,7 +15,10 @@
 // are the union of its query heads' selections, Q18), the device holds one
 // slot per page of the previous step (slot_page), and:
 //   k_reuse_count  per (b, KV head): reusable pages = |this step's pages AND
-//                  the cached pages| (Step 1, before truncation);
+//                  the cached pages| (Step 1, before truncation) -- only when
+//                  a sequence has more than 8 KV heads; otherwise the KV heads
+//                  of a sequence form one cluster and k_reuse_apply exchanges
+//                  the counts through distributed shared memory;
 //   k_reuse_apply  per (b, KV head): reuse_len = min over the sequence's KV
 //                  heads (truncate) -> the first reuse_len reusable pages in
 //                  ascending page order are kept in their slots (Q24); every
@@ -31,6 +34,10 @@
 // for bit (reuse decides what is moved, never what is computed).
 #include "common.cuh"
 #include "kernels.h"
+
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
 
 namespace dsk {
 
@@ -101,9 +108,10 @@ __global__ void __launch_bounds__(kRT) k_reuse_apply(
     int32_t* __restrict__ map, int32_t* __restrict__ freelist, int32_t* __restrict__ slot_page,
     int32_t* __restrict__ fetch, int32_t* __restrict__ fetch_count, int32_t* __restrict__ stats,
     int32_t* __restrict__ reuse_len, int32_t* __restrict__ c_hdr, int32_t* __restrict__ c_count,
-    WLEntry* __restrict__ c_wl, int* err) {
+    WLEntry* __restrict__ c_wl, int* err, int in_cluster) {
   extern __shared__ uint32_t bm[];
   __shared__ int scan_sm[(kRT / 32 + 1) * 2];
+  __shared__ int s_cnt;
   const int Hkv = gridDim.x, hk = blockIdx.x, b = blockIdx.y;
   const int nwp = (max_pages + 31) >> 5;
   const size_t BH = (size_t)gridDim.x * gridDim.y, bh = (size_t)b * Hkv + hk;
@@ -114,11 +122,31 @@ __global__ void __launch_bounds__(kRT) k_reuse_apply(
   if (bh == 0 && threadIdx.x < 64) c_hdr[threadIdx.x] = wl_hdr[threadIdx.x];
   int cnt;
   reuse_bitmaps(cur, prv, nwp, wl_count, wl, BH, bh, slot_page, n_slots, max_pages, reuse, cnt, err);
-  // Step 1: the reuse length of the sequence (min over its KV heads)
+  // Step 1: the reuse length of the sequence (min over its KV heads).  With
+  // the sequence's KV heads in one cluster (Hkv <= 8) each CTA counts its own
+  // reusable pages and reads the others' counts from their shared memory;
+  // otherwise k_reuse_count has published them.
   int rl = 0x7fffffff;
-  if (!reuse) rl = 0;
-  else if (truncate)
+  if (in_cluster) {
+    cg::cluster_group cluster = cg::this_cluster();
+    int c = 0;
+    for (int i = threadIdx.x; i < nwp; i += kRT) c += __popc(cur[i] & prv[i]);
+    c = warp_sum_i(c);
+    if ((threadIdx.x & 31) == 0) scan_sm[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < kRT / 32; ++w) t += scan_sm[w];
+      s_cnt = t;
+    }
+    cluster.sync();
+    for (int h = 0; h < Hkv; ++h) rl = min(rl, *cluster.map_shared_rank(&s_cnt, h));
+    cluster.sync();  // the peers' counts stay alive until every CTA has read them
+  } else if (truncate && reuse) {
     for (int h = 0; h < Hkv; ++h) rl = min(rl, reusable[(size_t)b * Hkv + h]);
+  }
+  if (!reuse) rl = 0;
+  else if (!truncate) rl = 0x7fffffff;
   // the reusable pages in ascending order, the first rl kept: thread t owns
   // words [t * wpt, (t + 1) * wpt)
   const int wpt = (nwp + kRT - 1) / kRT;
@@ -280,13 +308,18 @@ cudaError_t launch_reuse_plan(const int32_t* wl_hdr, const int32_t* wl_count, co
   allow_max_dyn_smem(k_reuse_count);
   allow_max_dyn_smem(k_reuse_apply);
   const dim3 grid(Hkv, B);
-  launch_ex(k_reuse_count, grid, dim3(kRT), smem, st, 1, wl_count, wl, slot_page, n_slots, max_pages, reuse,
-            reusable, err);
-  cudaError_t e = post_launch("k_reuse_count", st);
-  if (e != cudaSuccess) return e;
-  launch_ex(k_reuse_apply, grid, dim3(kRT), smem, st, 1, wl_hdr, wl_count, wl, n_slots, max_pages, reuse,
-            truncate, reusable, map, freelist, slot_page, fetch, fetch_count, stats, reuse_len, c_hdr, c_count,
-            c_wl, err);
+  // one cluster per sequence (its KV heads) when it fits the portable size:
+  // one launch; otherwise the counts go through k_reuse_count
+  const int in_cluster = Hkv <= 8 && (truncate && reuse);
+  if (truncate && reuse && !in_cluster) {
+    launch_ex(k_reuse_count, grid, dim3(kRT), smem, st, 1, wl_count, wl, slot_page, n_slots, max_pages, reuse,
+              reusable, err);
+    cudaError_t e = post_launch("k_reuse_count", st);
+    if (e != cudaSuccess) return e;
+  }
+  launch_ex(k_reuse_apply, grid, dim3(kRT), smem, st, in_cluster ? Hkv : 1, wl_hdr, wl_count, wl, n_slots,
+            max_pages, reuse, truncate, reusable, map, freelist, slot_page, fetch, fetch_count, stats, reuse_len,
+            c_hdr, c_count, c_wl, err, in_cluster);
   return post_launch("k_reuse_apply", st);
 }
 

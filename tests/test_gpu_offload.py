@@ -106,7 +106,8 @@ def _check_against_oracle(steps, ref, Hkv, truncate, reuse):
 
 
 @pytest.mark.parametrize("truncate", [True, False])
-@pytest.mark.parametrize("S,Hq,Hkv,budget", [(3000, 8, 2, 256), (2100, 16, 4, 128)])
+@pytest.mark.parametrize("S,Hq,Hkv,budget", [(3000, 8, 2, 256), (2100, 16, 4, 128),
+                                              (1500, 12, 12, 128)])   # > 8 KV heads: two-kernel plan
 def test_offload_reuse_matches_oracle(S, Hq, Hkv, budget, truncate):
     T = 6
     toks, qs, K, V, starts, layer = _setup(71, S, Hq, Hkv, budget, T)
