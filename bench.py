@@ -480,7 +480,10 @@ def decode_block(args, torch, D, wl: Workload, L, budget, dev, cur, world, barri
            "union_factor": sum(union_rows[l % Ld] for l in range(L)) / (L * B * Hkv * budget),
            "fused_launches_per_step": fused_per_step}
     # the dominant (only) kernel: k_decode_fused, one launch per layer
-    res["roofline"] = {"bound": "hbm", "kernel": "k_decode_fused (a5+a6+a7+a8)",
+    kname = ("k_decode_fused (a5+a6+a7+a8)" if fused_per_step == L else
+             "three kernels per layer: k_score_blocks_tc -> k_select_reg -> k_decode_attn (the fused layer "
+             "declined this shape)")
+    res["roofline"] = {"bound": "hbm", "kernel": kname,
                        "achieved": step_bytes / L / (ms * 1e-3 / L) / 1e9, "peak": peak[0], "unit": "GB/s",
                        "frac": step_bytes / (ms * 1e-3) / 1e9 / peak[0],
                        "traffic": ncu_traffic("k_decode_fused"), "peak_source": peak[1],

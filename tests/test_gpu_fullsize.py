@@ -91,7 +91,8 @@ def test_prefill_scoring_64k_sampled():
 def test_decode_128k_batch8():
     """Config 3 unsharded (all 8 sequences of 128K on one GPU, the bench's
     c3_b8 block): dynsplit_decode_layer (one k_decode_fused launch, 2 splits
-    per (sequence, KV head), double-buffered digest staging) against the
+    per (sequence, KV head), double-buffered digest staging, the range's
+    scores re-staged in region A) against the
     three-kernel path bit for bit and every head of every sequence against
     the oracle."""
     from paper_2602_03184_b200 import dynsplit as D
@@ -105,7 +106,12 @@ def test_decode_128k_batch8():
     layer = D.build_blocks(t(toks), t(G.T7_IDS), t(np.stack(Ks), torch.bfloat16), t(np.stack(Vs), torch.bfloat16),
                            cfg, static_w10=G.T7_W10, Hq=Hq)
     qt = t(q, torch.bfloat16)
+    import ctypes
+    lib = D.lib()
+    lib.dynsplit_debug_fused_launches.restype = ctypes.c_longlong
+    n0 = lib.dynsplit_debug_fused_launches()
     o_l, lse_l, sel_l = D.decode_layer(qt, layer, budget)
+    assert lib.dynsplit_debug_fused_launches() - n0 == 1          # the fused layer took this shape
     sel = D.select(qt, layer, budget)
     o, lse = D.decode_attn(qt, layer, sel.worklist)
     torch.cuda.synchronize()
