@@ -42,7 +42,7 @@ namespace cg = cooperative_groups;
 namespace dsk {
 
 constexpr int kRT = 512;   // threads of the reuse kernels
-constexpr int kFW = 8;     // warps (pages) per fetch CTA
+constexpr int kFW = 4;     // warps per (persistent) fetch CTA
 
 // Bitmaps of one (b, KV head): bit p of `cur` = page p is in this step's
 // worklist; bit p of `prv` = page p sits in a cache slot.  Pages outside
@@ -246,53 +246,58 @@ __global__ void __launch_bounds__(kRT) k_reuse_apply(
   }
 }
 
-// One warp per page: rows [0, page_valid) of K and V, host -> cache slot.
-// dense: page p -> slot p for p < n_pages[b] (the offloaded dense baseline).
+// Persistent mover: one small CTA per SM; each warp walks the (b, KV head,
+// fetch index) items with a grid stride and copies a page's valid rows of K
+// and V, host -> cache slot (dense: page p -> slot p for p < n_pages[b]),
+// 8 16-byte loads per lane in flight before the stores.
 template <int ROWB>
 __global__ void __launch_bounds__(kFW * 32) k_fetch_pages(
     const unsigned char* __restrict__ Kh, const unsigned char* __restrict__ Vh,
     const int16_t* __restrict__ page_valid, const int32_t* __restrict__ n_pages,
-    const int32_t* __restrict__ fetch, const int32_t* __restrict__ fetch_count, int dense, int Hkv,
+    const int32_t* __restrict__ fetch, const int32_t* __restrict__ fetch_count, int dense, int B, int Hkv,
     int max_pages, int n_slots, int P, unsigned char* __restrict__ Kc, unsigned char* __restrict__ Vc) {
   constexpr int CPR = ROWB / 16;  // 16-byte chunks per row
   constexpr int U = 8;            // chunks per lane in flight (x2: K and V)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bh = blockIdx.y, b = bh / Hkv;
-  const int i = blockIdx.x * kFW + warp;
+  const int lane = threadIdx.x & 31;
   pdl_trigger();
-  pdl_wait();  // the fetch list is the predecessor's output
-  int page, slot;
-  if (dense) {
-    if (i >= min(n_pages[b], n_slots)) return;
-    page = slot = i;
-  } else {
-    if (i >= fetch_count[bh]) return;
-    page = fetch[((size_t)bh * n_slots + i) * 2];
-    slot = fetch[((size_t)bh * n_slots + i) * 2 + 1];
-    if ((unsigned)page >= (unsigned)max_pages || (unsigned)slot >= (unsigned)n_slots) return;
-  }
-  const int rows = min((int)page_valid[(size_t)b * max_pages + page], P);
-  const int nch = rows * CPR;
-  const uint4* ks = reinterpret_cast<const uint4*>(Kh + ((size_t)bh * max_pages + page) * P * ROWB);
-  const uint4* vs = reinterpret_cast<const uint4*>(Vh + ((size_t)bh * max_pages + page) * P * ROWB);
-  uint4* kd = reinterpret_cast<uint4*>(Kc + ((size_t)bh * n_slots + slot) * P * ROWB);
-  uint4* vd = reinterpret_cast<uint4*>(Vc + ((size_t)bh * n_slots + slot) * P * ROWB);
-  for (int c0 = 0; c0 < nch; c0 += 32 * U) {
-    uint4 a[U], v[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int c = c0 + k * 32 + lane;
-      if (c < nch) {
-        a[k] = __ldcs(ks + c);
-        v[k] = __ldcs(vs + c);
-      }
+  pdl_wait();  // the fetch lists are the predecessor's output
+  const long long items = (long long)B * Hkv * n_slots;
+  const long long nwarps = (long long)gridDim.x * kFW;
+  for (long long it = (long long)blockIdx.x * kFW + (threadIdx.x >> 5); it < items; it += nwarps) {
+    const int bh = (int)(it / n_slots), i = (int)(it % n_slots), b = bh / Hkv;
+    int page, slot;
+    if (dense) {
+      if (i >= min(n_pages[b], n_slots)) continue;
+      page = slot = i;
+    } else {
+      if (i >= fetch_count[bh]) continue;
+      page = fetch[((size_t)bh * n_slots + i) * 2];
+      slot = fetch[((size_t)bh * n_slots + i) * 2 + 1];
+      if ((unsigned)page >= (unsigned)max_pages || (unsigned)slot >= (unsigned)n_slots) continue;
     }
+    const int rows = min((int)page_valid[(size_t)b * max_pages + page], P);
+    const int nch = rows * CPR;
+    const uint4* ks = reinterpret_cast<const uint4*>(Kh + ((size_t)bh * max_pages + page) * P * ROWB);
+    const uint4* vs = reinterpret_cast<const uint4*>(Vh + ((size_t)bh * max_pages + page) * P * ROWB);
+    uint4* kd = reinterpret_cast<uint4*>(Kc + ((size_t)bh * n_slots + slot) * P * ROWB);
+    uint4* vd = reinterpret_cast<uint4*>(Vc + ((size_t)bh * n_slots + slot) * P * ROWB);
+    for (int c0 = 0; c0 < nch; c0 += 32 * U) {
+      uint4 a[U], v[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int c = c0 + k * 32 + lane;
-      if (c < nch) {
-        kd[c] = a[k];
-        vd[c] = v[k];
+      for (int k = 0; k < U; ++k) {
+        const int c = c0 + k * 32 + lane;
+        if (c < nch) {
+          a[k] = __ldcs(ks + c);
+          v[k] = __ldcs(vs + c);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int c = c0 + k * 32 + lane;
+        if (c < nch) {
+          kd[c] = a[k];
+          vd[c] = v[k];
+        }
       }
     }
   }
@@ -327,17 +332,17 @@ cudaError_t launch_fetch_pages(int dtype, const void* Kh, const void* Vh, const 
                                const int32_t* n_pages, const int32_t* fetch, const int32_t* fetch_count,
                                int dense, int B, int Hkv, int max_pages, int n_slots, int P, void* Kc, void* Vc,
                                cudaStream_t st) {
-  const dim3 grid((n_slots + kFW - 1) / kFW, B * Hkv);
+  const dim3 grid(num_sms());
   const auto* kh = static_cast<const unsigned char*>(Kh);
   const auto* vh = static_cast<const unsigned char*>(Vh);
   auto* kc = static_cast<unsigned char*>(Kc);
   auto* vc = static_cast<unsigned char*>(Vc);
   if (dtype == 0)
     launch_ex(k_fetch_pages<kD * 2>, grid, dim3(kFW * 32), 0, st, 1, kh, vh, page_valid, n_pages, fetch,
-              fetch_count, dense, Hkv, max_pages, n_slots, P, kc, vc);
+              fetch_count, dense, B, Hkv, max_pages, n_slots, P, kc, vc);
   else
     launch_ex(k_fetch_pages<kD * 4>, grid, dim3(kFW * 32), 0, st, 1, kh, vh, page_valid, n_pages, fetch,
-              fetch_count, dense, Hkv, max_pages, n_slots, P, kc, vc);
+              fetch_count, dense, B, Hkv, max_pages, n_slots, P, kc, vc);
   return post_launch("k_fetch_pages", st);
 }
 
