@@ -481,8 +481,12 @@ static size_t select_reg_smem_bytes(int G) {
   return (size_t)kRMax * 2 + (size_t)kRMax * 4 * 2 + (size_t)G * kRW * 4 + (size_t)kRW * 4;
 }
 
-template <int G>
-__global__ void __launch_bounds__(kSelNT, 1) k_select_reg(
+// MINB = 2 (64 registers, a few spilled bytes) lets two CTAs share an SM:
+// used when the launch has more CTAs than SMs (B Hkv G > SMs, e.g. 8 x 128K
+// per GPU: one wave instead of two, 131.7 -> 121.3 us per layer); otherwise
+// MINB = 1 (128 registers) is faster (B = 1: 32.4 vs 35.9 us per layer).
+template <int G, int MINB>
+__global__ void __launch_bounds__(kSelNT, MINB) k_select_reg(
     const float* __restrict__ scores, const int32_t* __restrict__ block_starts,
     const int32_t* __restrict__ n_blocks, const int32_t* __restrict__ page_first, int Hq, int Hkv,
     int maxb, int S, int max_sel, int max_wl, int Pshift, int budget, int blk_lo, int blk_hi,
@@ -885,8 +889,9 @@ static cudaError_t run_select(int B, int Hkv, size_t smem, const float* scores, 
                               int32_t* sel_blocks, int32_t* n_sel, int32_t* marg, int32_t* keep,
                               int32_t* wl_count, WLEntry* wl, int* err, cudaStream_t st) {
   if (maxb <= kRMax && !g_select_generic) {
-    allow_max_dyn_smem(k_select_reg<G>);
-    launch_ex(k_select_reg<G>, dim3(Hkv * G, B), dim3(kSelNT), select_reg_smem_bytes(G), st, G, scores,
+    auto kern = (size_t)B * Hkv * G > (size_t)num_sms() ? k_select_reg<G, 2> : k_select_reg<G, 1>;
+    allow_max_dyn_smem(kern);
+    launch_ex(kern, dim3(Hkv * G, B), dim3(kSelNT), select_reg_smem_bytes(G), st, G, scores,
               bs, nb, pf, Hq, Hkv, maxb, S, max_sel, max_wl, Pshift, budget, blk_lo, blk_hi, sel_blocks,
               n_sel, marg, keep, wl_count, wl, err);
     return post_launch("k_select_reg", st);
