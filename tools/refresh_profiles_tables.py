@@ -1,0 +1,56 @@
+"""Regenerate the round-2 summary tables of profiles/README.md from
+profiles/r2_bench_final.json (the committed bench line)."""
+import json
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+d = json.load(open(os.path.join(ROOT, "profiles", "r2_bench_final.json")))
+o = d["offload"]
+rows = [
+    ("headline: config 3 per-GPU shard (128K, 32 layers, 32Q/8KV, budget 4K, B = 1)", d["ms_per_step"], d["value"],
+     d["roofline"]["frac"], d["dense"]["sparse_speedup"], "`k_decode_fused`"),
+    ("config 3 unsharded (8 x 128K on one GPU)", d["c3_b8"]["ms_per_step"], d["c3_b8"]["GB_s"],
+     d["c3_b8"]["roofline"]["frac"], d["c3_b8"]["dense"]["sparse_speedup"],
+     "three kernels (the fused layer declines: shared memory; a variant that fits measured slower)"),
+    ("config 4 on one GPU (40 MHA heads, 40 layers, 128K)", d["c4"]["ms_per_step"], d["c4"]["GB_s"],
+     d["c4"]["roofline"]["frac"], d["c4"]["dense"]["sparse_speedup"], "`k_decode_fused`"),
+]
+t = ["| block | ms / step | GB/s (algorithmic) | frac of HBM peak | vs own dense | path |", "|---|---|---|---|---|---|"]
+for name, ms, gbs, fr, sp, path in rows:
+    t.append(f"| {name} | {ms:.3f} | {gbs:.0f} | {fr:.3f} | {sp:.2f}x | {path} |")
+t.append(f"| e2e (host q / o / lse, `dynsplit_decode_step_host_layers`) | {d['e2e']['ms_per_step']:.3f} | "
+         f"{d['e2e']['value']:.0f} | | | |")
+v = d["variants"]["gqa_group_shared"]
+t.append(f"| NEXT-2 group-shared GQA selection (R23), headline shape | {v['ms_per_step']:.3f} | {v['GB_s']:.0f} | "
+         f"{v['frac_of_peak']:.3f} | | `k_decode_fused` |")
+m = d["e2e_model"]
+t.append(f"| NEXT-4 decoder (8 x 32K, random Llama-3-8B weights), ms per token | {m['ms_per_token_sparse']:.2f} "
+         f"(dense {m['ms_per_token_dense']:.2f}) | | | {m['speedup']:.2f}x | |")
+t.append(f"| prefill config 5 (64K, B = 4): a1 | {d['prefill']['a1_ms']:.1f} | | "
+         f"{d['prefill']['a1_roofline']['frac_executed']:.2f} of the MUFU ex2 rate | | `k_lse_band_tc` |")
+main_table = "\n".join(t) + "\n"
+u = ["| mode | ms / step | bytes moved / step | PCIe GB/s | pages reused |", "|---|---|---|---|---|"]
+for key, name in (("paper_reuse_truncated", "paper: reuse truncated to the min over KV heads (Steps 1-3)"),
+                  ("reuse_untruncated", "reuse without truncation (R26)"),
+                  ("no_reuse", "no reuse (every selected page moved)")):
+    x = o[key]
+    u.append(f"| {name} | {x['ms_per_step']:.2f} | {x['moved_bytes_per_step'] / 1e6:.0f} MB | {x['pcie_GB_s']:.1f} | "
+             f"{x['reused_page_frac']:.2f} |")
+x = o["dense_offload"]
+u.append(f"| dense offloaded baseline (every page moved, dense attention) | {x['ms_per_step']:.2f} | "
+         f"{x['moved_bytes_per_step'] / 1e6:.0f} MB | {x['pcie_GB_s']:.1f} | -- |")
+off_table = "\n".join(u) + "\n"
+f = o["fetch_kernel"]
+off_text = (f"Sparse with reuse = {o['speedup_vs_dense_offload']:.1f}x the dense offloaded step (the paper reports\n"
+            "2.4x over full attention in its CPU-GPU deployment, P:473, on A800 + PCIe\n"
+            "with other models: context only).  The page mover (`k_fetch_pages`,\n"
+            f"persistent) alone: {f['achieved']:.1f} GB/s against this box's `cudaMemcpyAsync`\n"
+            f"pinned H2D rate measured in the same run ({f['peak']:.1f} GB/s): {f['frac']:.2f}.\n")
+p = os.path.join(ROOT, "profiles", "README.md")
+s = open(p).read()
+s = re.sub(r"\| block \| ms / step \| GB/s \(algorithmic\).*?\n\n", main_table + "\n", s, count=1, flags=re.S)
+s = re.sub(r"\| mode \| ms / step \| bytes moved / step.*?\n\n", off_table + "\n", s, count=1, flags=re.S)
+s = re.sub(r"Sparse with reuse = .*?\(\d+\.\d GB/s\)[^\n]*\n", off_text, s, count=1, flags=re.S)
+open(p, "w").write(s)
+print("ok")
