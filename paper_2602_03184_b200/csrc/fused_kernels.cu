@@ -67,7 +67,8 @@ constexpr int kFRC = 32;             // boundary candidates ranked by one warp
 constexpr int kFBox = 32;            // digest rows per TMA box and per scoring-range granule
 constexpr int kFSlabRowB = 128;      // bytes per row of one 64-dim digest slab
 constexpr int kFMaxGroups = 1024;    // (b, KV head) groups x NS bound of the moment slots
-constexpr int kBandCap = 256;        // band entries resolved by one warp (8 per lane)
+constexpr int kBandCap = 512;        // the largest band list (kernel template BC: 256 or 512)
+constexpr float kHiQ = 0.55f;        // t_hi = the (kHiQ budget / tokens) upper Gaussian quantile
 constexpr int kSlot = kBandCap;      // band entries one CTA publishes per head (any range may hold the whole band)
 constexpr int kSub = 16;             // sub-bands of [t_lo, t_hi] (per-range token weights)
 constexpr int kH = 256;              // bins of a head's score histogram (the fallback of R25)
@@ -401,12 +402,13 @@ struct SelScratch2 {  // static shared memory of the band selection
 // blocks (bits: the head's words).
 // Returns (m, keep, T).  (Inlined: a noinline copy measured 0.6 us slower per
 // layer.)
+template <int BC>
 DSK_DEVICE int4 f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, int need,
                                            uint32_t* bits) {
   const int lane = threadIdx.x & 31;
   int m, keep;
   uint32_t T;
-  constexpr int J = kBandCap / 32;
+  constexpr int J = BC / 32;
   uint32_t k[J], sbr[J];
   int ix[J], ln[J];
   uint32_t valid = 0;
@@ -493,7 +495,7 @@ DSK_DEVICE int4 f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, i
         T = lo;
         uint32_t taken = 0;
 #pragma unroll 1
-        for (int it = 0; it < kBandCap; ++it) {
+        for (int it = 0; it < BC; ++it) {
           uint32_t mi = 0xffffffffu;
 #pragma unroll
           for (int r = 0; r < J; ++r)
@@ -557,7 +559,7 @@ DSK_DEVICE int4 f_band_select(uint2* band, int c, int wsb, const int32_t* sbs, i
   return make_int4(m, keep, (int)T, 0);
 }
 
-template <int G>
+template <int G, int BC>
 __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     const __grid_constant__ CUtensorMap tmD, const bf16* __restrict__ q,
     const int32_t* __restrict__ block_starts, const int32_t* __restrict__ n_blocks,
@@ -590,8 +592,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   float* ssl = reinterpret_cast<float*>(s_rows + kFNW * kFD);    // [G][per_cap] this range's scores
   // region A in phases 2-3: histogram | band entries | selection words
   uint32_t* hist = reinterpret_cast<uint32_t*>(smA);                         // [kFBkt] (slow path)
-  uint2* sband = reinterpret_cast<uint2*>(hist + kFBkt);                     // [G][kBandCap]
-  uint32_t* sbits = reinterpret_cast<uint32_t*>(sband + G * kBandCap);       // [G][nwords] selection words
+  uint2* sband = reinterpret_cast<uint2*>(hist + kFBkt);                     // [G][BC]
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(sband + G * BC);       // [G][nwords] selection words
 
   const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z, NS = gridDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -908,7 +910,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         const float mu = c1 / cn, var = fmaxf(c2 / cn - mu * mu, 0.f), sd = sqrtf(var);
         if (sd > 0.f) {
           tl = mu + sd * normcdfinvf(1.f - fminf(0.45f, 1.8f * pb));
-          th = mu + sd * normcdfinvf(1.f - 0.55f * pb);
+          th = mu + sd * normcdfinvf(1.f - kHiQ * pb);
         }
       }
       S2.tlo[g2] = tl;
@@ -1038,8 +1040,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         }
 #pragma unroll
         for (int e2 = 0; e2 < 16; ++e2) {
-          if (e0 + e2 < n0 && d0 + e0 + e2 < kBandCap) sband[g2 * kBandCap + d0 + e0 + e2] = ev0[e2];
-          if (e0 + e2 < n1 && d1 + e0 + e2 < kBandCap) sband[g2 * kBandCap + d1 + e0 + e2] = ev1[e2];
+          if (e0 + e2 < n0 && d0 + e0 + e2 < BC) sband[g2 * BC + d0 + e0 + e2] = ev0[e2];
+          if (e0 + e2 < n1 && d1 + e0 + e2 < BC) sband[g2 * BC + d1 + e0 + e2] = ev1[e2];
         }
       }
     }
@@ -1048,11 +1050,11 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     uint32_t T = 0;
     if (total <= budget) {
       all = 1;
-    } else if (W_hi >= budget || W_hi + W_bd < budget || over || nband > kBandCap || force) {
+    } else if (W_hi >= budget || W_hi + W_bd < budget || over || nband > BC || force) {
       fb = 1;  // the bounds did not bracket the marginal block: exact slow path below
     } else {
       if (tid == 0) fstampx(6);
-      const int4 r = f_band_select(sband + (size_t)g2 * kBandCap, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
+      const int4 r = f_band_select<BC>(sband + (size_t)g2 * BC, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
       if (tid == 0) fstampx(7);
       m = r.x;
       keep = r.y;
@@ -1078,7 +1080,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   // bin whose suffix weight reaches the budget: bins above j* are selected
   // (W_hi < budget by construction) and the blocks of bin j* are ranked by
   // f_band_select (sub-band = the fraction of the bin x 16, also monotone).
-  // A crossing bin of more than kBandCap blocks (massive ties) leaves the
+  // A crossing bin of more than BC blocks (massive ties) leaves the
   // head to the CTA-wide slow path below.
   uint32_t fbm = 0;  // heads to the fallback (the same in every CTA of the group)
 #pragma unroll
@@ -1088,7 +1090,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     // the heads' scores are copied into the free tail of region A (past the
     // selection scratch), as many heads per round as fit
     const int nb4 = (nb + 3) & ~3;
-    const size_t sel_b = ((size_t)kFBkt * 4 + (size_t)G * kBandCap * 8 + (size_t)G * nwords * 4 + 15) & ~(size_t)15;
+    const size_t sel_b = ((size_t)kFBkt * 4 + (size_t)G * BC * 8 + (size_t)G * nwords * 4 + 15) & ~(size_t)15;
     float* sx = reinterpret_cast<float*>(smA + sel_b);
     const int hpp = max(1, (int)((region_a - sel_b) / ((size_t)nb4 * 4)));
     uint32_t ph = 0;
@@ -1112,8 +1114,8 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         const int g2 = warp;
         const float* xs = sx + (size_t)(g2 - h0) * nb4;
         const float gmn = S2.gmn[g2], kb = S2.kb[g2];
-        uint2* lst = sband + (size_t)g2 * kBandCap;
-        uint32_t* h = reinterpret_cast<uint32_t*>(lst);  // [kH] histogram, then the band list (kBandCap x 8 B >= kH x 4 B)
+        uint2* lst = sband + (size_t)g2 * BC;
+        uint32_t* h = reinterpret_cast<uint32_t*>(lst);  // [kH] histogram, then the band list (BC x 8 B >= kH x 4 B)
         for (int j = lane; j < kH; j += 32) h[j] = 0u;
         if (lane < kSub) S2.wsub[g2 * kSub + lane] = 0;
         __syncwarp();
@@ -1178,7 +1180,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
               const int pos = nband + __popc(bb & lt);
               const int sb = min((int)((tb - (float)bn) * (float)kSub), kSub - 1);
               atomicAdd(&S2.wsub[g2 * kSub + sb], blen(sbs, i));
-              if (pos < kBandCap) lst[pos] = make_uint2(float_key(x4[u]), (uint32_t)i | ((uint32_t)sb << 24));
+              if (pos < BC) lst[pos] = make_uint2(float_key(x4[u]), (uint32_t)i | ((uint32_t)sb << 24));
             }
             nband += __popc(bb);
           }
@@ -1186,11 +1188,11 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
         __syncwarp();
         if (lane == 0 && g2 == 0) fstampx(2);
         if (lane == 0 && g2 < 4) fdbg(16 + g2, 1 + nband);
-        if (nband <= kBandCap) {
+        if (nband <= BC) {
           const int wsb = lane < kSub ? S2.wsub[g2 * kSub + lane] : 0;
           int m = -1, keep = 0;
           uint32_t T = 0;
-          const int4 r = f_band_select(lst, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
+          const int4 r = f_band_select<BC>(lst, nband, wsb, sbs, budget - W_hi, sbits + g2 * nwords);
           m = r.x;
           keep = r.y;
           T = (uint32_t)r.z;
@@ -1413,7 +1415,7 @@ size_t fused_scratch_bytes(int B, int Hq, int maxb) {
          fs_al((size_t)B * Hq * nwords * 4) + fs_al((size_t)kFMaxGroups * kMaxG * kSub * 4);
 }
 
-template <int G>
+template <int G, int BC>
 static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cudaStream_t st, const bf16* q,
                              const int32_t* bs, const int32_t* nb, const int32_t* pf, const bf16* Kp,
                              const bf16* Vp, int Hq, int Hkv, int maxb, int max_pages, int S, int Pshift,
@@ -1423,9 +1425,9 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
                              uint2* cls_band, uint32_t* gbits, int* counters, unsigned* gbar,
                              float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
                              int32_t* wl_count, WLEntry* wl, float* o, float* lse, int* err) {
-  allow_max_dyn_smem(k_decode_fused<G>);
-  if (occupancy_of(k_decode_fused<G>, kFNT, smem) < 1) return cudaErrorNotSupported;
-  launch_ex(k_decode_fused<G>, grid, dim3(kFNT), smem, st, 1, tm, q, bs, nb, pf, Kp, Vp, Hq, Hkv, maxb,
+  allow_max_dyn_smem(k_decode_fused<G, BC>);
+  if (occupancy_of(k_decode_fused<G, BC>, kFNT, smem) < 1) return cudaErrorNotSupported;
+  launch_ex(k_decode_fused<G, BC>, grid, dim3(kFNT), smem, st, 1, tm, q, bs, nb, pf, Kp, Vp, Hq, Hkv, maxb,
             max_pages, S, Pshift, budget, gqa_mode, budget_mode, cap, cap2, ent_cap, nwords, sstride, region_a,
             per_cap, sl2, scores, mom,
             cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep, wl_count, wl, o,
@@ -1458,7 +1460,12 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   // band entries, selection words (phases 2-3) | page rings, merge scratch (4)
   const int nd = attn_depth(kFD, kFNW, kD * 2, P);
   const size_t ring = (size_t)kFNW * nd * attn_stage_bytes(kD * 2, P);
-  const size_t sel_bytes = (size_t)kFBkt * 4 + (size_t)G * kBandCap * 8 + (size_t)G * nwords * 4;
+  // band list capacity: 256 unless the expected band -- (1.8 - 0.55) budget /
+  // tokens of the ~nb_hint / 1.25 blocks -- comes near it (large budgets),
+  // then 512 (the bigger per-lane rank arrays cost ~1 us per layer when not
+  // needed; budget 8192 at 128K: 57 -> 40 us per layer)
+  const int BC = (long long)budget * max(nb_hint, 1) > (long long)192 * max(S, 1) ? 512 : 256;
+  const size_t sel_bytes = (size_t)kFBkt * 4 + (size_t)G * BC * 8 + (size_t)G * nwords * 4;
   const int per_hint = (((max(nb_hint, 1) + NS - 1) / NS) + kFBox - 1) & ~(kFBox - 1);
   const int capA = max(kFBox, (int)(max(ring, sel_bytes) / (4 * kFSlabRowB)) / kFBox * kFBox);
   const int cap = min(per_hint, capA);
@@ -1496,7 +1503,7 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   const float sl2 = scale * 1.4426950408889634f;
   const dim3 grid(NS, Hkv, B);
 #define DSK_FU(GG)                                                                                        \
-  return run_fused<GG>(tm, grid, smem, st, static_cast<const bf16*>(q), bs, nb, pf,                       \
+  return (BC == 512 ? run_fused<GG, 512> : run_fused<GG, 256>)(tm, grid, smem, st, static_cast<const bf16*>(q), bs, nb, pf, \
                        static_cast<const bf16*>(Kp), static_cast<const bf16*>(Vp), Hq, Hkv, maxb, max_pages, \
                        S, Pshift, budget, gqa_mode, budget_mode, cap, cap2, ent_cap, nwords, sstride,       \
                        region_a, per_cap, sl2, scores,                                                      \
