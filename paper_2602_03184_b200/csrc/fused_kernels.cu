@@ -909,7 +909,11 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       if (cn > 1.f && pb < 0.25f) {
         const float mu = c1 / cn, var = fmaxf(c2 / cn - mu * mu, 0.f), sd = sqrtf(var);
         if (sd > 0.f) {
-          tl = mu + sd * normcdfinvf(1.f - fminf(0.45f, 1.8f * pb));
+          // lower bound: the 1.8 p upper quantile, or p + 40 blocks' worth when
+          // the budget is only a few dozen blocks (the far tail of block
+          // scores is thinner than the normal one; budget 1024 at 128K
+          // otherwise misses W(x >= t_lo) >= budget for some heads)
+          tl = mu + sd * normcdfinvf(1.f - fminf(0.45f, fmaxf(1.8f * pb, pb + 40.f / cn)));
           th = mu + sd * normcdfinvf(1.f - kHiQ * pb);
         }
       }

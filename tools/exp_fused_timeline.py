@@ -102,6 +102,11 @@ for k, name in XN.items():
     if len(col):
         r = (col - t0) / 1e3
         print(f"x{k} {name:22s} n={len(col):3d}  min {r.min():7.2f}  p50 {np.median(r):7.2f}  max {r.max():7.2f} us")
+# fast-path diagnostics of each group's split 0 (debug slots 32 + 4 g ..: band entries, overflow, W_hi, W_bd)
+if os.environ.get("DYNSPLIT_TL_DIAG"):
+    dg = tc[:, 32:48].astype(np.int64)
+    for c in range(0, int(used.sum()), max(1, int(used.sum()) // (B * Hkv))):
+        print("group CTA", c, [tuple(dg[c, 4 * g:4 * g + 4]) for g in range(4)], "budget", budget)
 # per-layer time from the graph
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
