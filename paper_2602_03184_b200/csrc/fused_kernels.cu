@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     const int32_t* __restrict__ page_first, const bf16* __restrict__ Kp, const bf16* __restrict__ Vp, int Hq,
     int Hkv, int maxb, int max_pages, int S, int Pshift, int budget, int gqa_mode, int budget_mode, int cap, int cap2,
     int ent_cap, int nwords,
-    int sstride, size_t region_a, int per_cap, float scale_log2, float* __restrict__ scores,
+    int sstride, size_t region_a, int per_cap, int local_sel, float scale_log2, float* __restrict__ scores,
     unsigned long long* __restrict__ mom, int4* __restrict__ cls_w, int* __restrict__ cls_sub, uint2* __restrict__ cls_band,
     uint32_t* __restrict__ gbits,
     int* __restrict__ counters, unsigned* __restrict__ gbar, float* __restrict__ part_o,
@@ -845,6 +845,9 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     // that sees the tag sees the value -- no flag and no second round trip
     const unsigned long long tag = (unsigned long long)s_target << 32;
     unsigned long long* mw = mom + (((size_t)bh * NS + split) * G + tid) * 4;
+    // local selection reads every CTA's scores right after barrier A: the
+    // CTA's score stores (ordered by the barrier above) are released first
+    if (local_sel) asm volatile("fence.acq_rel.gpu;" ::: "memory");
     st_relaxed_u64(mw + 0, tag | __float_as_uint(a));
     st_relaxed_u64(mw + 1, tag | __float_as_uint(c2));
     st_relaxed_u64(mw + 2, tag | __float_as_uint(mn));
@@ -894,6 +897,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       }
     }
     if (!done && lane == 0) raise_err(err, kErrSyncTimeout);
+    if (local_sel) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the peers' scores, for the local selection
     c1 = warp_sum(c1);
     c2 = warp_sum(c2);
     gmn = -warp_max(-gmn);
@@ -924,6 +928,17 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   }
   __syncthreads();
   fstamp(4);
+  if (local_sel) {
+    // Local selection (short sequences, few blocks per head): after barrier A
+    // every CTA selects every head itself from the full score rows -- the
+    // exact histogram path below, the same data and arithmetic in every CTA
+    // of the group -- instead of the distributed classification and barrier
+    // B (faster for short sequences over few splits, see the launcher).  Every CTA has
+    // read the epoch before publishing its moments: publish it now.
+    if (tid < G) S2.sel[tid] = make_int4(-1, 0, 0, total <= budget ? 1 : 2);
+    if (tid == 0 && split == 0)
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(gb), "r"(s_target) : "memory");
+  } else {
   if (tid == 0) fstampx(4);
   // classification of this CTA's range: warp w takes head g = w % G and the
   // range's words w / G, w / G + 8 / G, ...; lane l is block lo + 32 word + l.
@@ -1072,6 +1087,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       fdbg(4 * g2 + 2, W_hi);
       fdbg(4 * g2 + 3, W_bd);
     }
+  }
   }
   __syncthreads();
   fstamp(7);
@@ -1425,7 +1441,8 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
                              const bf16* Vp, int Hq, int Hkv, int maxb, int max_pages, int S, int Pshift,
                              int budget, int gqa_mode, int budget_mode, int cap, int cap2, int ent_cap, int nwords,
                              int sstride, size_t region_a,
-                             int per_cap, float sl2, float* scores, unsigned long long* mom, int4* cls_w, int* cls_sub,
+                             int per_cap, int local_sel, float sl2, float* scores, unsigned long long* mom,
+                             int4* cls_w, int* cls_sub,
                              uint2* cls_band, uint32_t* gbits, int* counters, unsigned* gbar,
                              float* part_o, float* part_lse, int32_t* n_sel, int32_t* marg, int32_t* keep,
                              int32_t* wl_count, WLEntry* wl, float* o, float* lse, int* err) {
@@ -1433,7 +1450,7 @@ static cudaError_t run_fused(const CUtensorMap& tm, dim3 grid, size_t smem, cuda
   if (occupancy_of(k_decode_fused<G, BC>, kFNT, smem) < 1) return cudaErrorNotSupported;
   launch_ex(k_decode_fused<G, BC>, grid, dim3(kFNT), smem, st, 1, tm, q, bs, nb, pf, Kp, Vp, Hq, Hkv, maxb,
             max_pages, S, Pshift, budget, gqa_mode, budget_mode, cap, cap2, ent_cap, nwords, sstride, region_a,
-            per_cap, sl2, scores, mom,
+            per_cap, local_sel, sl2, scores, mom,
             cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, keep, wl_count, wl, o,
             lse, err);
   g_fused_launches.fetch_add(1);
@@ -1480,6 +1497,12 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   const int cap2 = max(kFBox, (int)(region_a / (2 * 4 * kFSlabRowB)) / kFBox * kFBox);  // two staging buffers
   const int ent_cap = min(512, (max_pages + NS - 1) / NS + 1);
   const int per_cap = (((maxb + NS - 1) / NS) + kFBox - 1) & ~(kFBox - 1);  // >= any range
+  // local selection for short sequences split over few CTAs (measured: 32K,
+  // 8 sequences, 2 splits: 62.9 -> 57.3 us per layer; but 32K, one sequence,
+  // 18 splits: 20.4 -> 23.3, where the distributed fast path holds);
+  // DYNSPLIT_FUSED_LOCAL=0/1 overrides (A/B, tests)
+  int local_sel = (nb_hint <= 1300 && NS <= 2) ? 1 : 0;
+  if (const char* e = getenv("DYNSPLIT_FUSED_LOCAL")) local_sel = atoi(e) != 0;
   const size_t smem = 1024 + region_a + (size_t)2 * (nwords * 32 + 8) * 4 + (size_t)ent_cap * 16 +
                       (size_t)G * kD * 2 + (size_t)kFNW * kFD * 8 + (size_t)G * per_cap * 4;
   if (smem + 6144 > (size_t)max_smem_optin()) return cudaErrorNotSupported;
@@ -1510,7 +1533,7 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   return (BC == 512 ? run_fused<GG, 512> : run_fused<GG, 256>)(tm, grid, smem, st, static_cast<const bf16*>(q), bs, nb, pf, \
                        static_cast<const bf16*>(Kp), static_cast<const bf16*>(Vp), Hq, Hkv, maxb, max_pages, \
                        S, Pshift, budget, gqa_mode, budget_mode, cap, cap2, ent_cap, nwords, sstride,       \
-                       region_a, per_cap, sl2, scores,                                                      \
+                       region_a, per_cap, local_sel, sl2, scores,                                           \
                        mom, cls_w, cls_sub, cls_band, gbits, counters, gbar, part_o, part_lse, n_sel, marg, \
                        keep,                                                                                \
                        wl_count, wl, o, lse, err)

@@ -42,7 +42,7 @@ namespace cg = cooperative_groups;
 namespace dsk {
 
 constexpr int kRT = 512;   // threads of the reuse kernels
-constexpr int kFW = 4;     // warps per (persistent) fetch CTA
+constexpr int kFW = 8;     // warps per (persistent) fetch CTA (two CTAs per SM)
 
 // Bitmaps of one (b, KV head): bit p of `cur` = page p is in this step's
 // worklist; bit p of `prv` = page p sits in a cache slot.  Pages outside
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kRT) k_reuse_apply(
   }
 }
 
-// Persistent mover: one small CTA per SM; each warp walks the (b, KV head,
+// Persistent mover: two 8-warp CTAs per SM; each warp walks the (b, KV head,
 // fetch index) items with a grid stride and copies a page's valid rows of K
 // and V, host -> cache slot (dense: page p -> slot p for p < n_pages[b]),
 // 8 16-byte loads per lane in flight before the stores.
@@ -332,7 +332,7 @@ cudaError_t launch_fetch_pages(int dtype, const void* Kh, const void* Vh, const 
                                const int32_t* n_pages, const int32_t* fetch, const int32_t* fetch_count,
                                int dense, int B, int Hkv, int max_pages, int n_slots, int P, void* Kc, void* Vc,
                                cudaStream_t st) {
-  const dim3 grid(num_sms());
+  const dim3 grid(2 * num_sms());  // 2 x 8 warps per SM: enough PCIe reads in flight across NUMA distances
   const auto* kh = static_cast<const unsigned char*>(Kh);
   const auto* vh = static_cast<const unsigned char*>(Vh);
   auto* kc = static_cast<unsigned char*>(Kc);

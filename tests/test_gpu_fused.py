@@ -324,3 +324,32 @@ def test_variants_unsupported_outside_the_fused_layer(D):
                            static_w10=G.T7_W10, Hq=Hq)
     with pytest.raises(D.DynsplitError):
         D.select(t(q[None], torch.bfloat16), layer, 300)
+
+
+@pytest.mark.parametrize("B,S,Hq,Hkv,budget,kind", [
+    (1, 20000, 32, 8, 1024, "cont"),
+    (8, 3000, 32, 8, 300, "cont"),
+    (3, 5000, 32, 8, 600, "int"),
+    (1, 6000, 8, 8, 300, "hightail"),
+    (2, 3000, 32, 8, 5000, "cont"),      # all fit
+])
+def test_fused_local_selection(D, monkeypatch, B, S, Hq, Hkv, budget, kind):
+    """The local-selection mode (every CTA selects every head from the full
+    score rows right after barrier A; the default for short sequences over
+    few splits), forced on: the same selections, worklists, o and lse as the
+    three kernels, and the oracle's."""
+    monkeypatch.setenv("DYNSPLIT_FUSED_LOCAL", "1")
+    d = 128
+    toks = np.stack([G.tokens(3600 + b, S) for b in range(B)])
+    starts = [O.segment(toks[b], G.T7_IDS, G.T7_W10, 32, 14) for b in range(B)]
+    gen = G.decode_qkv_integer if kind == "int" else G.decode_qkv
+    qs, Ks, Vs = zip(*[gen(3700 + b, S, Hq, Hkv, d) for b in range(B)])
+    q, K, V = np.stack(qs), np.stack(Ks), np.stack(Vs)
+    if kind == "hightail":
+        K[:, S - 600:] *= 4.0
+    if kind != "int":
+        q = H.certify_queries(3700, q, K, starts, budget, "bf16")
+    layer = build(D, toks, K, V, Hq)
+    a, b = run_both(D, t(q, torch.bfloat16), layer, budget)
+    assert_same(D, a, b, D.make_shape(B, S, Hq, Hkv, d), Hq // Hkv)
+    check_oracle(a[2], a[0], a[1], H.oracle_decode(q, K, V, starts, budget), B, Hq)
