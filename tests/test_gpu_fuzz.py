@@ -18,20 +18,24 @@ pytestmark = pytest.mark.gpu
 LAYOUTS = [(8, 8), (16, 8), (32, 8), (16, 2), (32, 4), (8, 1), (64, 8)]
 
 
-def _cases(n=14):
-    r = G.rng(424242, 1)
+def _cases(n=14, seed=424242, long=False):
+    r = G.rng(seed, 1)
     out = []
     for i in range(n):
         Hq, Hkv = LAYOUTS[int(r.integers(len(LAYOUTS)))]
         B = int(r.integers(1, 4))
         S = int(r.choice([int(r.integers(1, 64)), int(r.integers(64, 4000)), int(r.integers(4000, 24000))]))
+        if long:
+            S = int(r.integers(24000, 140000))
+            B = int(r.integers(1, 3))
         budget = int(r.choice([1, int(r.integers(2, 64)), int(r.integers(64, 2048)), S + 7]))
         P = int(r.choice([8, 16, 32]))
         out.append((i, B, S, Hq, Hkv, budget, P))
     return out
 
 
-@pytest.mark.parametrize("case", _cases(), ids=lambda c: "c%d_B%d_S%d_H%d-%d_b%d_P%d" % c)
+@pytest.mark.parametrize("case", _cases() + [(100 + c[0],) + c[1:] for c in _cases(6, 777, long=True)],
+                         ids=lambda c: "c%d_B%d_S%d_H%d-%d_b%d_P%d" % c)
 def test_fuzz_fused_vs_three_kernels_vs_oracle(D, case):
     i, B, S, Hq, Hkv, budget, P = case
     d = 128
