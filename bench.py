@@ -813,7 +813,21 @@ def run_seqsplit(args, world, rank, local):
     cur = torch.cuda.current_stream(dev)
     clk = ClockSampler(local)
     clk.__enter__()
-    ms, per, _ = time_graph(torch, step, args.steps, args.warmup, cur, dev, world, barrier)
+    if os.environ.get("DYNSPLIT_BENCH_ONE_GPU") == "1":
+        # control-flow check only (gloo stages CUDA collectives through the
+        # host, which a CUDA graph cannot capture): eager steps, no timing claim
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for _ in range(args.steps):
+            step()
+        e1.record(cur)
+        barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:
+        ms, per, _ = time_graph(torch, step, args.steps, args.warmup, cur, dev, world, barrier)
     clk.__exit__(None, None, None)
     vals = torch.tensor([ms], dtype=torch.float64, device=dev)
     tot = torch.tensor([float(rank_bytes)], dtype=torch.float64, device=dev)
@@ -851,10 +865,18 @@ def main():
     from paper_2602_03184_b200 import dynsplit as D
     from synth import generators as G
 
+    # DYNSPLIT_BENCH_ONE_GPU=1 (control-flow checks of the multi-rank path on a
+    # one-GPU box only; never a timing): every rank on cuda:0, gloo collectives
+    one_gpu = os.environ.get("DYNSPLIT_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     D.lib()
     if args.mode == "seqsplit":
         return run_seqsplit(args, world, rank, local)
