@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   __shared__ FusedScratch F;
   __shared__ SelScratch2<G> S2;
   __shared__ float4 red_m[kFNW][8];
-  __shared__ unsigned s_target;
+  __shared__ unsigned s_target, s_pref;
   __shared__ int s_last;
 
   const uint32_t raw_s = smem_u32(smem_raw);
@@ -699,7 +699,11 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   fstamp(1);
   pdl_trigger();
   pdl_wait();  // q, the scores/worklist buffers and the outputs belong to the step
-  if (tid == 0) s_target = ld_relaxed_gpu_u(gbar + (size_t)bh * kGbarWords) + 1u;
+  if (tid == 0) {
+    s_target = ld_relaxed_gpu_u(gbar + (size_t)bh * kGbarWords) + 1u;
+    // word 1: launches left to run the local selection after a fast-path miss
+    s_pref = ld_relaxed_gpu_u(gbar + (size_t)bh * kGbarWords + 1);
+  }
   fstamp(2);
   if (skip) {
     if (tid == 0 && split == 0) {
@@ -728,6 +732,10 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     reinterpret_cast<uint4*>(s_q)[tid] =
         __ldca(reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD) + tid);
   __syncthreads();
+  // local selection: by the launcher's rule, or -- adaptively -- for a few
+  // launches after one where the moment bounds missed for a head of this
+  // group (the same word for every CTA of the group: a uniform choice)
+  const bool lsel = local_sel || (s_pref != 0u && !force);
   fstamp(14);
   {
     const int g = lane >> 2, t = lane & 3;
@@ -847,7 +855,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     unsigned long long* mw = mom + (((size_t)bh * NS + split) * G + tid) * 4;
     // local selection reads every CTA's scores right after barrier A: the
     // CTA's score stores (ordered by the barrier above) are released first
-    if (local_sel) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (lsel) asm volatile("fence.acq_rel.gpu;" ::: "memory");
     st_relaxed_u64(mw + 0, tag | __float_as_uint(a));
     st_relaxed_u64(mw + 1, tag | __float_as_uint(c2));
     st_relaxed_u64(mw + 2, tag | __float_as_uint(mn));
@@ -897,7 +905,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
       }
     }
     if (!done && lane == 0) raise_err(err, kErrSyncTimeout);
-    if (local_sel) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the peers' scores, for the local selection
+    if (lsel) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the peers' scores, for the local selection
     c1 = warp_sum(c1);
     c2 = warp_sum(c2);
     gmn = -warp_max(-gmn);
@@ -928,7 +936,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
   }
   __syncthreads();
   fstamp(4);
-  if (local_sel) {
+  if (lsel) {
     // Local selection (short sequences, few blocks per head): after barrier A
     // every CTA selects every head itself from the full score rows -- the
     // exact histogram path below, the same data and arithmetic in every CTA
@@ -1106,6 +1114,10 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
 #pragma unroll
   for (int g2 = 0; g2 < G; ++g2) fbm |= (uint32_t)((S2.sel[g2].w >> 1) & 1) << g2;
   if (force & 2) fbm = 0;
+  if (tid == 0 && split == 0 && !local_sel) {  // the adaptive choice for the next launch of this group
+    const unsigned nxt = lsel ? (s_pref > 0u ? s_pref - 1u : 0u) : (fbm ? 8u : 0u);
+    if (nxt != s_pref) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(gbar + (size_t)bh * kGbarWords + 1), "r"(nxt) : "memory");
+  }
   if (fbm) {
     // the heads' scores are copied into the free tail of region A (past the
     // selection scratch), as many heads per round as fit
