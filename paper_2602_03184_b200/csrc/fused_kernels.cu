@@ -732,10 +732,10 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
     reinterpret_cast<uint4*>(s_q)[tid] =
         __ldca(reinterpret_cast<const uint4*>(q + ((size_t)b * Hq + hk * G) * kD) + tid);
   __syncthreads();
-  // local selection: by the launcher's rule, or -- adaptively -- for a few
-  // launches after one where the moment bounds missed for a head of this
-  // group (the same word for every CTA of the group: a uniform choice)
-  const bool lsel = local_sel || (s_pref != 0u && !force);
+  // local selection: by the launcher's rule (bit 0), or -- adaptively (bit
+  // 1) -- for a few launches after one where the moment bounds missed for a
+  // head of this group (the same word for every CTA of the group: uniform)
+  const bool lsel = (local_sel & 1) || ((local_sel & 2) && s_pref != 0u && !force);
   fstamp(14);
   {
     const int g = lane >> 2, t = lane & 3;
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__(kFNT, 1) k_decode_fused(
 #pragma unroll
   for (int g2 = 0; g2 < G; ++g2) fbm |= (uint32_t)((S2.sel[g2].w >> 1) & 1) << g2;
   if (force & 2) fbm = 0;
-  if (tid == 0 && split == 0 && !local_sel) {  // the adaptive choice for the next launch of this group
+  if (tid == 0 && split == 0 && local_sel == 2) {  // the adaptive choice for the next launch of this group
     const unsigned nxt = lsel ? (s_pref > 0u ? s_pref - 1u : 0u) : (fbm ? 8u : 0u);
     if (nxt != s_pref) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(gbar + (size_t)bh * kGbarWords + 1), "r"(nxt) : "memory");
   }
@@ -1513,8 +1513,11 @@ cudaError_t launch_decode_fused(int dtype, int digest_mode, int G, const void* q
   // 8 sequences, 2 splits: 62.9 -> 57.3 us per layer; but 32K, one sequence,
   // 18 splits: 20.4 -> 23.3, where the distributed fast path holds);
   // DYNSPLIT_FUSED_LOCAL=0/1 overrides (A/B, tests)
-  int local_sel = (nb_hint <= 1300 && NS <= 2) ? 1 : 0;
-  if (const char* e = getenv("DYNSPLIT_FUSED_LOCAL")) local_sel = atoi(e) != 0;
+  // bit 0: always; bit 1: adaptively after a miss, for mid-sized sequences
+  // only (<= ~2600 blocks: at 128K the local path costs more than a rare
+  // miss -- 128K budget 1K: 22.8 vs 26.6 us per layer over 32 layers)
+  int local_sel = (nb_hint <= 1300 && NS <= 2) ? 1 : (nb_hint <= 2600 ? 2 : 0);
+  if (const char* e = getenv("DYNSPLIT_FUSED_LOCAL")) local_sel = atoi(e) != 0 ? 1 : 0;
   const size_t smem = 1024 + region_a + (size_t)2 * (nwords * 32 + 8) * 4 + (size_t)ent_cap * 16 +
                       (size_t)G * kD * 2 + (size_t)kFNW * kFD * 8 + (size_t)G * per_cap * 4;
   if (smem + 6144 > (size_t)max_smem_optin()) return cudaErrorNotSupported;
