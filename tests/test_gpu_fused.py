@@ -353,3 +353,46 @@ def test_fused_local_selection(D, monkeypatch, B, S, Hq, Hkv, budget, kind):
     a, b = run_both(D, t(q, torch.bfloat16), layer, budget)
     assert_same(D, a, b, D.make_shape(B, S, Hq, Hkv, d), Hq // Hkv)
     check_oracle(a[2], a[0], a[1], H.oracle_decode(q, K, V, starts, budget), B, Hq)
+
+
+def test_fused_adaptive_local_selection(D):
+    """After a launch whose moment bounds missed (forced here through the
+    test hook), the group's next launches select locally (a countdown in the
+    group's barrier word 1, sequences of <= ~2600 blocks): the countdown is
+    set to 8 and then decrements, and every launch equals the three-kernel
+    path."""
+    lib = D.lib()
+    B, S, Hq, Hkv, d, budget = 1, 20000, 32, 8, 128, 1024
+    toks = G.tokens(3900, S)[None]
+    q, K, V = G.decode_qkv(3901, S, Hq, Hkv, d)
+    starts = [O.segment(toks[0], G.T7_IDS, G.T7_W10, 32, 14)]
+    q = H.certify_queries(3901, q[None], K[None], starts, budget, "bf16")
+    layer = build(D, toks, K[None], V[None], Hq)
+    qt = t(q, torch.bfloat16)
+    shape = D.make_shape(B, S, Hq, Hkv, d)
+    ws = D.workspace(D.workspace_bytes(D.OP_DECODE_LAYER, shape, layer.cfg, budget), DEV, "adaptive_test")
+    ws.zero_()
+    # the group barrier words: workspace header (256 B), then the decode
+    # body's counters (65536 int32), the barriers in their upper half,
+    # 8 + 64 words per (b, KV head)
+    words = ws[256:256 + 65536 * 4].view(torch.int32)[32768:]
+
+    def state():
+        torch.cuda.synchronize()
+        return [int(words[bh * 72 + 1]) for bh in range(B * Hkv)]
+
+    ref_o, ref_l, _ = D.decode_layer(qt, layer, budget, ws=ws)
+    assert state() == [0] * (B * Hkv)
+    lib.dynsplit_debug_fused_force(1)          # every head through the exact fallback: a "miss"
+    try:
+        o1, l1, _ = D.decode_layer(qt, layer, budget, ws=ws)
+    finally:
+        lib.dynsplit_debug_fused_force(0)
+    assert state() == [8] * (B * Hkv)
+    for k in range(3):                          # local selection, counting down
+        o2, l2, _ = D.decode_layer(qt, layer, budget, ws=ws)
+        assert state() == [7 - k] * (B * Hkv)
+        assert torch.equal(o2, ref_o) and torch.equal(l2, ref_l)
+    assert torch.equal(o1, ref_o) and torch.equal(l1, ref_l)
+    res = H.oracle_decode(q, K[None], V[None], starts, budget)
+    assert np.all(H.row_rel_err(o2[0].cpu().numpy(), res[0]["o"]) <= ATT_TOL)
