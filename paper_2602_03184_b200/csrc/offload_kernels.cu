@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(kRT) k_reuse_apply(
           slot_page[bh * n_slots + s] = p;
           fetch[(bh * n_slots + fi) * 2] = p;
           fetch[(bh * n_slots + fi) * 2 + 1] = s;
+        } else {
+          mp[p] = n_slots;  // no slot left (DEVERR_PAGE_CAPACITY): the attention skips the page
         }
       }
   }
