@@ -693,12 +693,14 @@ class OffloadedLayer:
         self.slot_page.fill_(-1)
 
 
-def offload_layer(layer: PagedLayer, budget: int, Hq: int, n_slots: Optional[int] = None,
+def offload_layer(layer: PagedLayer, budget: int, Hq: Optional[int] = None, n_slots: Optional[int] = None,
                   keep_device: bool = False) -> OffloadedLayer:
     """Move a built layer's pages to pinned host memory and allocate its page
     cache (n_slots defaults to dynsplit_cache_slots: always enough for one
     step).  keep_device=False drops the device copies of Kp / Vp."""
     s = layer.shape
+    if Hq is None:
+        Hq = s.Hq
     shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
     if n_slots is None:
         n_slots = cache_slots(shape, layer.cfg, budget)
