@@ -726,9 +726,11 @@ def _host_ptr(t: torch.Tensor):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def reuse_plan(off: OffloadedLayer, worklist, Hq: int, truncate: bool = True, reuse: bool = True, ws=None):
+def reuse_plan(off: OffloadedLayer, worklist, Hq: Optional[int] = None, truncate: bool = True, reuse: bool = True,
+               ws=None):
     """dynsplit_reuse_plan: Steps 1 and 3 against the cache's previous pages."""
     s = off.layer.shape
+    Hq = Hq or s.Hq
     shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
     if ws is None:
         ws = workspace(workspace_bytes(OP_REUSE, shape, off.layer.cfg), worklist.device, "reuse")
@@ -738,9 +740,10 @@ def reuse_plan(off: OffloadedLayer, worklist, Hq: int, truncate: bool = True, re
            "reuse_plan")
 
 
-def fetch_pages(off: OffloadedLayer, Hq: int, dense: bool = False) -> None:
+def fetch_pages(off: OffloadedLayer, Hq: Optional[int] = None, dense: bool = False) -> None:
     """dynsplit_fetch_pages: move the planned pages (dense: every page) host -> cache."""
     s = off.layer.shape
+    Hq = Hq or s.Hq
     shape = make_shape(s.B, s.S, Hq, s.Hkv, s.d, 1, s.kv_dtype)
     c = off.c()
     _check(lib().dynsplit_fetch_pages(ctypes.byref(shape), ctypes.byref(off.layer.cfg), _host_ptr(off.Kh),
